@@ -1,0 +1,208 @@
+/*
+ * libb200link -- C ABI of the B200-native pipeline-parallel serving hot path.
+ *
+ * The reference (`pipelink`, /root/reference/pkg/src/pipelink) has NO FFI: its
+ * two hot-path subsystems are virtual.  Each entry point below names the
+ * reference call site it replaces:
+ *
+ *   compute   engine.py:376-388  PipelineEngine._try_start_compute ->
+ *             compute_time(stage.profile, phase, mb.batched_tokens) (engine.py:384,
+ *             profiles.py:95-121).  The latency-table lookup becomes a real
+ *             decoder forward of the stage's layer range: pl_stage_forward, built
+ *             from the kernel entry points pl_embed ... pl_lmhead_argmax.
+ *   transport engine.py:347-372 / 546-576 (_link_emit_next -> transmission_ns,
+ *             transport.py:199-200) and wire.py:124-149 (SocketLinkSender.run
+ *             `sendall` of one LinkQueue chunk).  Each LinkQueue chunk becomes
+ *             one NCCL send/recv pair: pl_p2p_send / pl_p2p_recv.
+ *   throttle  transport.py:199-200 + engine.py:552 (`round(bytes*1e9/bw)` +
+ *             latency) reproduced in wall time on the GPU: pl_gate_until_ns.
+ *
+ * Conventions: plain C types only; every pointer argument is a device pointer
+ * unless named *_host; `stream` is a cudaStream_t passed as void*.  Kernel
+ * entry points never allocate and never synchronize.  Every function except
+ * pl_abi_version / pl_last_error returns a pl_status; on failure
+ * pl_last_error() holds a thread-local message.  The Python wrapper maps
+ * PL_ERR_CONFIG -> pipelink.errors.ConfigError, PL_ERR_PROTOCOL ->
+ * ProtocolError, anything else -> PipelinkError (errors.py:4-39).
+ */
+#ifndef B200LINK_H_
+#define B200LINK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PL_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PL_API __attribute__((visibility("default")))
+#else
+#define PL_API
+#endif
+
+typedef enum pl_status {
+  PL_OK = 0,
+  PL_ERR_CONFIG = 1,   /* bad shape, alignment or argument  -> ConfigError   */
+  PL_ERR_PROTOCOL = 2, /* transport / NCCL failure           -> ProtocolError */
+  PL_ERR_CUDA = 3,     /* CUDA runtime / launch failure      -> PipelinkError */
+} pl_status;
+
+/* GEMM epilogues (see pl_gemm). */
+typedef enum pl_epilogue {
+  PL_EPI_NONE = 0,     /* C = bf16(acc)                                      */
+  PL_EPI_BIAS = 1,     /* C = bf16(acc + bias[n])                            */
+  PL_EPI_RESIDUAL = 2, /* C = bf16(bf16(acc) + residual[t, n]) (may alias C) */
+  PL_EPI_SWIGLU = 3,   /* W rows in 64-row blocks [gate|up]; C[t, N/2]       */
+  PL_EPI_ARGMAX = 4,   /* argmax over n of acc, int64 per row                */
+} pl_epilogue;
+
+PL_API int32_t pl_abi_version(void);
+PL_API const char* pl_last_error(void);
+PL_API int32_t pl_device_sm_count(int32_t device);
+
+/* ---------------------------------------------------------------- init --- */
+
+/* dst[i] = bf16(float(hash(seed, tensor_id, i) - 2^23) * (scale * 2^-23) + offset):
+ * the counter-based synthetic weight init shared bit-for-bit with oracle/hashinit.py. */
+PL_API int32_t pl_fill_hash_bf16(void* dst, int64_t n, uint32_t seed, uint32_t tensor_id, float scale,
+                          float offset, void* stream);
+
+/* ------------------------------------------------------- decoder kernels - */
+
+/* out[t] = table[ids[t]]                          (ids != NULL: prompt tokens)
+ * out[t] = table[last_token[req_slot[t]]]          (ids == NULL: decode feedback) */
+PL_API int32_t pl_embed(const int64_t* ids, const int32_t* req_slot, const int64_t* last_token,
+                 const void* table, int64_t vocab, int64_t T, int32_t d, void* out, void* stream);
+
+/* out[r] = rmsnorm(x[row_idx ? row_idx[r] : r]) * w, fp32 math, HF rounding points
+ * (modeling_llama.py:62-67). */
+PL_API int32_t pl_rmsnorm(const void* x, int64_t ldx, const int32_t* row_idx, const void* w, float eps,
+                   int64_t rows, int32_t d, void* out, int64_t ldo, void* stream);
+
+/* C[T, N] = epilogue(X[T, K] . W[N, K]^T) on tcgen05 tensor cores.  workspace:
+ * pl_gemm_workspace_bytes(T, N, K, epilogue) bytes (split-K partials / argmax). */
+PL_API int64_t pl_gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t epilogue);
+PL_API int32_t pl_gemm(const void* X, int64_t ldx, const void* W, int64_t ldw, const void* bias, void* C,
+                int64_t ldc, const void* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,
+                int32_t epilogue, void* workspace, int64_t workspace_bytes, int64_t* argmax_out,
+                void* stream);
+
+/* Neox RoPE on the q and k heads of qkv[T, (Hq+2Hkv)*hd] in place, then k and v
+ * written to the paged caches [num_blocks, Hkv, block_size, hd] at slot[t]
+ * (slot < 0 skips the write).  cos_sin: bf16 [max_pos, hd] = [cos | sin]. */
+PL_API int32_t pl_rope_kv_write(void* qkv, int64_t ldqkv, const int32_t* pos, const int32_t* slot,
+                         const void* cos_sin, int32_t max_pos, void* k_cache, void* v_cache,
+                         int32_t block_size, int64_t T, int32_t Hq, int32_t Hkv, int32_t hd,
+                         void* stream);
+
+/* Causal varlen GQA attention over the prompt rows of qkv (no prior context;
+ * prefill is never split, engine.py:215-223).  out[T, Hq*hd]. */
+PL_API int32_t pl_attn_prefill(const void* qkv, int64_t ldqkv, const int32_t* cu_seqlens, int32_t R,
+                        int32_t max_seqlen, int32_t Hq, int32_t Hkv, int32_t hd, float scale,
+                        void* out, int64_t ldo, void* stream);
+
+/* One query token per request over its paged KV (ctx_len[r] tokens incl. the
+ * current one).  q rows: [R, Hq*hd] with leading dim ldq. */
+PL_API int64_t pl_attn_decode_workspace_bytes(int32_t R, int32_t Hq, int32_t max_ctx, int32_t hd);
+PL_API int32_t pl_attn_decode(const void* q, int64_t ldq, const void* k_cache, const void* v_cache,
+                       int32_t block_size, const int32_t* block_table, int32_t max_blocks,
+                       const int32_t* ctx_len, int32_t R, int32_t max_ctx, int32_t Hq, int32_t Hkv,
+                       int32_t hd, float scale, void* out, int64_t ldo, void* workspace,
+                       int64_t workspace_bytes, void* stream);
+
+/* Greedy next token: out_ids[r] = argmax_v h[r] . W[v]  (fp32 logits, lowest
+ * index on ties).  Replaces the 8-byte token feedback size of engine.py:409. */
+PL_API int64_t pl_lmhead_workspace_bytes(int32_t R, int64_t vocab);
+PL_API int32_t pl_lmhead_argmax(const void* h, int64_t ldh, const void* W, int64_t vocab, int32_t d,
+                         int32_t R, int64_t* out_ids, void* workspace, int64_t workspace_bytes,
+                         void* stream);
+
+/* Return hop landing on the head stage: last_token[req_slot[r]] = ids[r] and
+ * gen_tokens[req_slot[r] * gen_stride + out_pos[r]] = ids[r]. */
+PL_API int32_t pl_token_scatter(const int64_t* ids, const int32_t* req_slot, const int32_t* out_pos,
+                         int32_t R, int64_t* last_token, int64_t* gen_tokens, int32_t gen_stride,
+                         void* stream);
+
+/* --------------------------------------------------------- stage runtime - */
+
+typedef struct pl_layer_weights {
+  const void* attn_norm; /* bf16 [d]                                   */
+  const void* w_qkv;     /* bf16 [(Hq+2Hkv)*hd, d]                     */
+  const void* b_qkv;     /* bf16 [(Hq+2Hkv)*hd] or NULL (Qwen2 bias)   */
+  const void* w_o;       /* bf16 [d, Hq*hd]                            */
+  const void* mlp_norm;  /* bf16 [d]                                   */
+  const void* w_gate_up; /* bf16 [2*ffn, d], 64-row blocks [gate|up]   */
+  const void* w_down;    /* bf16 [d, ffn]                              */
+  void* k_cache;         /* bf16 [num_blocks, Hkv, block_size, hd]     */
+  void* v_cache;
+} pl_layer_weights;
+
+typedef struct pl_stage_config {
+  int32_t d, Hq, Hkv, hd, ffn;
+  int32_t num_layers;
+  int64_t vocab;
+  float eps;
+  int32_t block_size, max_blocks_per_req, max_pos;
+  int32_t is_first, is_last;
+  int32_t max_tokens; /* activation rows the workspace is sized for */
+  int32_t max_reqs;   /* requests per micro-batch                   */
+  int32_t max_ctx;    /* longest context (tokens)                   */
+  const void* embed;      /* bf16 [vocab, d]  (first stage)  */
+  const void* final_norm; /* bf16 [d]         (last stage)   */
+  const void* lm_head;    /* bf16 [vocab, d]  (last stage)   */
+  const void* cos_sin;    /* bf16 [max_pos, hd]              */
+} pl_stage_config;
+
+/* Packed int32 micro-batch metadata (one H2D copy per micro-batch):
+ *   pos[T] | slot[T] | req_slot[T] | cu_seqlens[R+1] | ctx_len[R] | last_idx[R]
+ *   | block_table[R * max_blocks_per_req]                                    */
+typedef struct pl_microbatch {
+  int32_t T, R;
+  int32_t phase;      /* 0 prefill, 1 decode */
+  int32_t max_seqlen; /* prefill: longest prompt in the micro-batch */
+  int32_t max_ctx;    /* decode: longest context in the micro-batch */
+  const int32_t* meta;
+  const int64_t* token_ids;  /* first stage, prefill: prompt ids [T]          */
+  const int64_t* last_token; /* first stage, decode: per-slot feedback table  */
+  void* hidden;              /* bf16 [T, d] residual stream: input (non-first),
+                                output (non-last), updated in place           */
+  int64_t* out_ids;          /* last stage: [R] greedy tokens                 */
+} pl_microbatch;
+
+PL_API int64_t pl_stage_workspace_bytes(const pl_stage_config* cfg);
+PL_API int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* layers,
+                        void* workspace, int64_t workspace_bytes, void** handle);
+PL_API int32_t pl_stage_forward(void* handle, const pl_microbatch* mb, void* stream);
+PL_API int32_t pl_stage_destroy(void* handle);
+
+/* Live kernel timing for bench.py: CUDA events around the kernel groups of one
+ * layer (layer < 0 disables).  pl_stage_probe_read returns, per recorded
+ * forward, out_ms[5] = {qkv gemm, rope+attention, o gemm, gate_up gemm, down
+ * gemm} and out_meta[2] = {phase, T}; the stream must be synchronized first. */
+PL_API int32_t pl_stage_probe(void* handle, int32_t layer);
+PL_API int32_t pl_stage_probe_read(void* handle, float* out_ms_host, int32_t* out_meta_host, int32_t cap,
+                            int32_t* n_host);
+
+/* ------------------------------------------------------------ transport --- */
+
+/* NCCL 2.28 P2P over NVLink.  One communicator per directed stage hop. */
+PL_API int32_t pl_nccl_version(void);
+PL_API int32_t pl_nccl_unique_id(uint8_t* id_host, int32_t len); /* len >= 128 */
+PL_API int32_t pl_comm_init_rank(const uint8_t* id_host, int32_t nranks, int32_t rank, void** comm);
+PL_API int32_t pl_comm_destroy(void* comm);
+PL_API int32_t pl_p2p_send(void* comm, const void* buf, int64_t bytes, int32_t peer, void* stream);
+PL_API int32_t pl_p2p_recv(void* comm, void* buf, int64_t bytes, int32_t peer, void* stream);
+
+/* Link-throttle gate: block `stream` until %globaltimer >= *t0 + offset_ns. */
+PL_API int32_t pl_record_globaltimer(uint64_t* dst, void* stream);
+PL_API int32_t pl_gate_until_ns(const uint64_t* t0, uint64_t offset_ns, void* stream);
+
+/* Host<->device plumbing without a Python round trip. */
+PL_API int32_t pl_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200LINK_H_ */

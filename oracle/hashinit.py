@@ -1,0 +1,72 @@
+"""ORACLE (test infrastructure only): counter-based synthetic initialisation.
+
+Independent numpy restatement of the generator behind ``pl_fill_hash_bf16``
+(paper_2507_05043_b200/csrc/kernels.cu) so the CPU oracle and the GPU build
+start from bit-identical bf16 weights and prompt token ids.  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline leg import this.
+
+    key  = mix(seed * 0x9E3779B9 + tensor_id * 0x85EBCA6B + 0x632BE5AB)
+    key2 = mix(key ^ 0x5bd1e995)
+    h    = mix(mix(i + key) ^ key2)                       (uint32 wrap-around)
+    w[i] = bf16_rne( f32(int(h >> 8) - 2^23) * f32(scale * 2^-23) + f32(offset) )
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+M32 = np.uint32(0xFFFFFFFF)
+
+
+def _mix(x: np.ndarray) -> np.ndarray:
+    x = x.astype(np.uint32, copy=True)
+    with np.errstate(over="ignore"):
+        x ^= x >> np.uint32(16)
+        x *= np.uint32(0x7FEB352D)
+        x ^= x >> np.uint32(15)
+        x *= np.uint32(0x846CA68B)
+        x ^= x >> np.uint32(16)
+    return x
+
+
+def _mix_scalar(x: int) -> int:
+    return int(_mix(np.array([x & 0xFFFFFFFF], dtype=np.uint32))[0])
+
+
+def keys(seed: int, tensor_id: int) -> tuple[int, int]:
+    key = _mix_scalar((seed * 0x9E3779B9 + tensor_id * 0x85EBCA6B + 0x632BE5AB) & 0xFFFFFFFF)
+    key2 = _mix_scalar(key ^ 0x5BD1E995)
+    return key, key2
+
+
+def hash_u32(n: int, seed: int, tensor_id: int, start: int = 0) -> np.ndarray:
+    key, key2 = keys(seed, tensor_id)
+    i = np.arange(start, start + n, dtype=np.uint64).astype(np.uint32)
+    with np.errstate(over="ignore"):
+        h = _mix((i + np.uint32(key)).astype(np.uint32)) ^ np.uint32(key2)
+    return _mix(h)
+
+
+def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16, returned as uint16 bit patterns."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    rounding = ((u >> 16) & 1) + 0x7FFF
+    return ((u + rounding) >> 16).astype(np.uint16)
+
+
+def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def hash_bf16_bits(n: int, seed: int, tensor_id: int, scale: float, offset: float = 0.0,
+                   start: int = 0) -> np.ndarray:
+    h = hash_u32(n, seed, tensor_id, start)
+    v = ((h >> np.uint32(8)).astype(np.int64) - 8388608).astype(np.float32)
+    mult = np.float32(scale) * np.float32(2.0 ** -23)
+    w = (v * mult).astype(np.float32) + np.float32(offset)
+    return f32_to_bf16_bits(w.astype(np.float32))
+
+
+def hash_tokens(n: int, seed: int, tensor_id: int, vocab: int, start: int = 0) -> np.ndarray:
+    """Prompt token ids: hash mod vocab (int64)."""
+    return (hash_u32(n, seed, tensor_id, start).astype(np.int64) % vocab).astype(np.int64)

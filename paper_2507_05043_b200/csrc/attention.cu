@@ -1,0 +1,507 @@
+// GQA attention for the decoder stages (hd = 128).
+//
+// prefill: causal varlen self-attention over the prompt rows of the fused qkv
+//   buffer.  The reference admits a prompt whole into one micro-batch and never
+//   splits compute (engine.py:215-223), so a prefill has no prior
+//   context: q, k and v come straight from the QKV GEMM output (post-RoPE)
+//   instead of the paged cache.  Flash-attention-2 tiling: 64 query rows per
+//   CTA (16 per warp), 64-token K/V tiles double-buffered in XOR-swizzled shared
+//   memory via cp.async, m16n8k16 bf16 tensor-core MMAs, fp32 online softmax.
+//
+// decode: one query token per request over its paged KV cache
+//   [num_blocks, Hkv, 64, hd].  One CTA per (kv head, request, KV split) serves
+//   the whole GQA group, so each KV page is read from HBM exactly once.  Pages
+//   are staged in padded shared memory with 16-byte cp.async; splits are a fixed
+//   8 pages (512 tokens) so the reduction order depends on the context length
+//   only, never on the batch.
+#include "common.cuh"
+#include "pl_internal.h"
+
+namespace pl {
+
+constexpr int HD = 128;
+constexpr float LOG2E = 1.4426950408889634f;
+
+// ======================================================= prefill (mma.sync)
+
+PL_DEV void ldmatrix_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+PL_DEV void ldmatrix_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3,
+                              uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+PL_DEV void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// 64 x 128 bf16 tile, rows of 256 B = 16 chunks of 16 B, chunk c of row r at c ^ (r & 7).
+PL_DEV uint32_t swz(int row, int chunk) { return row * 256 + ((chunk ^ (row & 7)) << 4); }
+
+PL_DEV void load_tile_64x128(uint8_t* smem, const __nv_bfloat16* base, int64_t ld, int rows_valid) {
+  // 64 rows x 16 chunks = 1024 chunks, 8 per thread
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = threadIdx.x + i * 128;
+    const int row = c >> 4, ch = c & 15;
+    const bool ok = row < rows_valid;
+    const __nv_bfloat16* src = base + (ok ? static_cast<int64_t>(row) * ld : 0) + ch * 8;
+    cp_async16_zfill(smem + swz(row, ch), src, ok);
+  }
+}
+
+__global__ void __launch_bounds__(128, 2)
+    attn_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldqkv,
+                        const int32_t* __restrict__ cu_seqlens, int Hq, int Hkv, float scale_log2,
+                        __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sQ = smem_raw;                 // 16 KB
+  uint8_t* sK = smem_raw + 16384;         // 2 x 16 KB
+  uint8_t* sV = smem_raw + 16384 * 3;     // 2 x 16 KB
+
+  const int r = blockIdx.z, h = blockIdx.y;
+  const int seq0 = cu_seqlens[r];
+  const int L = cu_seqlens[r + 1] - seq0;
+  const int q0 = blockIdx.x * 64;
+  if (q0 >= L) return;
+  const int kh = h / (Hq / Hkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const __nv_bfloat16* qbase = qkv + static_cast<int64_t>(seq0 + q0) * ldqkv + h * HD;
+  const __nv_bfloat16* kbase = qkv + static_cast<int64_t>(seq0) * ldqkv + (Hq + kh) * HD;
+  const __nv_bfloat16* vbase = qkv + static_cast<int64_t>(seq0) * ldqkv + (Hq + Hkv + kh) * HD;
+
+  const int q_hi = min(q0 + 64, L);          // exclusive
+  const int n_kv_tiles = (q_hi + 63) / 64;   // causal: keys < q_hi
+
+  load_tile_64x128(sQ, qbase, ldqkv, q_hi - q0);
+  load_tile_64x128(sK, kbase, ldqkv, min(64, L));
+  load_tile_64x128(sV, vbase, ldqkv, min(64, L));
+  cp_async_commit();
+
+  // Q fragments for this warp's 16 rows: 8 k-steps x 4 regs
+  uint32_t qf[8][4];
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY};
+  float l_r[2] = {0.f, 0.f};
+
+  const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK), sVa = smem_u32(sV);
+  const int mi = lane >> 3, ri = lane & 7;
+
+  for (int j = 0; j < n_kv_tiles; ++j) {
+    const int buf = j & 1;
+    if (j + 1 < n_kv_tiles) {
+      const int kv0 = (j + 1) * 64;
+      load_tile_64x128(sK + (buf ^ 1) * 16384, kbase + static_cast<int64_t>(kv0) * ldqkv, ldqkv,
+                       min(64, L - kv0));
+      load_tile_64x128(sV + (buf ^ 1) * 16384, vbase + static_cast<int64_t>(kv0) * ldqkv, ldqkv,
+                       min(64, L - kv0));
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (j == 0) {
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int row = warp * 16 + (mi & 1) * 8 + ri;
+        const int ch = ks * 2 + (mi >> 1);
+        ldmatrix_x4(qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], sQa + swz(row, ch));
+      }
+    }
+    // S = Q K^T  (16 rows x 64 keys per warp)
+    float s[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+    const uint32_t kt = sKa + buf * 16384;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+      for (int nt = 0; nt < 8; nt += 2) {
+        uint32_t b0, b1, b2, b3;
+        const int row = nt * 8 + (mi >> 1) * 8 + ri;
+        const int ch = ks * 2 + (mi & 1);
+        ldmatrix_x4(b0, b1, b2, b3, kt + swz(row, ch));
+        mma_bf16_16816(s[nt], qf[ks], b0, b1);
+        mma_bf16_16816(s[nt + 1], qf[ks], b2, b3);
+      }
+    }
+    // causal + length mask, online softmax (base 2)
+    const int kv0 = j * 64;
+    const int qrow0 = q0 + warp * 16 + (lane >> 2);
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int qi = qrow0 + (e >> 1) * 8;
+        const int kj = kv0 + nt * 8 + (lane & 3) * 2 + (e & 1);
+        float v = s[nt][e] * scale_log2;
+        if (kj > qi || kj >= L) v = -INFINITY;
+        s[nt][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+    }
+    float corr[2];
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 1));
+      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 2));
+      const float m_new = fmaxf(m_r[hr], mx[hr]);
+      corr[hr] = (m_new == -INFINITY) ? 1.f : exp2f(m_r[hr] - m_new);
+      m_r[hr] = m_new;
+    }
+    float rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int hr = e >> 1;
+        const float p = (m_r[hr] == -INFINITY) ? 0.f : exp2f(s[nt][e] - m_r[hr]);
+        s[nt][e] = p;
+        rs[hr] += p;
+      }
+    }
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 1);
+      rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 2);
+      l_r[hr] = l_r[hr] * corr[hr] + rs[hr];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      o[nt][0] *= corr[0];
+      o[nt][1] *= corr[0];
+      o[nt][2] *= corr[1];
+      o[nt][3] *= corr[1];
+    }
+    // O += P V
+    const uint32_t vt = sVa + buf * 16384;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {  // 16 keys per k-step
+      uint32_t a[4];
+      a[0] = pack_bf16x2(s[2 * ks][0], s[2 * ks][1]);
+      a[1] = pack_bf16x2(s[2 * ks][2], s[2 * ks][3]);
+      a[2] = pack_bf16x2(s[2 * ks + 1][0], s[2 * ks + 1][1]);
+      a[3] = pack_bf16x2(s[2 * ks + 1][2], s[2 * ks + 1][3]);
+#pragma unroll
+      for (int nt = 0; nt < 16; nt += 2) {
+        uint32_t b0, b1, b2, b3;
+        const int row = ks * 16 + (mi & 1) * 8 + ri;
+        const int ch = nt + (mi >> 1);
+        ldmatrix_x4_trans(b0, b1, b2, b3, vt + swz(row, ch));
+        mma_bf16_16816(o[nt], a, b0, b1);
+        mma_bf16_16816(o[nt + 1], a, b2, b3);
+      }
+    }
+    __syncthreads();
+  }
+
+  // normalize and store
+#pragma unroll
+  for (int hr = 0; hr < 2; ++hr) {
+    const int qi = q0 + warp * 16 + (lane >> 2) + hr * 8;
+    if (qi >= L) continue;
+    const float inv = l_r[hr] > 0.f ? 1.f / l_r[hr] : 0.f;
+    __nv_bfloat16* orow = out + static_cast<int64_t>(seq0 + qi) * ldo + h * HD;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const int col = nt * 8 + (lane & 3) * 2;
+      *reinterpret_cast<uint32_t*>(orow + col) =
+          pack_bf16x2(o[nt][hr * 2] * inv, o[nt][hr * 2 + 1] * inv);
+    }
+  }
+}
+
+int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* cu_seqlens, int R,
+                        int max_seqlen, int Hq, int Hkv, int hd, float scale, __nv_bfloat16* out,
+                        int64_t ldo, cudaStream_t st) {
+  if (R <= 0 || max_seqlen <= 0) return PL_OK;
+  if (hd != HD) return set_error(PL_ERR_CONFIG, "attention: head_dim must be 128 (got %d)", hd);
+  if (Hkv <= 0 || Hq % Hkv) return set_error(PL_ERR_CONFIG, "attention: Hq must be a multiple of Hkv");
+  if (ldqkv % 8 || ldo % 8) return set_error(PL_ERR_CONFIG, "attention: leading dims % 8");
+  constexpr int smem = 16384 * 5;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_prefill_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "attn_prefill smem attribute");
+    attr = true;
+  }
+  dim3 grid((max_seqlen + 63) / 64, Hq, R);
+  attn_prefill_kernel<<<grid, 128, smem, st>>>(qkv, ldqkv, cu_seqlens, Hq, Hkv, scale * LOG2E, out,
+                                               ldo);
+  return check_launch("attn_prefill_kernel");
+}
+
+// ======================================================= decode (paged)
+
+constexpr int PAGE = 64;               // tokens per KV block
+constexpr int PAGES_PER_SPLIT = 8;     // 512 tokens per split (context-length driven only)
+constexpr int KROW = HD * 2 + 16;      // padded smem row: 272 B, conflict-free 16 B reads
+
+struct DecodeSmem {
+  static constexpr int KV_TILE = PAGE * KROW;           // 17408 B
+  static constexpr int Q_OFF = 4 * KV_TILE;             // K0 K1 V0 V1
+  static constexpr int P_OFF = Q_OFF + 8 * HD * 4;      // q fp32 [8][128]
+  static constexpr int TOTAL = P_OFF + 8 * PAGE * 4;    // p fp32 [8][64]
+};
+
+PL_DEV void load_page(uint8_t* dst, const __nv_bfloat16* src, int rows_valid) {
+  // 64 rows x 16 chunks, 8 per thread
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = threadIdx.x + i * 128;
+    const int row = c >> 4, ch = c & 15;
+    const bool ok = row < rows_valid;
+    cp_async16_zfill(dst + row * KROW + ch * 16, src + (ok ? row * HD + ch * 8 : 0), ok);
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(128)
+    attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int64_t ldq,
+                       const __nv_bfloat16* __restrict__ k_cache,
+                       const __nv_bfloat16* __restrict__ v_cache,
+                       const int32_t* __restrict__ block_table, int max_blocks,
+                       const int32_t* __restrict__ ctx_len, int Hkv, float scale_log2,
+                       __nv_bfloat16* __restrict__ out, int64_t ldo, float* __restrict__ ws_o,
+                       float2* __restrict__ ws_ml) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sK = smem_raw;
+  uint8_t* sV = smem_raw + 2 * DecodeSmem::KV_TILE;
+  float* sq = reinterpret_cast<float*>(smem_raw + DecodeSmem::Q_OFF);
+  float* sp = reinterpret_cast<float*>(smem_raw + DecodeSmem::P_OFF);
+
+  const int kh = blockIdx.x, r = blockIdx.y, split = blockIdx.z, nsplit = gridDim.z;
+  const int Hq = Hkv * G;
+  const int ctx = ctx_len[r];
+  const int n_pages = (ctx + PAGE - 1) / PAGE;
+  const int p0 = split * PAGES_PER_SPLIT;
+  const int p1 = min(n_pages, p0 + PAGES_PER_SPLIT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // q for the GQA group, pre-scaled into the log2 domain
+  for (int i = threadIdx.x; i < G * HD; i += 128) {
+    const int g = i / HD, e = i % HD;
+    sq[i] = bf2f(q[static_cast<int64_t>(r) * ldq + (kh * G + g) * HD + e]) * scale_log2;
+  }
+
+  // PV ownership: warp w -> heads w, w+4 (< G); lane -> dims [4*lane, 4*lane+4)
+  constexpr int HPW = (G + 3) / 4;
+  float acc[HPW][4];
+  float m_run[HPW], l_run[HPW];
+#pragma unroll
+  for (int a = 0; a < HPW; ++a) {
+    m_run[a] = -INFINITY;
+    l_run[a] = 0.f;
+    acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
+  }
+
+  const int32_t* bt = block_table + static_cast<int64_t>(r) * max_blocks;
+  auto page_src = [&](const __nv_bfloat16* cache, int p) {
+    return cache + (static_cast<int64_t>(bt[p]) * Hkv + kh) * PAGE * HD;
+  };
+  if (p0 < p1) {
+    load_page(sK, page_src(k_cache, p0), min(PAGE, ctx - p0 * PAGE));
+    load_page(sV, page_src(v_cache, p0), min(PAGE, ctx - p0 * PAGE));
+    cp_async_commit();
+  }
+  for (int p = p0; p < p1; ++p) {
+    const int buf = (p - p0) & 1;
+    if (p + 1 < p1) {
+      load_page(sK + (buf ^ 1) * DecodeSmem::KV_TILE, page_src(k_cache, p + 1),
+                min(PAGE, ctx - (p + 1) * PAGE));
+      load_page(sV + (buf ^ 1) * DecodeSmem::KV_TILE, page_src(v_cache, p + 1),
+                min(PAGE, ctx - (p + 1) * PAGE));
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const uint8_t* kt = sK + buf * DecodeSmem::KV_TILE;
+    const uint8_t* vt = sV + buf * DecodeSmem::KV_TILE;
+    const int n_tok = min(PAGE, ctx - p * PAGE);
+
+    // scores: thread -> token j = tid & 63, heads g = (tid >> 6) + 2i
+    {
+      const int j = threadIdx.x & 63, g0 = threadIdx.x >> 6;
+      constexpr int NG = (G + 1) / 2;
+      float sc[NG];
+#pragma unroll
+      for (int i = 0; i < NG; ++i) sc[i] = 0.f;
+      const uint4* krow = reinterpret_cast<const uint4*>(kt + j * KROW);
+#pragma unroll 4
+      for (int c = 0; c < HD / 8; ++c) {
+        const uint4 kv = krow[c];
+        const uint32_t* kp = reinterpret_cast<const uint32_t*>(&kv);
+        float kf[8];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const float2 f = unpack_bf16x2(kp[x]);
+          kf[2 * x] = f.x;
+          kf[2 * x + 1] = f.y;
+        }
+#pragma unroll
+        for (int i = 0; i < NG; ++i) {
+          const int g = g0 + 2 * i;
+          if (g < G) {
+            const float4* qv = reinterpret_cast<const float4*>(sq + g * HD + c * 8);
+            const float4 qa = qv[0], qb = qv[1];
+            sc[i] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qb.x * kf[4] +
+                     qb.y * kf[5] + qb.z * kf[6] + qb.w * kf[7];
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NG; ++i) {
+        const int g = g0 + 2 * i;
+        if (g < G) sp[g * PAGE + j] = (j < n_tok) ? sc[i] : -INFINITY;
+      }
+    }
+    __syncthreads();
+
+    // online softmax + PV
+#pragma unroll
+    for (int a = 0; a < HPW; ++a) {
+      const int g = warp + 4 * a;
+      if (g >= G) continue;
+      const float s0 = sp[g * PAGE + lane], s1 = sp[g * PAGE + lane + 32];
+      const float mt = warp_max(fmaxf(s0, s1));
+      const float m_new = fmaxf(m_run[a], mt);
+      const float corr = (m_run[a] == -INFINITY) ? 0.f : exp2f(m_run[a] - m_new);
+      const float e0 = exp2f(s0 - m_new), e1 = exp2f(s1 - m_new);
+      l_run[a] = l_run[a] * corr + warp_sum(e0 + e1);
+      m_run[a] = m_new;
+      __syncwarp();
+      sp[g * PAGE + lane] = e0;
+      sp[g * PAGE + lane + 32] = e1;
+      __syncwarp();
+      acc[a][0] *= corr;
+      acc[a][1] *= corr;
+      acc[a][2] *= corr;
+      acc[a][3] *= corr;
+      for (int jj = 0; jj < n_tok; ++jj) {
+        const float pj = sp[g * PAGE + jj];
+        const uint2 vv = *reinterpret_cast<const uint2*>(vt + jj * KROW + lane * 8);
+        const float2 va = unpack_bf16x2(vv.x), vb = unpack_bf16x2(vv.y);
+        acc[a][0] += pj * va.x;
+        acc[a][1] += pj * va.y;
+        acc[a][2] += pj * vb.x;
+        acc[a][3] += pj * vb.y;
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int a = 0; a < HPW; ++a) {
+    const int g = warp + 4 * a;
+    if (g >= G) continue;
+    const int head = kh * G + g;
+    if (nsplit == 1) {
+      const float inv = l_run[a] > 0.f ? 1.f / l_run[a] : 0.f;
+      uint2 pk;
+      pk.x = pack_bf16x2(acc[a][0] * inv, acc[a][1] * inv);
+      pk.y = pack_bf16x2(acc[a][2] * inv, acc[a][3] * inv);
+      *reinterpret_cast<uint2*>(out + static_cast<int64_t>(r) * ldo + head * HD + lane * 4) = pk;
+    } else {
+      const int64_t base = (static_cast<int64_t>(r) * Hq + head) * nsplit + split;
+      *reinterpret_cast<float4*>(ws_o + base * HD + lane * 4) =
+          make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+      if (lane == 0) ws_ml[base] = make_float2(m_run[a], l_run[a]);
+    }
+  }
+}
+
+// Merge the per-split partial softmax states in split order.
+__global__ void attn_decode_combine_kernel(const float* __restrict__ ws_o,
+                                           const float2* __restrict__ ws_ml, int Hq, int nsplit,
+                                           __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  const int head = blockIdx.x, r = blockIdx.y, e = threadIdx.x;
+  const int64_t base = (static_cast<int64_t>(r) * Hq + head) * nsplit;
+  float M = -INFINITY;
+  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, ws_ml[base + s].x);
+  float Lsum = 0.f, o = 0.f;
+  for (int s = 0; s < nsplit; ++s) {
+    const float2 ml = ws_ml[base + s];
+    if (ml.x == -INFINITY) continue;
+    const float w = exp2f(ml.x - M);
+    Lsum += ml.y * w;
+    o += ws_o[(base + s) * HD + e] * w;
+  }
+  out[static_cast<int64_t>(r) * ldo + head * HD + e] = f2bf(Lsum > 0.f ? o / Lsum : 0.f);
+}
+
+int64_t attn_decode_workspace_bytes(int R, int Hq, int max_ctx, int hd) {
+  const int pages = (max_ctx + PAGE - 1) / PAGE;
+  const int nsplit = std::max(1, (pages + PAGES_PER_SPLIT - 1) / PAGES_PER_SPLIT);
+  if (nsplit == 1) return 0;
+  return static_cast<int64_t>(R) * Hq * nsplit * (hd * 4 + 8);
+}
+
+int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16* k_cache,
+                       const __nv_bfloat16* v_cache, int block_size, const int32_t* block_table,
+                       int max_blocks, const int32_t* ctx_len, int R, int max_ctx, int Hq, int Hkv,
+                       int hd, float scale, __nv_bfloat16* out, int64_t ldo, void* ws,
+                       int64_t ws_bytes, cudaStream_t st) {
+  if (R <= 0) return PL_OK;
+  if (hd != HD) return set_error(PL_ERR_CONFIG, "attention: head_dim must be 128 (got %d)", hd);
+  if (block_size != PAGE) return set_error(PL_ERR_CONFIG, "attention: KV block size must be 64");
+  if (Hkv <= 0 || Hq % Hkv) return set_error(PL_ERR_CONFIG, "attention: Hq must be a multiple of Hkv");
+  const int G = Hq / Hkv;
+  const int pages = (max_ctx + PAGE - 1) / PAGE;
+  const int nsplit = std::max(1, (pages + PAGES_PER_SPLIT - 1) / PAGES_PER_SPLIT);
+  const int64_t need = attn_decode_workspace_bytes(R, Hq, max_ctx, hd);
+  if (need > 0 && (ws_bytes < need || !ws))
+    return set_error(PL_ERR_CONFIG, "attn_decode: workspace too small (%lld < %lld)",
+                     (long long)ws_bytes, (long long)need);
+  float* ws_o = reinterpret_cast<float*>(ws);
+  float2* ws_ml = need > 0 ? reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(ws) +
+                                                       static_cast<int64_t>(R) * Hq * nsplit * hd * 4)
+                           : nullptr;
+  dim3 grid(Hkv, R, nsplit);
+  constexpr int smem = DecodeSmem::TOTAL;
+  const float sl2 = scale * LOG2E;
+#define PL_DECODE_CASE(GG)                                                                      \
+  case GG: {                                                                                    \
+    static bool attr = false;                                                                   \
+    if (!attr) {                                                                                \
+      cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<GG>,                              \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);  \
+      if (e != cudaSuccess) return set_cuda_error(e, "attn_decode smem attribute");             \
+      attr = true;                                                                              \
+    }                                                                                           \
+    attn_decode_kernel<GG><<<grid, 128, smem, st>>>(q, ldq, k_cache, v_cache, block_table,      \
+                                                    max_blocks, ctx_len, Hkv, sl2, out, ldo,    \
+                                                    ws_o, ws_ml);                               \
+    break;                                                                                      \
+  }
+  switch (G) {
+    PL_DECODE_CASE(1)
+    PL_DECODE_CASE(2)
+    PL_DECODE_CASE(4)
+    PL_DECODE_CASE(8)
+    default:
+      return set_error(PL_ERR_CONFIG, "attn_decode: GQA group %d unsupported (1,2,4,8)", G);
+  }
+#undef PL_DECODE_CASE
+  int rc = check_launch("attn_decode_kernel");
+  if (rc || nsplit == 1) return rc;
+  attn_decode_combine_kernel<<<dim3(Hq, R), HD, 0, st>>>(ws_o, ws_ml, Hq, nsplit, out, ldo);
+  return check_launch("attn_decode_combine_kernel");
+}
+
+}  // namespace pl

@@ -1,0 +1,65 @@
+// Internal declarations shared by the libb200link translation units.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "../../include/b200link.h"
+
+namespace pl {
+
+enum Epi : int {
+  EPI_STORE = PL_EPI_NONE,
+  EPI_BIAS = PL_EPI_BIAS,
+  EPI_RESIDUAL = PL_EPI_RESIDUAL,
+  EPI_SWIGLU = PL_EPI_SWIGLU,
+  EPI_ARGMAX = PL_EPI_ARGMAX,
+  EPI_PARTIAL = 100,
+};
+
+// thread-local error reporting (pl_last_error)
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(cudaError_t e, const char* what);
+int check_launch(const char* what);
+
+// gemm_tc.cu
+int gemm_num_splits(int64_t N, int64_t K, bool swap);
+int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi);
+int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int64_t ldw,
+                const __nv_bfloat16* bias, __nv_bfloat16* C, int64_t ldc,
+                const __nv_bfloat16* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,
+                int epi, void* ws, int64_t ws_bytes, int64_t* argmax_out, cudaStream_t st);
+
+// kernels.cu
+int fill_hash_launch(__nv_bfloat16* dst, int64_t n, uint32_t seed, uint32_t tensor_id,
+                     float scale, float offset, cudaStream_t st);
+int embed_launch(const int64_t* ids, const int32_t* req_slot, const int64_t* last_token,
+                 const __nv_bfloat16* table, int64_t vocab, int64_t T, int d, __nv_bfloat16* out,
+                 cudaStream_t st);
+int rmsnorm_launch(const __nv_bfloat16* x, int64_t ldx, const int32_t* row_idx,
+                   const __nv_bfloat16* w, float eps, int64_t rows, int d, __nv_bfloat16* out,
+                   int64_t ldo, cudaStream_t st);
+int rope_kv_launch(__nv_bfloat16* qkv, int64_t ldqkv, const int32_t* pos, const int32_t* slot,
+                   const __nv_bfloat16* cos_sin, int max_pos, __nv_bfloat16* k_cache,
+                   __nv_bfloat16* v_cache, int block_size, int64_t T, int Hq, int Hkv, int hd,
+                   cudaStream_t st);
+int token_scatter_launch(const int64_t* ids, const int32_t* req_slot, const int32_t* out_pos,
+                         int R, int64_t* last_token, int64_t* gen_tokens, int gen_stride,
+                         cudaStream_t st);
+
+// attention.cu
+int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* cu_seqlens, int R,
+                        int max_seqlen, int Hq, int Hkv, int hd, float scale, __nv_bfloat16* out,
+                        int64_t ldo, cudaStream_t st);
+int64_t attn_decode_workspace_bytes(int R, int Hq, int max_ctx, int hd);
+int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16* k_cache,
+                       const __nv_bfloat16* v_cache, int block_size, const int32_t* block_table,
+                       int max_blocks, const int32_t* ctx_len, int R, int max_ctx, int Hq, int Hkv,
+                       int hd, float scale, __nv_bfloat16* out, int64_t ldo, void* ws,
+                       int64_t ws_bytes, cudaStream_t st);
+
+}  // namespace pl

@@ -1,0 +1,290 @@
+// Stage runtime: the per-stage decoder forward that replaces the reference's
+// simulated compute call `compute_time(stage.profile, phase, mb.batched_tokens)`
+// (engine.py:384).  One C call launches every kernel of the stage's layer range
+// on the caller's stream, so the Python driver pays one FFI crossing per
+// micro-batch per stage instead of ~10 per layer.
+//
+// Layer (modeling_llama.py:313-331, with the residual add fused into the GEMM
+// epilogues so only the single residual stream `hidden` crosses stages):
+//   a   = rmsnorm(hidden) * w_attn
+//   qkv = a . Wqkv^T (+ b)                      tcgen05 GEMM
+//   q,k = rope(q,k); cache[k,v] <- k,v          rope_kv
+//   o   = attn(q, k, v)                         prefill (mma.sync FA2) | decode (paged)
+//   hidden = hidden + o . Wo^T                  tcgen05 GEMM, RESIDUAL epilogue
+//   a   = rmsnorm(hidden) * w_mlp
+//   m   = silu(a . Wg^T) * (a . Wu^T)           tcgen05 GEMM, SWIGLU epilogue
+//   hidden = hidden + m . Wd^T                  tcgen05 GEMM, RESIDUAL epilogue
+// First stage: hidden = embed(ids).  Last stage: final norm of each request's
+// last row, lm_head GEMM with fused argmax -> int64 token ids (engine.py:409).
+#include <vector>
+
+#include "common.cuh"
+#include "pl_internal.h"
+
+namespace pl {
+
+namespace {
+
+int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+struct Layout {
+  int64_t a, qkv, o, m, hn, gemm_ws, attn_ws, total;
+};
+
+Layout stage_layout(const pl_stage_config& c) {
+  const int64_t T = c.max_tokens, R = c.max_reqs;
+  const int64_t qkv_dim = static_cast<int64_t>(c.Hq + 2 * c.Hkv) * c.hd;
+  const int64_t attn_dim = static_cast<int64_t>(c.Hq) * c.hd;
+  Layout L{};
+  int64_t off = 0;
+  L.a = off;
+  off += align256(T * c.d * 2);
+  L.qkv = off;
+  off += align256(T * qkv_dim * 2);
+  L.o = off;
+  off += align256(T * attn_dim * 2);
+  L.m = off;
+  off += align256(T * static_cast<int64_t>(c.ffn) * 2);
+  L.hn = off;
+  off += align256(R * c.d * 2);
+  // split-K partials are only used on the SWAP (T <= 256) path
+  int64_t gws = 0;
+  const int64_t Ts[2] = {std::min<int64_t>(T, 256), std::min<int64_t>(R, 256)};
+  for (int64_t t : Ts) {
+    gws = std::max(gws, gemm_workspace_bytes(t, qkv_dim, c.d, EPI_BIAS));
+    gws = std::max(gws, gemm_workspace_bytes(t, c.d, attn_dim, EPI_RESIDUAL));
+    gws = std::max(gws, gemm_workspace_bytes(t, 2 * static_cast<int64_t>(c.ffn), c.d, EPI_SWIGLU));
+    gws = std::max(gws, gemm_workspace_bytes(t, c.d, c.ffn, EPI_RESIDUAL));
+  }
+  if (c.is_last) gws = std::max(gws, gemm_workspace_bytes(std::min<int64_t>(R, 256), c.vocab, c.d, EPI_ARGMAX));
+  L.gemm_ws = off;
+  off += align256(gws);
+  L.attn_ws = off;
+  off += align256(attn_decode_workspace_bytes(static_cast<int>(R), c.Hq, c.max_ctx, c.hd));
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+struct ProbeRec {
+  cudaEvent_t ev[7];
+  int phase, T;
+};
+
+struct Stage {
+  pl_stage_config cfg;
+  std::vector<pl_layer_weights> layers;
+  uint8_t* ws;
+  Layout L;
+  int probe_layer = -1;
+  std::vector<ProbeRec> probes;
+  size_t probe_used = 0;
+
+  __nv_bfloat16* buf(int64_t off) const { return reinterpret_cast<__nv_bfloat16*>(ws + off); }
+
+  cudaEvent_t* next_probe(int phase, int T) {
+    if (probe_used == probes.size()) {
+      if (probes.size() >= 65536) return nullptr;
+      ProbeRec r{};
+      for (auto& e : r.ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      probes.push_back(r);
+    }
+    ProbeRec& r = probes[probe_used++];
+    r.phase = phase;
+    r.T = T;
+    return r.ev;
+  }
+
+  int forward(const pl_microbatch& mb, cudaStream_t st) {
+    const pl_stage_config& c = cfg;
+    const int T = mb.T, R = mb.R;
+    if (T <= 0 || R <= 0) return set_error(PL_ERR_CONFIG, "stage_forward: empty micro-batch");
+    if (T > c.max_tokens || R > c.max_reqs)
+      return set_error(PL_ERR_CONFIG, "stage_forward: micro-batch (T=%d, R=%d) exceeds capacity (%d, %d)",
+                       T, R, c.max_tokens, c.max_reqs);
+    const bool decode = mb.phase == 1;
+    if (decode && T != R) return set_error(PL_ERR_CONFIG, "stage_forward: decode needs T == R");
+    if (!mb.meta || !mb.hidden) return set_error(PL_ERR_CONFIG, "stage_forward: missing buffers");
+    const int32_t* pos = mb.meta;
+    const int32_t* slot = pos + T;
+    const int32_t* req_slot = slot + T;
+    const int32_t* cu = req_slot + T;
+    const int32_t* ctx = cu + R + 1;
+    const int32_t* last_idx = ctx + R;
+    const int32_t* bt = last_idx + R;
+
+    const int64_t d = c.d;
+    const int64_t qkv_dim = static_cast<int64_t>(c.Hq + 2 * c.Hkv) * c.hd;
+    const int64_t attn_dim = static_cast<int64_t>(c.Hq) * c.hd;
+    const int64_t ffn = c.ffn;
+    __nv_bfloat16* hid = static_cast<__nv_bfloat16*>(mb.hidden);
+    __nv_bfloat16* a = buf(L.a);
+    __nv_bfloat16* qkv = buf(L.qkv);
+    __nv_bfloat16* o = buf(L.o);
+    __nv_bfloat16* m = buf(L.m);
+    void* gws = ws + L.gemm_ws;
+    const int64_t gws_bytes = L.attn_ws - L.gemm_ws;
+    const float scale = 1.0f / sqrtf(static_cast<float>(c.hd));
+    int rc;
+
+    if (c.is_first) {
+      if (decode) {
+        if (!mb.last_token) return set_error(PL_ERR_CONFIG, "stage_forward: decode needs last_token");
+        rc = embed_launch(nullptr, req_slot, mb.last_token, static_cast<const __nv_bfloat16*>(c.embed),
+                          c.vocab, T, c.d, hid, st);
+      } else {
+        if (!mb.token_ids) return set_error(PL_ERR_CONFIG, "stage_forward: prefill needs token_ids");
+        rc = embed_launch(mb.token_ids, nullptr, nullptr, static_cast<const __nv_bfloat16*>(c.embed),
+                          c.vocab, T, c.d, hid, st);
+      }
+      if (rc) return rc;
+    }
+
+    for (int l = 0; l < c.num_layers; ++l) {
+      const pl_layer_weights& w = layers[l];
+      cudaEvent_t* ev = (l == probe_layer) ? next_probe(mb.phase, T) : nullptr;
+      auto mark = [&](int i) {
+        if (ev) cudaEventRecord(ev[i], st);
+      };
+      if ((rc = rmsnorm_launch(hid, d, nullptr, static_cast<const __nv_bfloat16*>(w.attn_norm), c.eps,
+                               T, c.d, a, d, st)))
+        return rc;
+      mark(0);
+      if ((rc = gemm_launch(a, d, static_cast<const __nv_bfloat16*>(w.w_qkv), d,
+                            static_cast<const __nv_bfloat16*>(w.b_qkv), qkv, qkv_dim, nullptr, 0, T,
+                            qkv_dim, d, w.b_qkv ? EPI_BIAS : EPI_STORE, gws, gws_bytes, nullptr, st)))
+        return rc;
+      mark(1);
+      if ((rc = rope_kv_launch(qkv, qkv_dim, pos, slot, static_cast<const __nv_bfloat16*>(c.cos_sin),
+                               c.max_pos, static_cast<__nv_bfloat16*>(w.k_cache),
+                               static_cast<__nv_bfloat16*>(w.v_cache), c.block_size, T, c.Hq, c.Hkv,
+                               c.hd, st)))
+        return rc;
+      if (decode) {
+        rc = attn_decode_launch(qkv, qkv_dim, static_cast<const __nv_bfloat16*>(w.k_cache),
+                                static_cast<const __nv_bfloat16*>(w.v_cache), c.block_size, bt,
+                                c.max_blocks_per_req, ctx, R, mb.max_ctx, c.Hq, c.Hkv, c.hd, scale, o,
+                                attn_dim, ws + L.attn_ws, L.total - L.attn_ws, st);
+      } else {
+        rc = attn_prefill_launch(qkv, qkv_dim, cu, R, mb.max_seqlen, c.Hq, c.Hkv, c.hd, scale, o,
+                                 attn_dim, st);
+      }
+      if (rc) return rc;
+      mark(2);
+      if ((rc = gemm_launch(o, attn_dim, static_cast<const __nv_bfloat16*>(w.w_o), attn_dim, nullptr,
+                            hid, d, hid, d, T, d, attn_dim, EPI_RESIDUAL, gws, gws_bytes, nullptr, st)))
+        return rc;
+      mark(3);
+      if ((rc = rmsnorm_launch(hid, d, nullptr, static_cast<const __nv_bfloat16*>(w.mlp_norm), c.eps, T,
+                               c.d, a, d, st)))
+        return rc;
+      mark(4);
+      if ((rc = gemm_launch(a, d, static_cast<const __nv_bfloat16*>(w.w_gate_up), d, nullptr, m, ffn,
+                            nullptr, 0, T, 2 * ffn, d, EPI_SWIGLU, gws, gws_bytes, nullptr, st)))
+        return rc;
+      mark(5);
+      if ((rc = gemm_launch(m, ffn, static_cast<const __nv_bfloat16*>(w.w_down), ffn, nullptr, hid, d,
+                            hid, d, T, d, ffn, EPI_RESIDUAL, gws, gws_bytes, nullptr, st)))
+        return rc;
+      mark(6);
+    }
+
+    if (c.is_last) {
+      if (!mb.out_ids) return set_error(PL_ERR_CONFIG, "stage_forward: last stage needs out_ids");
+      __nv_bfloat16* hn = buf(L.hn);
+      if ((rc = rmsnorm_launch(hid, d, last_idx, static_cast<const __nv_bfloat16*>(c.final_norm), c.eps,
+                               R, c.d, hn, d, st)))
+        return rc;
+      if ((rc = gemm_launch(hn, d, static_cast<const __nv_bfloat16*>(c.lm_head), d, nullptr, nullptr, 0,
+                            nullptr, 0, R, c.vocab, d, EPI_ARGMAX, gws, gws_bytes, mb.out_ids, st)))
+        return rc;
+    }
+    return PL_OK;
+  }
+};
+
+}  // namespace pl
+
+using namespace pl;
+
+extern "C" {
+
+int64_t pl_stage_workspace_bytes(const pl_stage_config* cfg) {
+  if (!cfg) return -1;
+  return stage_layout(*cfg).total;
+}
+
+int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* layers, void* workspace,
+                        int64_t workspace_bytes, void** handle) {
+  if (!cfg || !handle || (cfg->num_layers > 0 && !layers))
+    return set_error(PL_ERR_CONFIG, "stage_create: null argument");
+  if (cfg->hd != 128) return set_error(PL_ERR_CONFIG, "stage_create: head_dim must be 128");
+  if (cfg->d % 64 || cfg->ffn % 64)
+    return set_error(PL_ERR_CONFIG, "stage_create: d and ffn must be multiples of 64");
+  if (cfg->block_size != 64) return set_error(PL_ERR_CONFIG, "stage_create: KV block size must be 64");
+  if (cfg->is_first && !cfg->embed) return set_error(PL_ERR_CONFIG, "stage_create: first stage needs embed");
+  if (cfg->is_last && (!cfg->lm_head || !cfg->final_norm))
+    return set_error(PL_ERR_CONFIG, "stage_create: last stage needs lm_head and final_norm");
+  const Layout L = stage_layout(*cfg);
+  if (!workspace || workspace_bytes < L.total)
+    return set_error(PL_ERR_CONFIG, "stage_create: workspace %lld < required %lld",
+                     (long long)workspace_bytes, (long long)L.total);
+  Stage* s = new Stage();
+  s->cfg = *cfg;
+  s->layers.assign(layers, layers + cfg->num_layers);
+  s->ws = static_cast<uint8_t*>(workspace);
+  s->L = L;
+  *handle = s;
+  return PL_OK;
+}
+
+int32_t pl_stage_forward(void* handle, const pl_microbatch* mb, void* stream) {
+  if (!handle || !mb) return set_error(PL_ERR_CONFIG, "stage_forward: null argument");
+  return static_cast<Stage*>(handle)->forward(*mb, static_cast<cudaStream_t>(stream));
+}
+
+int32_t pl_stage_destroy(void* handle) {
+  Stage* s = static_cast<Stage*>(handle);
+  if (!s) return PL_OK;
+  for (auto& r : s->probes)
+    for (auto& e : r.ev) cudaEventDestroy(e);
+  delete s;
+  return PL_OK;
+}
+
+// Timing probe: CUDA events around each kernel group of one layer, recorded on
+// the launch stream (bench.py reads kernel durations live, not under ncu).
+int32_t pl_stage_probe(void* handle, int32_t layer) {
+  Stage* s = static_cast<Stage*>(handle);
+  if (!s) return set_error(PL_ERR_CONFIG, "stage_probe: null handle");
+  s->probe_layer = layer;
+  s->probe_used = 0;
+  return PL_OK;
+}
+
+// out_ms[i*5 + {0..4}] = {qkv gemm, rope+attention, o gemm, gate_up gemm, down gemm};
+// out_meta[i*2 + {0,1}] = {phase, T}.  Requires the stream to be synchronized.
+int32_t pl_stage_probe_read(void* handle, float* out_ms, int32_t* out_meta, int32_t cap, int32_t* n) {
+  Stage* s = static_cast<Stage*>(handle);
+  if (!s || !n) return set_error(PL_ERR_CONFIG, "stage_probe_read: null argument");
+  const int cnt = static_cast<int>(std::min<size_t>(s->probe_used, static_cast<size_t>(cap)));
+  for (int i = 0; i < cnt; ++i) {
+    const ProbeRec& r = s->probes[i];
+    const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 5}, {5, 6}};
+    for (int k = 0; k < 5; ++k) {
+      float ms = 0.f;
+      cudaError_t e = cudaEventElapsedTime(&ms, r.ev[pairs[k][0]], r.ev[pairs[k][1]]);
+      if (e != cudaSuccess) return set_cuda_error(e, "probe elapsed time");
+      out_ms[i * 5 + k] = ms;
+    }
+    out_meta[i * 2] = r.phase;
+    out_meta[i * 2 + 1] = r.T;
+  }
+  *n = cnt;
+  s->probe_used = 0;
+  return PL_OK;
+}
+
+}  // extern "C"

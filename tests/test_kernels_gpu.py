@@ -1,0 +1,217 @@
+"""Kernel parity: every libb200link kernel vs the CPU oracle (oracle/decoder.py).
+
+Tolerances (stated per test):
+* integer / byte work (hash init, embedding gather, argmax outside the tie
+  band, RoPE+KV append) is bit-exact;
+* bf16 outputs of fp32 reductions (RMSNorm, GEMM epilogues, attention) may
+  differ from the oracle only by the fp32 summation order, i.e. at most a
+  couple of bf16 ulps: |gpu - ref| <= 2^-7 |ref| + atol.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import decoder as OD
+from oracle import hashinit as H
+
+pytestmark = pytest.mark.gpu
+
+BF16 = torch.bfloat16
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2507_05043_b200 import ops as O
+
+    return O
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def close_bf16(gpu, ref, rel=2.0 ** -7, atol=1e-3, scale=None):
+    """|gpu - ref| <= rel * scale + atol, scale = |ref| unless the op sums terms that
+    can cancel (residual adds: scale = |a| + |b| of the two rounded addends)."""
+    g = gpu.float().cpu()
+    r = ref.float().cpu()
+    err = (g - r).abs()
+    bound = rel * (r.abs() if scale is None else scale) + atol
+    bad = (err > bound).sum().item()
+    assert bad == 0, f"{bad} / {err.numel()} elements out of tolerance; max err {err.max().item():.3g}"
+
+
+@pytest.mark.parametrize("n,tid,scale,offset", [(1, 3, 1.0, 0.0), (1000, 7, 0.0346, 0.0),
+                                                 (1 << 20, 0xFFFF0001, 0.02, 0.0),
+                                                 (4097, 17, 0.05, 1.0)])
+def test_fill_hash_bit_exact(ops, n, tid, scale, offset):
+    t = torch.empty(n, dtype=BF16, device=dev())
+    ops.fill_hash_(t, 0, tid, scale, offset)
+    want = H.hash_bf16_bits(n, 0, tid, scale, offset)
+    got = t.cpu().view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, want)
+
+
+def test_embed_exact(ops):
+    table = torch.randn(512, 256).to(BF16)
+    ids = torch.randint(0, 512, (37,))
+    out = ops.embed(ids.to(dev()), table.to(dev()))
+    assert torch.equal(out.cpu(), table[ids])
+    # decode path: gather through the per-slot feedback table
+    last = torch.randint(0, 512, (16,))
+    slot = torch.randint(0, 16, (9,), dtype=torch.int32)
+    out = ops.embed(None, table.to(dev()), req_slot=slot.to(dev()), last_token=last.to(dev()))
+    assert torch.equal(out.cpu(), table[last[slot.long()]])
+
+
+@pytest.mark.parametrize("rows,d", [(1, 256), (7, 4096), (64, 8192), (300, 4096)])
+def test_rmsnorm(ops, rows, d):
+    g = torch.Generator().manual_seed(rows * 7 + d)
+    x = (torch.randn(rows, d, generator=g) * 3).to(BF16)
+    w = (1 + 0.05 * torch.randn(d, generator=g)).to(BF16)
+    out = ops.rmsnorm(x.to(dev()), w.to(dev()), 1e-5)
+    close_bf16(out, OD.rmsnorm_ref(x, w, 1e-5), rel=2.0 ** -7, atol=1e-6)
+
+
+def test_rmsnorm_row_gather(ops):
+    x = torch.randn(50, 256).to(BF16)
+    w = torch.ones(256).to(BF16)
+    idx = torch.tensor([49, 0, 17], dtype=torch.int32)
+    out = ops.rmsnorm(x.to(dev()), w.to(dev()), 1e-6, row_idx=idx.to(dev()))
+    close_bf16(out, OD.rmsnorm_ref(x[idx.long()], w, 1e-6), atol=1e-6)
+
+
+GEMM_SHAPES = [  # (T, N, K)
+    (1, 512, 256), (5, 640, 256), (16, 6144, 4096), (17, 384, 768), (64, 4096, 4096),
+    (100, 1024, 512), (256, 512, 256), (300, 512, 256), (1000, 1536, 256), (2048, 768, 1024),
+]
+
+
+@pytest.mark.parametrize("T,N,K", GEMM_SHAPES)
+def test_gemm_store(ops, T, N, K):
+    g = torch.Generator().manual_seed(T * 31 + N + K)
+    x = torch.randn(T, K, generator=g).to(BF16)
+    w = (torch.randn(N, K, generator=g) * 0.05).to(BF16)
+    out = ops.gemm(x.to(dev()), w.to(dev()))
+    close_bf16(out, OD.linear_acc(x, w), atol=1e-3)
+
+
+@pytest.mark.parametrize("T,N,K", [(3, 512, 256), (64, 6144, 4096), (700, 512, 256)])
+def test_gemm_bias(ops, T, N, K):
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(T, K, generator=g).to(BF16)
+    w = (torch.randn(N, K, generator=g) * 0.05).to(BF16)
+    b = torch.randn(N, generator=g).to(BF16)
+    out = ops.gemm(x.to(dev()), w.to(dev()), ops.EPI_BIAS, bias=b.to(dev()))
+    close_bf16(out, OD.linear_acc(x, w) + b.float(), atol=1e-3)
+
+
+@pytest.mark.parametrize("T,N,K", [(8, 256, 256), (64, 4096, 14336), (513, 256, 768)])
+def test_gemm_residual_inplace(ops, T, N, K):
+    g = torch.Generator().manual_seed(9)
+    x = torch.randn(T, K, generator=g).to(BF16)
+    w = (torch.randn(N, K, generator=g) * 0.02).to(BF16)
+    h = torch.randn(T, N, generator=g).to(BF16)
+    hd = h.to(dev())
+    ops.gemm(x.to(dev()), w.to(dev()), ops.EPI_RESIDUAL, residual=hd, out=hd)
+    acc = OD.rbf(OD.linear_acc(x, w))
+    ref = acc + h.float()
+    close_bf16(hd, ref, atol=1e-3, scale=acc.abs() + h.float().abs())
+
+
+@pytest.mark.parametrize("T,ffn,K", [(4, 768, 256), (32, 14336, 4096), (400, 768, 256)])
+def test_gemm_swiglu(ops, T, ffn, K):
+    g = torch.Generator().manual_seed(11)
+    x = torch.randn(T, K, generator=g).to(BF16)
+    w = (torch.randn(2 * ffn, K, generator=g) * 0.05).to(BF16)
+    out = ops.gemm(x.to(dev()), w.to(dev()), ops.EPI_SWIGLU)
+    wg, wu = OD.deinterleave_gate_up(w)
+    ref = OD.swiglu_ref(OD.linear_acc(x, wg), OD.linear_acc(x, wu))
+    close_bf16(out, ref, rel=2.0 ** -6, atol=2e-3)
+
+
+@pytest.mark.parametrize("R,V,d", [(1, 512, 256), (8, 128256, 4096), (64, 32000, 256), (200, 1000, 256)])
+def test_lmhead_argmax(ops, R, V, d):
+    g = torch.Generator().manual_seed(R + V)
+    h = torch.randn(R, d, generator=g).to(BF16)
+    w = (torch.randn(V, d, generator=g) * 0.05).to(BF16)
+    ids = ops.lmhead_argmax(h.to(dev()), w.to(dev())).cpu()
+    logits = OD.linear_acc(h, w)
+    top2 = logits.topk(2, dim=-1).values
+    tie = (top2[:, 0] - top2[:, 1]) < 1e-3 * top2[:, 0].abs().clamp(min=1)
+    ref = logits.argmax(-1)
+    ok = (ids == ref) | tie
+    assert ok.all(), f"argmax mismatch outside tie band at rows {torch.nonzero(~ok).flatten().tolist()}"
+    # chosen id must be (near-)maximal
+    assert (logits.gather(1, ids[:, None]).squeeze(1) >= top2[:, 0] - 1e-3 * top2[:, 0].abs().clamp(min=1)).all()
+
+
+def test_rope_kv_bit_exact(ops):
+    T, Hq, Hkv, hd = 70, 4, 2, 128
+    g = torch.Generator().manual_seed(3)
+    qkv = torch.randn(T, (Hq + 2 * Hkv) * hd, generator=g).to(BF16)
+    pos = torch.randint(0, 900, (T,), dtype=torch.int32)
+    table = OD.rope_table_ref(5e5, hd, 1024)
+    num_blocks = 8
+    slot = torch.randperm(num_blocks * 64)[:T].to(torch.int32)
+    kc = torch.zeros(num_blocks, Hkv, 64, hd, dtype=BF16, device=dev())
+    vc = torch.zeros_like(kc)
+    q_gpu = qkv.to(dev())
+    ops.rope_kv_write(q_gpu, pos.to(dev()), slot.to(dev()), table.to(dev()), kc, vc, Hq, Hkv, hd)
+    x = qkv.reshape(T, Hq + 2 * Hkv, hd)
+    ref_q = OD.rope_ref(x[:, :Hq], pos, table)
+    ref_k = OD.rope_ref(x[:, Hq:Hq + Hkv], pos, table)
+    got = q_gpu.cpu().reshape(T, Hq + 2 * Hkv, hd)
+    assert torch.equal(got[:, :Hq], ref_q)
+    assert torch.equal(got[:, Hq:Hq + Hkv], ref_k)
+    assert torch.equal(got[:, Hq + Hkv:], x[:, Hq + Hkv:])
+    kc, vc = kc.cpu(), vc.cpu()
+    for t in range(T):
+        b, o = int(slot[t]) // 64, int(slot[t]) % 64
+        assert torch.equal(kc[b, :, o], ref_k[t])
+        assert torch.equal(vc[b, :, o], x[t, Hq + Hkv:])
+
+
+@pytest.mark.parametrize("lens,Hq,Hkv", [([128] * 8, 2, 1), ([1, 63, 64, 65, 200], 4, 2),
+                                         ([512, 512], 32, 8), ([2048], 8, 1)])
+def test_attn_prefill(ops, lens, Hq, Hkv):
+    hd = 128
+    T = sum(lens)
+    g = torch.Generator().manual_seed(sum(lens) + Hq)
+    qkv = torch.randn(T, (Hq + 2 * Hkv) * hd, generator=g).to(BF16)
+    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
+    out = ops.attn_prefill(qkv.to(dev()), cu.to(dev()), max(lens), Hq, Hkv, hd).cpu()
+    x = qkv.reshape(T, Hq + 2 * Hkv, hd)
+    refs = []
+    for r, n in enumerate(lens):
+        s = int(cu[r])
+        refs.append(OD.attention_ref(x[s:s + n, :Hq], x[s:s + n, Hq:Hq + Hkv], x[s:s + n, Hq + Hkv:], 0))
+    close_bf16(out, torch.cat(refs), rel=2.0 ** -6, atol=4e-3)
+
+
+@pytest.mark.parametrize("ctx,Hq,Hkv", [([1, 5, 64, 65, 640], 32, 8), ([700, 1300], 8, 8),
+                                        ([129] * 16, 2, 1), ([3000], 64, 8)])
+def test_attn_decode_paged(ops, ctx, Hq, Hkv):
+    hd, bs = 128, 64
+    R = len(ctx)
+    g = torch.Generator().manual_seed(sum(ctx) + Hq)
+    max_blocks = max((c + bs - 1) // bs for c in ctx)
+    num_blocks = R * max_blocks + 3
+    perm = torch.randperm(num_blocks, generator=g)
+    bt = perm[: R * max_blocks].reshape(R, max_blocks).to(torch.int32)
+    kc = torch.randn(num_blocks, Hkv, bs, hd, generator=g).to(BF16)
+    vc = torch.randn(num_blocks, Hkv, bs, hd, generator=g).to(BF16)
+    q = torch.randn(R, Hq * hd, generator=g).to(BF16)
+    ctx_t = torch.tensor(ctx, dtype=torch.int32)
+    out = ops.attn_decode(q.to(dev()), kc.to(dev()), vc.to(dev()), bt.to(dev()), ctx_t.to(dev()),
+                          max(ctx), Hq, Hkv, hd).cpu()
+    refs = []
+    for r in range(R):
+        pages = bt[r, : (ctx[r] + bs - 1) // bs].long()
+        k = kc[pages].permute(0, 2, 1, 3).reshape(-1, Hkv, hd)[: ctx[r]]
+        v = vc[pages].permute(0, 2, 1, 3).reshape(-1, Hkv, hd)[: ctx[r]]
+        refs.append(OD.attention_ref(q[r].reshape(1, Hq, hd), k, v, None))
+    close_bf16(out, torch.cat(refs), rel=2.0 ** -7, atol=2e-3)
