@@ -1,0 +1,421 @@
+"""B200 backend for the virtual-clock driver: real stage forwards and real links.
+
+Every rank runs the identical deterministic driver (decisions come from the
+virtual clock, never from completions), so all ranks agree on the schedule
+without exchanging control messages; each rank only issues the work of its
+own stages and links.  Per local stage there are three CUDA streams:
+
+  compute   H2D micro-batch metadata -> pl_stage_forward
+  send      outgoing link: one NCCL send (or device copy) per LinkQueue chunk
+  recv      incoming link: one NCCL recv per chunk into the same byte range
+
+Cross-stream ordering uses CUDA events (never host syncs):
+  compute(s, mb)   waits recv_done(s, slot) and the previous occupant's send_done(s, slot)
+  send chunk       waits comp_done(s, slot) (first chunk)
+  recv chunk       waits the previous occupant's send_done(dst, slot) (first chunk)
+  head decode      waits the latest token-scatter event (return hop)
+A micro-batch keeps one slot (= one hidden buffer per stage) from admission
+until its tokens come back (engine.py:478 caps in-flight micro-batches at n).
+
+Transports per hop: NCCL 2.28 ncclSend/ncclRecv between ranks
+(one 2-rank communicator per directed hop, NVLink/NVSwitch), a device copy
+when both stages live on the same process.
+"""
+
+from __future__ import annotations
+
+import os
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._pipelink import pipelink
+from .driver import Backend
+from .executor import StageExecutor, build_meta
+from .spec import BLOCK_SIZE, DecoderSpec, prompt_tokens
+
+BatchPhase = pipelink.engine.BatchPhase
+RequestState = pipelink.RequestState
+
+RUN_AHEAD = 24  # max launched-but-unfinished forwards per stage before the host waits
+
+
+@dataclass
+class _MbRec:
+    slot: int
+    T: int
+    R: int
+    decode: bool
+    max_seqlen: int
+    max_ctx: int
+    meta: np.ndarray
+    ids: np.ndarray | None
+    scatter: np.ndarray  # int32 [req_slot R | out_pos R]
+    rids: tuple = ()
+
+
+class Placement:
+    """Stage -> (rank, device).  Contiguous blocks of stages per rank."""
+
+    def __init__(self, n_stages: int, world_size: int = 1, rank: int = 0,
+                 devices: list | None = None):
+        if n_stages % world_size:
+            raise pipelink.ConfigError(f"{n_stages} stages do not split over {world_size} ranks")
+        self.n_stages, self.world, self.rank = n_stages, world_size, rank
+        per = n_stages // world_size
+        self.stage_rank = [s // per for s in range(n_stages)]
+        if world_size > 1:
+            local = int(os.environ.get("LOCAL_RANK", rank))
+            self.stage_device = [torch.device("cuda", local) if self.stage_rank[s] == rank else None
+                                 for s in range(n_stages)]
+        else:
+            devs = devices or [torch.device("cuda", 0)]
+            self.stage_device = [torch.device(devs[s * len(devs) // n_stages]) for s in range(n_stages)]
+
+    def local(self, s: int) -> bool:
+        return self.stage_rank[s] == self.rank
+
+
+class _PinnedRing:
+    """Pinned host staging buffers reused round-robin, each guarded by an event."""
+
+    def __init__(self, n: int, nbytes: int, device):
+        self.bufs = [torch.empty(nbytes, dtype=torch.uint8).pin_memory() for _ in range(n)]
+        self.events = [None] * n
+        self.i = 0
+        self.device = device
+
+    def take(self) -> tuple[int, torch.Tensor]:
+        k = self.i
+        self.i = (self.i + 1) % len(self.bufs)
+        ev = self.events[k]
+        if ev is not None:
+            ev.synchronize()
+        return k, self.bufs[k]
+
+    def mark(self, k: int, stream) -> None:
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.events[k] = ev
+
+
+class GpuBackend(Backend):
+    def __init__(self, spec: DecoderSpec, cfg, placement: Placement, *, seed: int = 0,
+                 prompts: dict | None = None, comms: dict | None = None, throttle: bool = False):
+        if cfg.allow_mixed_phase:
+            raise pipelink.ConfigError("mixed prefill/decode micro-batches are not supported on the "
+                                       "B200 backend yet (allow_mixed_phase=False)")
+        self.spec, self.cfg, self.pl = spec, cfg, placement
+        self.seed = seed
+        self.user_prompts = prompts
+        self.comms = comms or {}
+        self.throttle = throttle
+        self.S = placement.n_stages
+        self.layer_ranges = [rng for _, rng in cfg.partition.stages]
+        self.n_slots = cfg.controller.effective_n_max(self.S)
+        self.exe: dict[int, StageExecutor] = {}
+        self._built_for = None
+
+    # ------------------------------------------------------------ build
+    def prepare(self, trace) -> None:
+        """Allocate weights / KV / buffers sized for `trace` (idempotent per shape)."""
+        reqs = trace.requests
+        max_in = max(r.input_len for r in reqs)
+        max_ctx = max(r.input_len + r.output_len for r in reqs)
+        ctrl = self.cfg.controller
+        max_tokens = max(min(ctrl.max_batched_tokens, sum(r.input_len for r in reqs)), max_in,
+                         min(ctrl.max_batch_size, len(reqs)))
+        max_reqs = max(1, min(len(reqs), max(ctrl.max_batch_size, 1)))
+        # prefill micro-batches can carry more requests than max_batch_size? no: capped
+        blocks = sum(-(-(r.input_len + r.output_len) // BLOCK_SIZE) for r in reqs)
+        key = (max_tokens, max_reqs, max_ctx, blocks)
+        if self._built_for is not None and all(a >= b for a, b in zip(self._built_for, key)):
+            return
+        self.close()
+        self.max_tokens, self.max_reqs, self.max_ctx, self.num_blocks = key
+        self.max_blocks = -(-max_ctx // BLOCK_SIZE)
+        for s in range(self.S):
+            if not self.pl.local(s):
+                continue
+            lo, hi = self.layer_ranges[s]
+            self.exe[s] = StageExecutor(
+                self.spec, s, (lo, hi), s == 0, s == self.S - 1, self.pl.stage_device[s],
+                seed=self.seed, max_tokens=max_tokens, max_reqs=max_reqs, max_ctx=max_ctx,
+                num_blocks=blocks, n_slots=self.n_slots)
+        self._built_for = key
+        self._streams_built = False
+
+    def _build_streams(self) -> None:
+        self.send_stream, self.recv_stream = {}, {}
+        self.ev_comp, self.ev_send, self.ev_recv = {}, {}, {}
+        self.meta_ring, self.ids_ring = {}, {}
+        self.throttle_ev = {}
+        for s, exe in self.exe.items():
+            dev = exe.device
+            with torch.cuda.device(dev):
+                self.send_stream[s] = torch.cuda.Stream(dev)
+                self.recv_stream[s] = torch.cuda.Stream(dev)
+            self.ev_comp[s] = [None] * self.n_slots
+            self.ev_send[s] = [None] * self.n_slots
+            self.ev_recv[s] = [None] * self.n_slots
+            self.meta_ring[s] = _PinnedRing(RUN_AHEAD + 8, exe.meta_dev.numel() * 4, dev)
+            if exe.is_first:
+                self.ids_ring[s] = _PinnedRing(RUN_AHEAD + 8, exe.max_tokens * 8, dev)
+            self.throttle_ev[s] = deque()
+        head = self.exe.get(0)
+        if head is not None:
+            dev = head.device
+            n_req = self._n_requests
+            self.last_token = torch.zeros(n_req, dtype=torch.int64, device=dev)
+            self.gen_tokens = torch.zeros(n_req, self._max_out, dtype=torch.int64, device=dev)
+            self.ids_recv = [torch.zeros(self.max_reqs, dtype=torch.int64, device=dev)
+                             for _ in range(self.n_slots)]
+            self.scatter_dev = [torch.zeros(2 * self.max_reqs, dtype=torch.int32, device=dev)
+                                for _ in range(self.n_slots)]
+            self.scatter_ring = _PinnedRing(RUN_AHEAD + 8, 8 * self.max_reqs, dev)
+        self._streams_built = True
+
+    def close(self) -> None:
+        for exe in self.exe.values():
+            exe.close()
+        self.exe = {}
+        self._built_for = None
+
+    # ------------------------------------------------------------ driver hooks
+    def start(self, driver, trace) -> None:
+        self.driver = driver
+        self.prepare(trace)
+        reqs = trace.requests
+        self._n_requests = len(reqs)
+        self._max_out = max(r.output_len for r in reqs)
+        self.rid_index = {r.id: i for i, r in enumerate(reqs)}
+        self._build_streams()
+        self.req_len = {r.id: r.input_len for r in reqs}
+        self.req_out = {r.id: r.output_len for r in reqs}
+        self.free_slots = list(range(self.n_slots - 1, -1, -1))
+        self.free_blocks = list(range(self.num_blocks - 1, -1, -1))
+        self.bt_rows: dict[int, np.ndarray] = {}
+        self.mbs: dict[int, _MbRec] = {}
+        self.fb_events: list = []   # (event, mb request ids)
+        self.first_decode_ev = None
+        self.prompts = {}
+        for r in reqs:
+            if self.user_prompts is not None and r.id in self.user_prompts:
+                p = np.asarray(self.user_prompts[r.id], dtype=np.int64)
+                if p.shape != (r.input_len,):
+                    raise pipelink.ConfigError(f"prompt of request {r.id} has wrong length")
+            else:
+                p = prompt_tokens(self.seed, r.id, r.input_len, self.spec.vocab)
+            self.prompts[r.id] = p
+        # t0 on every local device
+        self.t0 = {}
+        for s, exe in self.exe.items():
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(exe.stream)
+            self.t0[s] = ev
+        if self.throttle:
+            self._start_gates()
+
+    def admit(self, mb, now_ns: int) -> None:
+        slot = self.free_slots.pop()
+        R = len(mb.request_ids)
+        decode = mb.phase is BatchPhase.DECODE
+        if mb.phase is BatchPhase.MIXED:
+            raise pipelink.ConfigError("mixed micro-batch reached the B200 backend")
+        reqs = [self.driver._requests[rid] for rid in mb.request_ids]
+        rows = np.empty((R, self.max_blocks), dtype=np.int32)
+        for i, r in enumerate(reqs):
+            bt = self.bt_rows.get(r.id)
+            if bt is None:
+                need = -(-(r.input_len + r.output_len) // BLOCK_SIZE)
+                if len(self.free_blocks) < need:
+                    raise pipelink.ConfigError("paged KV cache exhausted")
+                bt = np.zeros(self.max_blocks, dtype=np.int32)
+                bt[:need] = [self.free_blocks.pop() for _ in range(need)]
+                self.bt_rows[r.id] = bt
+            rows[i] = bt
+        ridx = np.array([self.rid_index[r.id] for r in reqs], dtype=np.int32)
+        out_pos = np.array([r.tokens_emitted for r in reqs], dtype=np.int32)
+        if decode:
+            T = R
+            pos = np.array([r.input_len + r.tokens_emitted - 1 for r in reqs], dtype=np.int64)
+            slots = rows[np.arange(R), pos // BLOCK_SIZE].astype(np.int64) * BLOCK_SIZE + pos % BLOCK_SIZE
+            cu = np.arange(R + 1, dtype=np.int32)
+            ctx = pos + 1
+            last = np.arange(R, dtype=np.int32)
+            meta = build_meta(T, R, self.max_blocks, pos, slots, ridx, cu, ctx, last, rows)
+            rec = _MbRec(slot, T, R, True, 1, int(ctx.max()), meta, None,
+                         np.concatenate([ridx, out_pos]).astype(np.int32), mb.request_ids)
+        else:
+            lens = np.array([r.input_len for r in reqs], dtype=np.int64)
+            T = int(lens.sum())
+            cu = np.zeros(R + 1, dtype=np.int64)
+            np.cumsum(lens, out=cu[1:])
+            pos = np.arange(T, dtype=np.int64) - np.repeat(cu[:-1], lens)
+            req_of = np.repeat(np.arange(R), lens)
+            slots = rows[req_of, pos // BLOCK_SIZE].astype(np.int64) * BLOCK_SIZE + pos % BLOCK_SIZE
+            meta = build_meta(T, R, self.max_blocks, pos, slots, np.repeat(ridx, lens), cu, lens,
+                              cu[1:] - 1, rows)
+            ids = np.concatenate([self.prompts[r.id] for r in reqs])
+            rec = _MbRec(slot, T, R, False, int(lens.max()), int(lens.max()), meta, ids,
+                         np.concatenate([ridx, out_pos]).astype(np.int32), mb.request_ids)
+        self.mbs[mb.id] = rec
+
+    def compute(self, s: int, mb, now_ns: int) -> None:
+        exe = self.exe.get(s)
+        if exe is None:
+            return
+        rec = self.mbs[mb.id]
+        st = exe.stream
+        # run-ahead cap (also guards the pinned staging rings)
+        q = self.throttle_ev[s]
+        if len(q) >= RUN_AHEAD:
+            q.popleft().synchronize()
+        k = rec.slot
+        if self.ev_send[s][k] is not None:
+            st.wait_event(self.ev_send[s][k])
+        if s > 0 and self.ev_recv[s][k] is not None:
+            st.wait_event(self.ev_recv[s][k])
+        if s == 0 and rec.decode and self.fb_events:
+            st.wait_event(self.fb_events[-1][0])
+            if self.first_decode_ev is None:
+                self.first_decode_ev = torch.cuda.Event(enable_timing=True)
+                self.first_decode_ev.record(st)
+        lib = N.lib()
+        i, buf = self.meta_ring[s].take()
+        nb = rec.meta.nbytes
+        buf[:nb].numpy()[:] = rec.meta.view(np.uint8)
+        lib.pl_memcpy_async(exe.meta_dev.data_ptr(), buf.data_ptr(), nb, st.cuda_stream)
+        self.meta_ring[s].mark(i, st)
+        if s == 0 and not rec.decode:
+            j, ib = self.ids_ring[s].take()
+            ib[: rec.ids.nbytes].numpy()[:] = rec.ids.view(np.uint8)
+            lib.pl_memcpy_async(exe.ids_dev.data_ptr(), ib.data_ptr(), rec.ids.nbytes, st.cuda_stream)
+            self.ids_ring[s].mark(j, st)
+        exe.forward(k, rec.T, rec.R, rec.decode, rec.max_seqlen, rec.max_ctx,
+                    last_token=self.last_token if (s == 0) else None)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        self.ev_comp[s][k] = ev
+        q.append(ev)
+        if self.S == 1:
+            self._scatter(rec, exe.out_ids[k], st)
+
+    def emit(self, link: int, payload, chunk, offset: int, now_ns: int) -> None:
+        mb_id = payload.micro_batch_id
+        rec = self.mbs[mb_id]
+        k = rec.slot
+        is_ret = link == self.S - 1
+        src = self.S - 1 if is_ret else link
+        dst = 0 if is_ret else link + 1
+        src_local, dst_local = self.pl.local(src), self.pl.local(dst)
+        first = offset == 0
+        last = chunk.is_last
+        size = chunk.size_bytes
+        if src_local:
+            sst = self.send_stream[src]
+            if first:
+                sst.wait_event(self.ev_comp[src][k])
+            sbuf = (self.exe[src].out_ids[k] if is_ret else self.exe[src].hidden[k]).data_ptr() + offset
+        if dst_local:
+            dbuf = (self.ids_recv[k] if is_ret else self.exe[dst].hidden[k]).data_ptr() + offset
+            prev_send = self.ev_send[dst][k]
+        if src_local and dst_local:
+            # same process: device (or peer) copy on the source's send stream
+            if first and prev_send is not None:
+                sst.wait_event(prev_send)
+            N.check(N.lib().pl_memcpy_async(dbuf, sbuf, size, sst.cuda_stream), "pl_memcpy_async")
+            if last:
+                ev = torch.cuda.Event()
+                ev.record(sst)
+                self.ev_send[src][k] = ev
+                self._recv_done(dst, rec, ev, is_ret)
+            return
+        if src_local:
+            comm = self.comms[link]
+            N.check(N.lib().pl_p2p_send(comm, sbuf, size, 1, sst.cuda_stream), "pl_p2p_send")
+            if last:
+                ev = torch.cuda.Event()
+                ev.record(sst)
+                self.ev_send[src][k] = ev
+        if dst_local:
+            rst = self.recv_stream[dst]
+            if first and prev_send is not None:
+                rst.wait_event(prev_send)
+            comm = self.comms[link]
+            N.check(N.lib().pl_p2p_recv(comm, dbuf, size, 0, rst.cuda_stream), "pl_p2p_recv")
+            if last:
+                ev = torch.cuda.Event()
+                ev.record(rst)
+                self._recv_done(dst, rec, ev, is_ret)
+
+    def _recv_done(self, dst: int, rec: _MbRec, ev, is_ret: bool) -> None:
+        if not is_ret:
+            self.ev_recv[dst][rec.slot] = ev
+            return
+        rst = self.recv_stream[0]
+        rst.wait_event(ev)
+        self._scatter(rec, self.ids_recv[rec.slot], rst)
+
+    def _scatter(self, rec: _MbRec, ids: torch.Tensor, stream) -> None:
+        """Return hop landed on the head: last_token / gen_tokens <- ids."""
+        i, buf = self.scatter_ring.take()
+        nb = rec.scatter.nbytes
+        buf[:nb].numpy()[:] = rec.scatter.view(np.uint8)
+        dev = self.scatter_dev[rec.slot]
+        lib = N.lib()
+        lib.pl_memcpy_async(dev.data_ptr(), buf.data_ptr(), nb, stream.cuda_stream)
+        self.scatter_ring.mark(i, stream)
+        R = rec.R
+        N.check(lib.pl_token_scatter(ids.data_ptr(), dev.data_ptr(), dev.data_ptr() + 4 * R, R,
+                                     self.last_token.data_ptr(), self.gen_tokens.data_ptr(),
+                                     self.gen_tokens.stride(0), stream.cuda_stream), "pl_token_scatter")
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        self.fb_events.append((ev, rec.rids))
+
+    def delivered(self, link: int, payload, mb, now_ns: int) -> None:
+        pass
+
+    def feedback(self, mb, now_ns: int) -> None:
+        rec = self.mbs.pop(mb.id)
+        self.free_slots.append(rec.slot)
+        for rid in mb.request_ids:
+            r = self.driver._requests[rid]
+            if r.state is RequestState.FINISHED:
+                bt = self.bt_rows.pop(rid, None)
+                if bt is not None:
+                    need = -(-(r.input_len + r.output_len) // BLOCK_SIZE)
+                    self.free_blocks.extend(int(b) for b in bt[:need][::-1])
+
+    def finish(self, result) -> None:
+        """Join all local streams, stop the clock, collect tokens and real timings."""
+        self.timing = {}
+        ends = {}
+        for s, exe in self.exe.items():
+            for st in (self.send_stream[s], self.recv_stream[s]):
+                ev = torch.cuda.Event()
+                ev.record(st)
+                exe.stream.wait_event(ev)
+            end = torch.cuda.Event(enable_timing=True)
+            end.record(exe.stream)
+            ends[s] = end
+        for s, exe in self.exe.items():
+            ends[s].synchronize()
+        self.run_time_s = max((self.t0[s].elapsed_time(ends[s]) / 1e3 for s in self.exe), default=0.0)
+        self.tokens = None
+        if 0 in self.exe:
+            gen = self.gen_tokens.cpu().numpy()
+            self.tokens = {r.id: gen[self.rid_index[r.id], : r.tokens_emitted].copy()
+                           for r in result.requests}
+            t0 = self.t0[0]
+            self.fb_times_s = [t0.elapsed_time(ev) / 1e3 for ev, _ in self.fb_events]
+            self.decode_start_s = (t0.elapsed_time(self.first_decode_ev) / 1e3
+                                   if self.first_decode_ev is not None else None)
+
+    # ---------------------------------------------------------- throttle
+    def _start_gates(self) -> None:
+        raise pipelink.ConfigError("link throttle mode is provided by ThrottledGpuBackend")

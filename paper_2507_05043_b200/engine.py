@@ -1,0 +1,145 @@
+"""B200PipelineEngine: the drop-in for ``pipelink.PipelineEngine`` with real compute and links.
+
+    from pipelink import EngineConfig, ControllerConfig, ...      # unchanged reference API
+    from paper_2507_05043_b200 import B200PipelineEngine, LLAMA3_8B
+
+    engine = B200PipelineEngine(cfg, cluster, stage_profiles, decoder=LLAMA3_8B)
+    result = engine.run(trace)          # pipelink.RunResult, schedule == PipelineEngine's
+    result.b200.tokens[rid]             # greedy token ids generated on the GPUs
+    result.b200.decode_tok_s            # measured on the device clock
+
+Same constructor arguments and ``run(trace, horizon_s)`` contract as the
+reference (engine.py:264-294, 509-600), plus the decoder shape the reference
+cannot know (its ModelSpec has no heads/FFN/vocab).  Under ``torchrun`` each
+rank constructs the engine identically and owns ``S / world_size`` contiguous
+stages; hops between ranks are NCCL P2P.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._pipelink import pipelink
+from .backend import GpuBackend, Placement
+from .driver import PipelineDriver
+from .spec import DecoderSpec
+
+nearest_rank = pipelink.metrics.nearest_rank
+
+
+@dataclass
+class B200Stats:
+    """Device-clock measurements of one run (rank-local; tokens on the head rank)."""
+
+    run_time_s: float
+    tokens: dict | None = None          # rid -> np.ndarray of generated ids (head rank)
+    token_times_s: dict | None = None   # rid -> device time of each emitted token
+    decode_start_s: float | None = None
+    total_tokens: int = 0
+    decode_tokens: int = 0
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def throughput_tok_s(self) -> float:
+        return self.total_tokens / self.run_time_s if self.run_time_s > 0 else 0.0
+
+    @property
+    def decode_time_s(self) -> float | None:
+        if self.decode_start_s is None:
+            return None
+        return self.run_time_s - self.decode_start_s
+
+    @property
+    def decode_tok_s(self) -> float | None:
+        t = self.decode_time_s
+        return self.decode_tokens / t if t else None
+
+    def tpot_p50_s(self) -> float | None:
+        if not self.token_times_s:
+            return None
+        tp = sorted((ts[-1] - ts[0]) / (len(ts) - 1) for ts in self.token_times_s.values() if len(ts) >= 2)
+        return nearest_rank(tp, 50) if tp else None
+
+    def ttft_p50_s(self) -> float | None:
+        if not self.token_times_s:
+            return None
+        return nearest_rank(sorted(ts[0] for ts in self.token_times_s.values()), 50)
+
+
+def create_link_comms(placement: Placement) -> dict:
+    """One 2-rank NCCL communicator per directed hop whose stages sit on different ranks.
+    Unique ids travel over the default torch.distributed group (rendezvous only)."""
+    import torch.distributed as dist
+
+    S = placement.n_stages
+    comms = {}
+    if S < 2:
+        return comms
+    me = placement.rank
+    for link in range(S):
+        src = S - 1 if link == S - 1 else link
+        dst = 0 if link == S - 1 else link + 1
+        ra, rb = placement.stage_rank[src], placement.stage_rank[dst]
+        if ra == rb:
+            continue
+        obj = [None]
+        if me == ra:
+            buf = (C.c_uint8 * 128)()
+            N.call("pl_nccl_unique_id", buf, 128)
+            obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=ra)
+        if me in (ra, rb):
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+            h = C.c_void_p()
+            N.call("pl_comm_init_rank", uid, 2, 0 if me == ra else 1, C.byref(h))
+            comms[link] = h
+    return comms
+
+
+class B200PipelineEngine(PipelineDriver):
+    def __init__(self, cfg, cluster, stage_profiles, *, decoder: DecoderSpec, seed: int = 0,
+                 devices: list | None = None, prompts: dict | None = None):
+        if cfg.model.hidden_dim != decoder.d or cfg.model.dtype_bytes != 2:
+            raise pipelink.ConfigError("cfg.model must describe the decoder's bf16 residual stream "
+                                       "(use DecoderSpec.model_spec())")
+        if cfg.partition.num_layers != decoder.num_layers:
+            raise pipelink.ConfigError("partition layer count != decoder layers")
+        S = len(cfg.partition.stages)
+        world, rank = 1, 0
+        if torch.distributed.is_available() and torch.distributed.is_initialized():
+            world, rank = torch.distributed.get_world_size(), torch.distributed.get_rank()
+        self.placement = Placement(S, world, rank, devices)
+        comms = create_link_comms(self.placement) if world > 1 else {}
+        self.gpu = GpuBackend(decoder, cfg, self.placement, seed=seed, prompts=prompts, comms=comms)
+        super().__init__(cfg, cluster, stage_profiles, backend=self.gpu)
+        self._comms = comms
+
+    def run(self, trace, horizon_s: float | None = None):
+        result = super().run(trace, horizon_s)
+        g = self.gpu
+        stats = B200Stats(run_time_s=g.run_time_s, tokens=g.tokens, decode_start_s=g.decode_start_s)
+        if g.tokens is not None:
+            times: dict = {}
+            for t, (ev, rids) in zip(g.fb_times_s, g.fb_events):
+                for rid in rids:
+                    times.setdefault(rid, []).append(t)
+            stats.token_times_s = times
+            stats.total_tokens = sum(len(v) for v in g.tokens.values())
+            stats.decode_tokens = sum(max(0, len(v) - 1) for v in g.tokens.values())
+        result.b200 = stats
+        return result
+
+    def prepare(self, trace) -> None:
+        """Allocate weights, KV cache and buffers for `trace` ahead of the first run."""
+        self.gpu.prepare(trace)
+
+    def close(self) -> None:
+        self.gpu.close()
+        for h in self._comms.values():
+            N.lib().pl_comm_destroy(h)
+        self._comms = {}

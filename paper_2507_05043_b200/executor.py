@@ -19,7 +19,6 @@ HBM layout per stage (bf16 unless noted):
 from __future__ import annotations
 
 import ctypes as C
-import math
 
 import numpy as np
 import torch
@@ -205,10 +204,3 @@ def build_meta(T: int, R: int, max_blocks: int, pos, slot, req_slot, cu, ctx, la
         out[o:o + n] = np.asarray(arr, dtype=np.int32).reshape(-1)[:n]
         o += n
     return out
-
-
-def math_ceil_div(a: int, b: int) -> int:
-    return -(-a // b)
-
-
-__all__ = ["StageExecutor", "build_meta", "meta_len", "math_ceil_div", "math"]
