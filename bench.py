@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark: decode throughput of the B200 pipeline (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one pipeline stage per GPU)
+
+Workload (BASELINE.json configs[1], pipeline depth = GPU count): Llama-3-8B-shape
+random-init decoder (hash init, bf16), 64 concurrent requests, prompt 512,
+output 256, ``ControllerConfig(max_batched_tokens=32768, max_batch_size=64)``,
+256 KiB prefill chunks, NVLink links.  One step = one full serving run of the
+trace through ``B200PipelineEngine.run`` (prefill + 255 decode iterations);
+the schedule is the reference scheduler's (bit-exact vs pipelink) on measured
+stage profiles.
+
+value = generated tokens / serving span on the device clock (max over ranks)
+        -- pipelink's MetricsReport.throughput_tok_s definition (metrics.py:78-117)
+e2e   = the same metric with the host wall clock around the public API call
+        (prompt ids from host memory in, generated ids to host memory out)
+Extra keys: decode_window_tok_s (tokens after the first decode iteration /
+device time), p50 TPOT/TTFT, the path roofline of SURVEY §8(d), and the
+dominant kernel's roofline (gate_up GEMM of decode micro-batches, timed live
+with CUDA events on the stage's compute stream).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MEASURED = ROOT / "MEASURED_PEAKS.json"
+
+
+def peaks():
+    try:
+        d = json.loads(MEASURED.read_text())
+        return d["hbm_gbs"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.summary = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return False
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        self.summary = {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                        "reasons": sorted(reasons), "samples": len(sm)}
+        return False
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group(backend="cuda:nccl,cpu:gloo", world_size=world, rank=rank,
+                                device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return x
+
+
+def barrier():
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.barrier()
+
+
+def broadcast(obj, src=0):
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        box = [obj]
+        dist.broadcast_object_list(box, src=src)
+        return box[0]
+    return obj
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+
+    world, rank, local = dist_setup()
+    import pipelink  # noqa: F401  (via the package's locator)
+    from paper_2507_05043_b200 import PRESETS, deploy
+    from paper_2507_05043_b200 import _native as N
+    from paper_2507_05043_b200.engine import B200PipelineEngine
+    from paper_2507_05043_b200.profiler import gather_profiles, profile_stage
+
+    N.lib()
+    import pipelink as PL
+
+    S = args.gpus
+    if world not in (1, S):
+        raise SystemExit(f"--gpus {S} but WORLD_SIZE {world}")
+    spec = PRESETS[args.model]
+    if args.layers:
+        spec = spec.with_(num_layers=args.layers)
+    cluster = deploy.b200_cluster(S)
+    plan = deploy.plan(cluster, spec, S)
+    ctrl = PL.ControllerConfig(max_batched_tokens=args.max_batched_tokens, max_batch_size=args.batch)
+    cfg = deploy.engine_config(plan, spec, ctrl)
+    trace = deploy.uniform_trace(args.batch, args.prompt, args.decode)
+    placeholder = [PL.synth_profile(hi - lo, 1e-6, 1e-4, stage_id=i)
+                   for i, (_, (lo, hi)) in enumerate(plan.stages)]
+    t_setup = time.time()
+    eng = B200PipelineEngine(cfg, cluster, placeholder, decoder=spec, seed=0)
+    eng.prepare(trace)
+    local_prof = {s: profile_stage(exe, ctx=args.prompt) for s, exe in eng.gpu.exe.items()}
+    profiles = gather_profiles(local_prof, S)
+    eng.set_stage_profiles(profiles)
+    t_setup = time.time() - t_setup
+
+    # dominant kernel probe: the first layer of each local stage
+    for exe in eng.gpu.exe.values():
+        exe.probe(0)
+    for _ in range(args.warmup):
+        barrier()
+        eng.run(trace)
+    for exe in eng.gpu.exe.values():
+        exe.probe_read()          # drop warm-up records
+        exe.probe(0)
+
+    dev_idx = torch.cuda.current_device() if world > 1 else 0
+    lib = N.lib()
+    runs = []
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = lib.pl_launch_count()
+    with ClockSampler(dev_idx) as clk:
+        for _ in range(args.steps):
+            barrier()
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            res = eng.run(trace)              # public API: host prompts in, host tokens out
+            wall = time.perf_counter() - w0
+            runs.append((res, wall))
+    launches = lib.pl_launch_count() - launches0
+    torch.cuda.synchronize()
+
+    # device-clock span per run: max over ranks
+    dev_times = [allreduce_max(r.b200.run_time_s) for r, _ in runs]
+    walls = [allreduce_max(w) for _, w in runs]
+    head = runs[-1][0].b200
+    decode_starts = broadcast([r.b200.decode_start_s for r, _ in runs] if rank == 0 else None)
+    tokens_per_run = args.batch * args.decode
+    decode_tokens_per_run = args.batch * (args.decode - 1)
+    value = tokens_per_run * len(runs) / sum(dev_times)
+    e2e = tokens_per_run * len(runs) / sum(walls)
+    dec_windows = [t - s for t, s in zip(dev_times, decode_starts) if s is not None]
+    decode_window_tok_s = decode_tokens_per_run * len(dec_windows) / sum(dec_windows) if dec_windows else None
+    tpot = broadcast(head.tpot_p50_s() if rank == 0 else None)
+    ttft = broadcast(head.ttft_p50_s() if rank == 0 else None)
+
+    hbm, tfl, peak_src = peaks()
+    # ---- dominant kernel: gate_up GEMM of decode micro-batches (probe, CUDA events)
+    gu_ms, gu_T = [], []
+    qkv_ms, o_ms, down_ms, attn_ms = [], [], [], []
+    for exe in eng.gpu.exe.values():
+        ms, meta = exe.probe_read()
+        for row, (phase, T) in zip(ms, meta):
+            if phase == 1:
+                qkv_ms.append(row[0]); attn_ms.append(row[1]); o_ms.append(row[2])
+                gu_ms.append(row[3]); down_ms.append(row[4]); gu_T.append(T)
+    roof = None
+    if gu_ms:
+        avg_T = float(np.mean(gu_T))
+        w_bytes = 2 * spec.ffn * spec.d * 2
+        act_bytes = avg_T * spec.d * 2 + avg_T * spec.ffn * 2
+        alg = w_bytes + act_bytes
+        avg_s = float(np.mean(gu_ms)) / 1e3
+        achieved = alg / avg_s / 1e9
+        roof = {"kernel": "gemm_tc_kernel<SWAP> gate_up+SwiGLU (decode, incl. split-K reduce)",
+                "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": int(alg), "avg_launch_us": round(avg_s * 1e6, 2),
+                "avg_T": round(avg_T, 2), "launches_timed": len(gu_ms), "peak_source": peak_src,
+                "other_decode_kernels_avg_us": {
+                    "qkv_gemm": round(float(np.mean(qkv_ms)) * 1e3, 2),
+                    "rope+attention": round(float(np.mean(attn_ms)) * 1e3, 2),
+                    "o_gemm": round(float(np.mean(o_ms)) * 1e3, 2),
+                    "down_gemm": round(float(np.mean(down_ms)) * 1e3, 2)}}
+    roofs = [None] * world
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_gather_object(roofs, roof)
+        # report the stage whose gate_up runs slowest (the pipeline's binding stage)
+        cands = [r for r in roofs if r]
+        roof = min(cands, key=lambda r: r["frac"]) if cands else None
+
+    # ---- path roofline for the decode window from the micro-batch log
+    path = decode_path_roofline(spec, eng, runs[-1][0], hbm, tfl)
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import cpu_baseline as CB
+            est = CB.estimate(spec, args.batch, args.prompt, args.decode)
+            cpu = {"value": round(est["tok_s"], 3), "unit": "tok/s", "cores": est["threads"],
+                   "kind": "port", "sample": est["sample"],
+                   "decode_tok_s": round(est["decode_tok_s"], 3)}
+        h2d = args.batch * args.prompt * 8
+        d2h = args.batch * args.decode * 8
+        out = {
+            "metric": "decode tokens/sec (generated tokens / serving span, pipelink MetricsReport "
+                      "definition) at N B200 pipeline stages; p50 TPOT",
+            "value": round(value, 2), "unit": "tok/s", "n_gpus": S, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * sum(dev_times) / len(dev_times), 3),
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (hash-init weights, hash prompts)",
+            "config": {"workload": f"{spec.name} {S}-stage pipeline, {args.batch} requests, "
+                                   f"prompt {args.prompt} / decode {args.decode}",
+                       "model": spec.name, "layers": spec.num_layers, "stages": S,
+                       "global_batch": args.batch, "seq_len": args.prompt, "decode_len": args.decode,
+                       "parallelism": f"pp{S}", "max_batched_tokens": args.max_batched_tokens,
+                       "chunk_size": 262144, "l2": "inputs larger than L2 (16 GB weights streamed per step)"},
+            "e2e": {"value": round(e2e, 2), "unit": "tok/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "decode_window_tok_s": round(decode_window_tok_s, 2) if decode_window_tok_s else None,
+            "tpot_p50_ms": round(tpot * 1e3, 4) if tpot else None,
+            "ttft_p50_ms": round(ttft * 1e3, 3) if ttft else None,
+            "roofline": roof,
+            "path_roofline": path,
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary,
+            "setup_s": round(t_setup, 1),
+            "schedule": {"decisions": len(runs[-1][0].decisions),
+                         "n_microbatches": sorted({d.n_microbatches for _, d in runs[-1][0].decisions})},
+        }
+    eng.close()
+    return out
+
+
+def decode_path_roofline(spec, eng, res, hbm_gbs, tflops):
+    """Roofline decode tok/s for the decode micro-batches of `res`."""
+    plan = eng.cfg.partition
+    S = len(plan.stages)
+    layer_b = spec.layer_bytes()
+    head_b = spec.vocab * spec.d * 2 + spec.d * 2
+    kv_tok_layer = spec.kv_bytes_per_token_layer()
+    # micro-batch composition from the decisions/events: recompute from the request log
+    # (decode micro-batches: tokens = requests; ctx grows by one per step)
+    per_stage_s = [0.0] * S
+    dec_tokens = 0
+    mbs = eng.gpu.mb_log
+    if not mbs:
+        return None
+    for (phase, R, ctx_sum) in mbs:
+        if phase != "decode":
+            continue
+        dec_tokens += R
+        for s, (_, (lo, hi)) in enumerate(plan.stages):
+            L = hi - lo
+            wb = L * layer_b + (head_b if s == S - 1 else 0)
+            kvb = ctx_sum * L * kv_tok_layer
+            flops = 2 * R * (L * spec.layer_params() + (spec.vocab * spec.d if s == S - 1 else 0))
+            per_stage_s[s] += max((wb + kvb) / (hbm_gbs * 1e9), flops / (tflops * 1e12))
+    t = max(per_stage_s)
+    return {"decode_roofline_tok_s": round(dec_tokens / t, 1), "binding_stage": per_stage_s.index(t),
+            "definition": "sum over decode micro-batches of max(weight+KV bytes / HBM, flops / bf16 "
+                          "peak) on the slowest stage (SURVEY 8(d)); NVLink activation time omitted "
+                          "(< 0.1%)"}
+
+
+def run_reference(args):
+    """--impl reference: the reference has no CPU forward; its compute is a latency table.
+    The CPU implementation of the path is the oracle decoder, timed on bounded samples."""
+    world, rank, local = dist_setup()
+    if rank != 0:
+        return None
+    from oracle import cpu_baseline as CB
+    from paper_2507_05043_b200 import PRESETS
+
+    spec = PRESETS[args.model]
+    if args.layers:
+        spec = spec.with_(num_layers=args.layers)
+    vals, t0 = [], time.time()
+    for _ in range(max(1, args.steps)):
+        est = CB.estimate(spec, args.batch, args.prompt, args.decode, reps=1)
+        vals.append(est["tok_s"])
+    v = sum(vals) / len(vals)
+    return {
+        "impl": "reference", "metric": "decode tokens/sec (generated tokens / serving span, pipelink "
+                                       "MetricsReport definition) at N B200 pipeline stages; p50 TPOT",
+        "value": round(v, 3), "unit": "tok/s", "n_gpus": args.gpus, "steps": len(vals),
+        "warmup": args.warmup, "higher_is_better": True, "dtype": "bf16 storage / fp32 math",
+        "data": "synthetic", "config": {"workload": f"{spec.name} {args.gpus}-stage pipeline, "
+                                                    f"{args.batch} requests, prompt {args.prompt} / "
+                                                    f"decode {args.decode}", "model": spec.name},
+        "cpu_baseline": {"value": round(v, 3), "unit": "tok/s", "cores": est["threads"], "kind": "port",
+                         "sample": est["sample"]},
+        "e2e": {"value": round(v, 3), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": round(time.time() - t0, 1),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--model", default="llama3-8b-shape")
+    ap.add_argument("--layers", type=int, default=0, help="truncate the model (debug only)")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--prompt", type=int, default=512)
+    ap.add_argument("--decode", type=int, default=256)
+    ap.add_argument("--max-batched-tokens", type=int, default=32768)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    out = run_reference(args) if args.impl == "reference" else run_b200(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -61,6 +61,8 @@ typedef enum pl_epilogue {
 PL_API int32_t pl_abi_version(void);
 PL_API const char* pl_last_error(void);
 PL_API int32_t pl_device_sm_count(int32_t device);
+/* Number of libb200link kernels launched by this process so far (bench.py's gpu_launches). */
+PL_API int64_t pl_launch_count(void);
 
 /* ---------------------------------------------------------------- init --- */
 

@@ -18,8 +18,9 @@ import numpy as np
 M32 = np.uint32(0xFFFFFFFF)
 
 
-def _mix(x: np.ndarray) -> np.ndarray:
-    x = x.astype(np.uint32, copy=True)
+def _mix(x: np.ndarray, inplace: bool = False) -> np.ndarray:
+    if not inplace:
+        x = x.astype(np.uint32, copy=True)
     with np.errstate(over="ignore"):
         x ^= x >> np.uint32(16)
         x *= np.uint32(0x7FEB352D)
@@ -41,17 +42,22 @@ def keys(seed: int, tensor_id: int) -> tuple[int, int]:
 
 def hash_u32(n: int, seed: int, tensor_id: int, start: int = 0) -> np.ndarray:
     key, key2 = keys(seed, tensor_id)
-    i = np.arange(start, start + n, dtype=np.uint64).astype(np.uint32)
+    h = np.arange(n, dtype=np.uint32)          # i < 2^32 (tensors are < 2^32 elements)
     with np.errstate(over="ignore"):
-        h = _mix((i + np.uint32(key)).astype(np.uint32)) ^ np.uint32(key2)
-    return _mix(h)
+        h += np.uint32((start + key) & 0xFFFFFFFF)
+        _mix(h, inplace=True)
+        h ^= np.uint32(key2)
+    return _mix(h, inplace=True)
 
 
 def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even fp32 -> bf16, returned as uint16 bit patterns."""
-    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
-    rounding = ((u >> 16) & 1) + 0x7FFF
-    return ((u + rounding) >> 16).astype(np.uint16)
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    with np.errstate(over="ignore"):
+        r = (u >> np.uint32(16)) & np.uint32(1)
+        r += np.uint32(0x7FFF)
+        r += u                                   # finite inputs never wrap
+    return (r >> np.uint32(16)).astype(np.uint16)
 
 
 def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
@@ -59,12 +65,21 @@ def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
 
 
 def hash_bf16_bits(n: int, seed: int, tensor_id: int, scale: float, offset: float = 0.0,
-                   start: int = 0) -> np.ndarray:
-    h = hash_u32(n, seed, tensor_id, start)
-    v = ((h >> np.uint32(8)).astype(np.int64) - 8388608).astype(np.float32)
+                   start: int = 0, chunk: int = 1 << 24) -> np.ndarray:
+    out = np.empty(n, dtype=np.uint16)
     mult = np.float32(scale) * np.float32(2.0 ** -23)
-    w = (v * mult).astype(np.float32) + np.float32(offset)
-    return f32_to_bf16_bits(w.astype(np.float32))
+    for a in range(0, n, chunk):
+        m = min(chunk, n - a)
+        h = hash_u32(m, seed, tensor_id, start + a)
+        h >>= np.uint32(8)
+        v = h.view(np.int32)
+        v -= np.int32(8388608)
+        w = v.astype(np.float32)
+        w *= mult
+        if offset:
+            w += np.float32(offset)
+        out[a:a + m] = f32_to_bf16_bits(w)
+    return out
 
 
 def hash_tokens(n: int, seed: int, tensor_id: int, vocab: int, start: int = 0) -> np.ndarray:

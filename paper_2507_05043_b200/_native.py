@@ -54,6 +54,7 @@ _SIGS = {
     "pl_abi_version": (i32, []),
     "pl_last_error": (C.c_char_p, []),
     "pl_device_sm_count": (i32, [i32]),
+    "pl_launch_count": (i64, []),
     "pl_fill_hash_bf16": (i32, [vp, i64, u32, u32, f32, f32, vp]),
     "pl_embed": (i32, [vp, vp, vp, vp, i64, i64, i32, vp, vp]),
     "pl_rmsnorm": (i32, [vp, i64, vp, vp, f32, i64, i32, vp, i64, vp]),

@@ -200,6 +200,7 @@ class GpuBackend(Backend):
         self.bt_rows: dict[int, np.ndarray] = {}
         self.mbs: dict[int, _MbRec] = {}
         self.fb_events: list = []   # (event, mb request ids)
+        self.mb_log: list = []      # (phase, R, sum of contexts) per admitted micro-batch
         self.first_decode_ev = None
         self.prompts = {}
         for r in reqs:
@@ -249,6 +250,7 @@ class GpuBackend(Backend):
             meta = build_meta(T, R, self.max_blocks, pos, slots, ridx, cu, ctx, last, rows)
             rec = _MbRec(slot, T, R, True, 1, int(ctx.max()), meta, None,
                          np.concatenate([ridx, out_pos]).astype(np.int32), mb.request_ids)
+            self.mb_log.append(("decode", R, int(ctx.sum())))
         else:
             lens = np.array([r.input_len for r in reqs], dtype=np.int64)
             T = int(lens.sum())
@@ -262,6 +264,7 @@ class GpuBackend(Backend):
             ids = np.concatenate([self.prompts[r.id] for r in reqs])
             rec = _MbRec(slot, T, R, False, int(lens.max()), int(lens.max()), meta, ids,
                          np.concatenate([ridx, out_pos]).astype(np.int32), mb.request_ids)
+            self.mb_log.append(("prefill", R, T))
         self.mbs[mb.id] = rec
 
     def compute(self, s: int, mb, now_ns: int) -> None:

@@ -1,5 +1,6 @@
 // extern "C" entry points of libb200link (declared in include/b200link.h) and
 // the thread-local error channel.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -11,6 +12,7 @@ namespace pl {
 
 namespace {
 thread_local char g_err[1024] = "";
+std::atomic<int64_t> g_launches{0};
 }
 
 int set_error(int code, const char* fmt, ...) {
@@ -26,6 +28,7 @@ int set_cuda_error(cudaError_t e, const char* what) {
 }
 
 int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, what);
   return PL_OK;
@@ -44,6 +47,8 @@ extern "C" {
 int32_t pl_abi_version(void) { return PL_ABI_VERSION; }
 
 const char* pl_last_error(void) { return g_err; }
+
+int64_t pl_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int32_t pl_device_sm_count(int32_t device) {
   int n = 0;

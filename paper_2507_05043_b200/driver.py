@@ -123,6 +123,14 @@ class PipelineDriver:
         self._decision_cache: dict = {}
         self._compute_ns_cache: dict = {}
 
+    def set_stage_profiles(self, stage_profiles) -> None:
+        """Swap in measured profiles (startup profiling) before the next run."""
+        if len(stage_profiles) != len(self.stage_profiles):
+            raise pipelink.ConfigError("profile count must equal the stage count")
+        self.stage_profiles = list(stage_profiles)
+        self._decision_cache.clear()
+        self._compute_ns_cache.clear()
+
     # --------------------------------------------------------------- helpers
     def _post(self, t: int, kind: int, subject: int, data=None) -> None:
         heapq.heappush(self._heap, (t, kind, subject, self._seq, data))
