@@ -145,8 +145,7 @@ def run_b200(args):
     import torch
 
     world, rank, local = dist_setup()
-    import pipelink  # noqa: F401  (via the package's locator)
-    from paper_2507_05043_b200 import PRESETS, deploy
+    from paper_2507_05043_b200 import PRESETS, deploy  # locates the reference pipelink first
     from paper_2507_05043_b200 import _native as N
     from paper_2507_05043_b200.engine import B200PipelineEngine
     from paper_2507_05043_b200.profiler import gather_profiles, profile_stage

@@ -84,7 +84,9 @@ PL_API int32_t pl_rmsnorm(const void* x, int64_t ldx, const int32_t* row_idx, co
                    int64_t rows, int32_t d, void* out, int64_t ldo, void* stream);
 
 /* C[T, N] = epilogue(X[T, K] . W[N, K]^T) on tcgen05 tensor cores.  workspace:
- * pl_gemm_workspace_bytes(T, N, K, epilogue) bytes (split-K partials / argmax). */
+ * pl_gemm_workspace_bytes(T, N, K, epilogue) bytes (split-K arrival counters +
+ * partials / argmax); zero it once before first use -- every call leaves its
+ * counters at zero again. */
 PL_API int64_t pl_gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t epilogue);
 PL_API int32_t pl_gemm(const void* X, int64_t ldx, const void* W, int64_t ldw, const void* bias, void* C,
                 int64_t ldc, const void* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,
@@ -106,10 +108,10 @@ PL_API int32_t pl_attn_prefill(const void* qkv, int64_t ldqkv, const int32_t* cu
                         void* out, int64_t ldo, void* stream);
 
 /* One query token per request over its paged KV (ctx_len[r] tokens incl. the
- * current one).  q rows: [R, Hq*hd] with leading dim ldq. */
+ * current one; caches hold num_blocks blocks).  q rows: [R, Hq*hd], leading dim ldq. */
 PL_API int64_t pl_attn_decode_workspace_bytes(int32_t R, int32_t Hq, int32_t max_ctx, int32_t hd);
 PL_API int32_t pl_attn_decode(const void* q, int64_t ldq, const void* k_cache, const void* v_cache,
-                       int32_t block_size, const int32_t* block_table, int32_t max_blocks,
+                       int64_t num_blocks, int32_t block_size, const int32_t* block_table, int32_t max_blocks,
                        const int32_t* ctx_len, int32_t R, int32_t max_ctx, int32_t Hq, int32_t Hkv,
                        int32_t hd, float scale, void* out, int64_t ldo, void* workspace,
                        int64_t workspace_bytes, void* stream);
@@ -147,6 +149,7 @@ typedef struct pl_stage_config {
   int64_t vocab;
   float eps;
   int32_t block_size, max_blocks_per_req, max_pos;
+  int64_t num_blocks; /* KV cache blocks per layer */
   int32_t is_first, is_last;
   int32_t max_tokens; /* activation rows the workspace is sized for */
   int32_t max_reqs;   /* requests per micro-batch                   */

@@ -37,7 +37,7 @@ class StageConfig(C.Structure):
     _fields_ = [
         ("d", i32), ("Hq", i32), ("Hkv", i32), ("hd", i32), ("ffn", i32), ("num_layers", i32),
         ("vocab", i64), ("eps", f32), ("block_size", i32), ("max_blocks_per_req", i32),
-        ("max_pos", i32), ("is_first", i32), ("is_last", i32), ("max_tokens", i32),
+        ("max_pos", i32), ("num_blocks", i64), ("is_first", i32), ("is_last", i32), ("max_tokens", i32),
         ("max_reqs", i32), ("max_ctx", i32), ("embed", vp), ("final_norm", vp), ("lm_head", vp),
         ("cos_sin", vp),
     ]
@@ -63,7 +63,7 @@ _SIGS = {
     "pl_rope_kv_write": (i32, [vp, i64, vp, vp, vp, i32, vp, vp, i32, i64, i32, i32, i32, vp]),
     "pl_attn_prefill": (i32, [vp, i64, vp, i32, i32, i32, i32, i32, f32, vp, i64, vp]),
     "pl_attn_decode_workspace_bytes": (i64, [i32, i32, i32, i32]),
-    "pl_attn_decode": (i32, [vp, i64, vp, vp, i32, vp, i32, vp, i32, i32, i32, i32, i32, f32, vp, i64, vp, i64, vp]),
+    "pl_attn_decode": (i32, [vp, i64, vp, vp, i64, i32, vp, i32, vp, i32, i32, i32, i32, i32, f32, vp, i64, vp, i64, vp]),
     "pl_lmhead_workspace_bytes": (i64, [i32, i64]),
     "pl_lmhead_argmax": (i32, [vp, i64, vp, i64, i32, i32, vp, vp, i64, vp]),
     "pl_token_scatter": (i32, [vp, vp, vp, i32, vp, vp, i32, vp]),

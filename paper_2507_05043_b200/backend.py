@@ -37,6 +37,9 @@ from .driver import Backend
 from .executor import StageExecutor, build_meta
 from .spec import BLOCK_SIZE, DecoderSpec, prompt_tokens
 
+transmission_ns = pipelink.transport.transmission_ns
+s_to_ns = pipelink.transport.s_to_ns
+
 BatchPhase = pipelink.engine.BatchPhase
 RequestState = pipelink.RequestState
 
@@ -335,7 +338,7 @@ class GpuBackend(Backend):
                 ev = torch.cuda.Event()
                 ev.record(sst)
                 self.ev_send[src][k] = ev
-                self._recv_done(dst, rec, ev, is_ret)
+                self._recv_done(dst, rec, ev, is_ret, self._deliver_ns(link, size, now_ns))
             return
         if src_local:
             comm = self.comms[link]
@@ -353,9 +356,24 @@ class GpuBackend(Backend):
             if last:
                 ev = torch.cuda.Event()
                 ev.record(rst)
-                self._recv_done(dst, rec, ev, is_ret)
+                self._recv_done(dst, rec, ev, is_ret, self._deliver_ns(link, size, now_ns))
 
-    def _recv_done(self, dst: int, rec: _MbRec, ev, is_ret: bool) -> None:
+    def _deliver_ns(self, link: int, size: int, emit_ns: int) -> int:
+        """Virtual delivery time of a chunk emitted at emit_ns (engine.py:355, 552-557)."""
+        lp = self.driver.link_profiles[link]
+        return emit_ns + transmission_ns(lp, size) + s_to_ns(lp.latency_s)
+
+    def _recv_done(self, dst: int, rec: _MbRec, ev, is_ret: bool, deliver_ns: int) -> None:
+        if self.throttle:
+            # link-throttle mode: the payload becomes usable on the destination only once
+            # the emulated link would have delivered it -- gated on a separate stream so the
+            # link's own chunk pipeline is never held back by the latency
+            ds = self.deliver_stream[dst]
+            ds.wait_event(ev)
+            N.check(N.lib().pl_gate_until_ns(self.t0_dev[dst].data_ptr(), deliver_ns, ds.cuda_stream),
+                    "pl_gate_until_ns")
+            ev = torch.cuda.Event()
+            ev.record(ds)
         if not is_ret:
             self.ev_recv[dst][rec.slot] = ev
             return
@@ -399,7 +417,8 @@ class GpuBackend(Backend):
         self.timing = {}
         ends = {}
         for s, exe in self.exe.items():
-            for st in (self.send_stream[s], self.recv_stream[s]):
+            extra = (self.deliver_stream[s],) if self.throttle else ()
+            for st in (self.send_stream[s], self.recv_stream[s], *extra):
                 ev = torch.cuda.Event()
                 ev.record(st)
                 exe.stream.wait_event(ev)
@@ -421,4 +440,15 @@ class GpuBackend(Backend):
 
     # ---------------------------------------------------------- throttle
     def _start_gates(self) -> None:
-        raise pipelink.ConfigError("link throttle mode is provided by ThrottledGpuBackend")
+        """Per-device time origin on the GPU clock (%globaltimer) for the link gates."""
+        self.t0_dev, self.deliver_stream = {}, {}
+        for s, exe in self.exe.items():
+            with torch.cuda.device(exe.device):
+                self.deliver_stream[s] = torch.cuda.Stream(exe.device)
+                t0 = torch.zeros(1, dtype=torch.int64, device=exe.device)
+            N.check(N.lib().pl_record_globaltimer(t0.data_ptr(), exe.stream.cuda_stream),
+                    "pl_record_globaltimer")
+            ev = torch.cuda.Event()
+            ev.record(exe.stream)
+            self.deliver_stream[s].wait_event(ev)
+            self.t0_dev[s] = t0

@@ -116,13 +116,14 @@ int64_t pl_attn_decode_workspace_bytes(int32_t R, int32_t Hq, int32_t max_ctx, i
 }
 
 int32_t pl_attn_decode(const void* q, int64_t ldq, const void* k_cache, const void* v_cache,
-                       int32_t block_size, const int32_t* block_table, int32_t max_blocks,
+                       int64_t num_blocks, int32_t block_size, const int32_t* block_table, int32_t max_blocks,
                        const int32_t* ctx_len, int32_t R, int32_t max_ctx, int32_t Hq, int32_t Hkv,
                        int32_t hd, float scale, void* out, int64_t ldo, void* workspace,
                        int64_t workspace_bytes, void* stream) {
   if (!q || !k_cache || !v_cache || !block_table || !ctx_len || !out)
     return set_error(PL_ERR_CONFIG, "attn_decode: null argument");
-  return attn_decode_launch(B(q), ldq, B(k_cache), B(v_cache), block_size, block_table, max_blocks,
+  return attn_decode_launch(B(q), ldq, B(k_cache), B(v_cache), num_blocks, block_size, block_table,
+                            max_blocks,
                             ctx_len, R, max_ctx, Hq, Hkv, hd, scale, BM_(out), ldo, workspace,
                             workspace_bytes, S(stream));
 }

@@ -11,8 +11,9 @@
 // decode: one query token per request over its paged KV cache
 //   [num_blocks, Hkv, 64, hd].  One CTA per (kv head, request, KV split) serves
 //   the whole GQA group, so each KV page is read from HBM exactly once.  Pages
-//   are staged in padded shared memory with 16-byte cp.async; splits are a fixed
-//   8 pages (512 tokens) so the reduction order depends on the context length
+//   arrive by TMA into 128-byte-swizzled shared memory; QK^T and PV run on
+//   m16n8k16 tensor cores; a request's context is cut into ceil(pages/8)
+//   even splits, so the reduction order depends on its own context length
 //   only, never on the batch.
 #include "common.cuh"
 #include "pl_internal.h"
@@ -246,182 +247,214 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
 }
 
 // ======================================================= decode (paged)
+//
+// One CTA per (kv head, request, split of <= 8 pages).  A single thread streams
+// each 64-token K and V page into shared memory with four 2-D TMA boxes
+// (64 dims x 64 tokens, 128-byte swizzle) completing on an mbarrier; the four
+// warps then each take 16 tokens of the page: S = Q K^T and O += P V on
+// m16n8k16 tensor cores with Q = the GQA group padded to 16 rows.  Every warp
+// keeps its own online-softmax state; warps are merged in shared memory and
+// splits by attn_decode_combine_kernel, both in a fixed order.
 
-constexpr int PAGE = 64;               // tokens per KV block
-constexpr int PAGES_PER_SPLIT = 8;     // 512 tokens per split (context-length driven only)
-constexpr int KROW = HD * 2 + 16;      // padded smem row: 272 B, conflict-free 16 B reads
+constexpr int PAGE = 64;                 // tokens per KV block
+constexpr int MAX_PAGES_PER_SPLIT = 8;   // <= 512 tokens per split, pages spread evenly
+constexpr int DEC_STAGES = 3;
+constexpr int HALF_TILE = 64 * 128;      // 64 tokens x 64 dims bf16 (one TMA box)
+constexpr int PAGE_BYTES = 4 * HALF_TILE;  // K lo | K hi | V lo | V hi
 
 struct DecodeSmem {
-  static constexpr int KV_TILE = PAGE * KROW;           // 17408 B
-  static constexpr int Q_OFF = 4 * KV_TILE;             // K0 K1 V0 V1
-  static constexpr int P_OFF = Q_OFF + 8 * HD * 4;      // q fp32 [8][128]
-  static constexpr int TOTAL = P_OFF + 8 * PAGE * 4;    // p fp32 [8][64]
+  static constexpr int Q_OFF = DEC_STAGES * PAGE_BYTES;        // 16 x 128 bf16, 256 B rows
+  static constexpr int BAR_OFF = Q_OFF + 16 * 256;
+  static constexpr int TOTAL = BAR_OFF + 64 + 1024;            // + alignment slack
 };
 
-PL_DEV void load_page(uint8_t* dst, const __nv_bfloat16* src, int rows_valid) {
-  // 64 rows x 16 chunks, 8 per thread
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int c = threadIdx.x + i * 128;
-    const int row = c >> 4, ch = c & 15;
-    const bool ok = row < rows_valid;
-    cp_async16_zfill(dst + row * KROW + ch * 16, src + (ok ? row * HD + ch * 8 : 0), ok);
-  }
+// address of 16-byte chunk `c` (0..15) of token row `row` in a (lo|hi) 128B-swizzled pair
+PL_DEV uint32_t kv_addr(uint32_t base, int row, int c) {
+  return base + (c >> 3) * HALF_TILE + row * 128 + (((c & 7) ^ (row & 7)) << 4);
 }
 
 template <int G>
 __global__ void __launch_bounds__(128)
-    attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int64_t ldq,
-                       const __nv_bfloat16* __restrict__ k_cache,
-                       const __nv_bfloat16* __restrict__ v_cache,
+    attn_decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                       const __nv_bfloat16* __restrict__ q, int64_t ldq,
                        const int32_t* __restrict__ block_table, int max_blocks,
                        const int32_t* __restrict__ ctx_len, int Hkv, float scale_log2,
                        __nv_bfloat16* __restrict__ out, int64_t ldo, float* __restrict__ ws_o,
                        float2* __restrict__ ws_ml) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sK = smem_raw;
-  uint8_t* sV = smem_raw + 2 * DecodeSmem::KV_TILE;
-  float* sq = reinterpret_cast<float*>(smem_raw + DecodeSmem::Q_OFF);
-  float* sp = reinterpret_cast<float*>(smem_raw + DecodeSmem::P_OFF);
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem + DecodeSmem::Q_OFF;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DecodeSmem::BAR_OFF);
 
   const int kh = blockIdx.x, r = blockIdx.y, split = blockIdx.z, nsplit = gridDim.z;
   const int Hq = Hkv * G;
   const int ctx = ctx_len[r];
+  // split layout depends on this request's context only (batch invariance)
   const int n_pages = (ctx + PAGE - 1) / PAGE;
-  const int p0 = split * PAGES_PER_SPLIT;
-  const int p1 = min(n_pages, p0 + PAGES_PER_SPLIT);
+  const int ns_r = max(1, (n_pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
+  const int pps = (n_pages + ns_r - 1) / ns_r;
+  const int p0 = split * pps;
+  const int np = max(0, min(n_pages, p0 + pps) - p0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // q for the GQA group, pre-scaled into the log2 domain
-  for (int i = threadIdx.x; i < G * HD; i += 128) {
-    const int g = i / HD, e = i % HD;
-    sq[i] = bf2f(q[static_cast<int64_t>(r) * ldq + (kh * G + g) * HD + e]) * scale_log2;
-  }
-
-  // PV ownership: warp w -> heads w, w+4 (< G); lane -> dims [4*lane, 4*lane+4)
-  constexpr int HPW = (G + 3) / 4;
-  float acc[HPW][4];
-  float m_run[HPW], l_run[HPW];
-#pragma unroll
-  for (int a = 0; a < HPW; ++a) {
-    m_run[a] = -INFINITY;
-    l_run[a] = 0.f;
-    acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-  }
-
   const int32_t* bt = block_table + static_cast<int64_t>(r) * max_blocks;
-  auto page_src = [&](const __nv_bfloat16* cache, int p) {
-    return cache + (static_cast<int64_t>(bt[p]) * Hkv + kh) * PAGE * HD;
+
+  auto issue = [&](int i) {
+    const int st = i % DEC_STAGES;
+    const int row0 = (bt[p0 + i] * Hkv + kh) * PAGE;
+    uint8_t* dst = smem + st * PAGE_BYTES;
+    mbar_arrive_expect_tx(&full[st], PAGE_BYTES);
+    const uint64_t pol = policy_evict_first();
+    tma_load_2d(dst, &tmK, &full[st], 0, row0, pol);
+    tma_load_2d(dst + HALF_TILE, &tmK, &full[st], 64, row0, pol);
+    tma_load_2d(dst + 2 * HALF_TILE, &tmV, &full[st], 0, row0, pol);
+    tma_load_2d(dst + 3 * HALF_TILE, &tmV, &full[st], 64, row0, pol);
   };
-  if (p0 < p1) {
-    load_page(sK, page_src(k_cache, p0), min(PAGE, ctx - p0 * PAGE));
-    load_page(sV, page_src(v_cache, p0), min(PAGE, ctx - p0 * PAGE));
-    cp_async_commit();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DEC_STAGES; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
   }
-  for (int p = p0; p < p1; ++p) {
-    const int buf = (p - p0) & 1;
-    if (p + 1 < p1) {
-      load_page(sK + (buf ^ 1) * DecodeSmem::KV_TILE, page_src(k_cache, p + 1),
-                min(PAGE, ctx - (p + 1) * PAGE));
-      load_page(sV + (buf ^ 1) * DecodeSmem::KV_TILE, page_src(v_cache, p + 1),
-                min(PAGE, ctx - (p + 1) * PAGE));
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const uint8_t* kt = sK + buf * DecodeSmem::KV_TILE;
-    const uint8_t* vt = sV + buf * DecodeSmem::KV_TILE;
-    const int n_tok = min(PAGE, ctx - p * PAGE);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int i = 0; i < min(np, DEC_STAGES); ++i) issue(i);
+  }
+  // Q tile: rows g < G are the group's query heads, rows G..15 zero
+  for (int c = threadIdx.x; c < 16 * 16; c += 128) {
+    const int row = c >> 4, ch = c & 15;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < G) v = *reinterpret_cast<const uint4*>(q + static_cast<int64_t>(r) * ldq + (kh * G + row) * HD + ch * 8);
+    *reinterpret_cast<uint4*>(sQ + swz(row, ch)) = v;
+  }
+  __syncthreads();
+  const int mi = lane >> 3, ri = lane & 7;
+  uint32_t qf[8][4];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+    ldmatrix_x4(qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3],
+                smem_u32(sQ) + swz((mi & 1) * 8 + ri, ks * 2 + (mi >> 1)));
 
-    // scores: thread -> token j = tid & 63, heads g = (tid >> 6) + 2i
-    {
-      const int j = threadIdx.x & 63, g0 = threadIdx.x >> 6;
-      constexpr int NG = (G + 1) / 2;
-      float sc[NG];
+  float o[16][4];
 #pragma unroll
-      for (int i = 0; i < NG; ++i) sc[i] = 0.f;
-      const uint4* krow = reinterpret_cast<const uint4*>(kt + j * KROW);
-#pragma unroll 4
-      for (int c = 0; c < HD / 8; ++c) {
-        const uint4 kv = krow[c];
-        const uint32_t* kp = reinterpret_cast<const uint32_t*>(&kv);
-        float kf[8];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          const float2 f = unpack_bf16x2(kp[x]);
-          kf[2 * x] = f.x;
-          kf[2 * x + 1] = f.y;
-        }
-#pragma unroll
-        for (int i = 0; i < NG; ++i) {
-          const int g = g0 + 2 * i;
-          if (g < G) {
-            const float4* qv = reinterpret_cast<const float4*>(sq + g * HD + c * 8);
-            const float4 qa = qv[0], qb = qv[1];
-            sc[i] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qb.x * kf[4] +
-                     qb.y * kf[5] + qb.z * kf[6] + qb.w * kf[7];
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < NG; ++i) {
-        const int g = g0 + 2 * i;
-        if (g < G) sp[g * PAGE + j] = (j < n_tok) ? sc[i] : -INFINITY;
-      }
-    }
-    __syncthreads();
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
 
-    // online softmax + PV
+  for (int i = 0; i < np; ++i) {
+    const int st = i % DEC_STAGES;
+    mbar_wait(&full[st], (i / DEC_STAGES) & 1);
+    const uint32_t kb = smem_u32(smem + st * PAGE_BYTES);
+    const uint32_t vb = kb + 2 * HALF_TILE;
+    float s[2][4];
 #pragma unroll
-    for (int a = 0; a < HPW; ++a) {
-      const int g = warp + 4 * a;
-      if (g >= G) continue;
-      const float s0 = sp[g * PAGE + lane], s1 = sp[g * PAGE + lane + 32];
-      const float mt = warp_max(fmaxf(s0, s1));
-      const float m_new = fmaxf(m_run[a], mt);
-      const float corr = (m_run[a] == -INFINITY) ? 0.f : exp2f(m_run[a] - m_new);
-      const float e0 = exp2f(s0 - m_new), e1 = exp2f(s1 - m_new);
-      l_run[a] = l_run[a] * corr + warp_sum(e0 + e1);
-      m_run[a] = m_new;
-      __syncwarp();
-      sp[g * PAGE + lane] = e0;
-      sp[g * PAGE + lane + 32] = e1;
-      __syncwarp();
-      acc[a][0] *= corr;
-      acc[a][1] *= corr;
-      acc[a][2] *= corr;
-      acc[a][3] *= corr;
-      for (int jj = 0; jj < n_tok; ++jj) {
-        const float pj = sp[g * PAGE + jj];
-        const uint2 vv = *reinterpret_cast<const uint2*>(vt + jj * KROW + lane * 8);
-        const float2 va = unpack_bf16x2(vv.x), vb = unpack_bf16x2(vv.y);
-        acc[a][0] += pj * va.x;
-        acc[a][1] += pj * va.y;
-        acc[a][2] += pj * vb.x;
-        acc[a][3] += pj * vb.y;
-      }
+    for (int t = 0; t < 2; ++t) s[t][0] = s[t][1] = s[t][2] = s[t][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4(b0, b1, b2, b3, kv_addr(kb, warp * 16 + (mi >> 1) * 8 + ri, ks * 2 + (mi & 1)));
+      mma_bf16_16816(s[0], qf[ks], b0, b1);
+      mma_bf16_16816(s[1], qf[ks], b2, b3);
     }
-    __syncthreads();
+    const int tok0 = (p0 + i) * PAGE + warp * 16;
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = tok0 + t * 8 + (lane & 3) * 2 + (e & 1);
+        const float v = (j < ctx) ? s[t][e] * scale_log2 : -INFINITY;
+        s[t][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+    float corr[2], rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 1));
+      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 2));
+      const float m_new = fmaxf(m_r[hr], mx[hr]);
+      corr[hr] = (m_new == -INFINITY) ? 1.f : exp2f(m_r[hr] - m_new);
+      m_r[hr] = m_new;
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int hr = e >> 1;
+        const float p = (m_r[hr] == -INFINITY) ? 0.f : exp2f(s[t][e] - m_r[hr]);
+        s[t][e] = p;
+        rs[hr] += p;
+      }
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 1);
+      rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 2);
+      l_r[hr] = l_r[hr] * corr[hr] + rs[hr];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      o[nt][0] *= corr[0];
+      o[nt][1] *= corr[0];
+      o[nt][2] *= corr[1];
+      o[nt][3] *= corr[1];
+    }
+    uint32_t a[4];
+    a[0] = pack_bf16x2(s[0][0], s[0][1]);
+    a[1] = pack_bf16x2(s[0][2], s[0][3]);
+    a[2] = pack_bf16x2(s[1][0], s[1][1]);
+    a[3] = pack_bf16x2(s[1][2], s[1][3]);
+#pragma unroll
+    for (int nt = 0; nt < 16; nt += 2) {
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4_trans(b0, b1, b2, b3, kv_addr(vb, warp * 16 + (mi & 1) * 8 + ri, nt + (mi >> 1)));
+      mma_bf16_16816(o[nt], a, b0, b1);
+      mma_bf16_16816(o[nt + 1], a, b2, b3);
+    }
+    __syncthreads();  // every warp is done with stage st
+    if (threadIdx.x == 0 && i + DEC_STAGES < np) issue(i + DEC_STAGES);
   }
 
+  // merge the four warps' softmax states (shared memory reused: all loads consumed)
+  float* red_o = reinterpret_cast<float*>(smem);               // [4][16][128]
+  float* red_m = red_o + 4 * 16 * HD;                           // [4][16]
+  float* red_l = red_m + 4 * 16;                                // [4][16]
+  __syncthreads();
 #pragma unroll
-  for (int a = 0; a < HPW; ++a) {
-    const int g = warp + 4 * a;
-    if (g >= G) continue;
+  for (int hr = 0; hr < 2; ++hr) {
+    const int row = (lane >> 2) + hr * 8;
+    if ((lane & 3) == 0) {
+      red_m[warp * 16 + row] = m_r[hr];
+      red_l[warp * 16 + row] = l_r[hr];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const int col = nt * 8 + (lane & 3) * 2;
+      red_o[(warp * 16 + row) * HD + col] = o[nt][hr * 2];
+      red_o[(warp * 16 + row) * HD + col + 1] = o[nt][hr * 2 + 1];
+    }
+  }
+  __syncthreads();
+  const int e = threadIdx.x;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, red_m[w * 16 + g]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = red_m[w * 16 + g];
+      if (mw == -INFINITY) continue;
+      const float f = exp2f(mw - M);
+      L += red_l[w * 16 + g] * f;
+      O += red_o[(w * 16 + g) * HD + e] * f;
+    }
     const int head = kh * G + g;
     if (nsplit == 1) {
-      const float inv = l_run[a] > 0.f ? 1.f / l_run[a] : 0.f;
-      uint2 pk;
-      pk.x = pack_bf16x2(acc[a][0] * inv, acc[a][1] * inv);
-      pk.y = pack_bf16x2(acc[a][2] * inv, acc[a][3] * inv);
-      *reinterpret_cast<uint2*>(out + static_cast<int64_t>(r) * ldo + head * HD + lane * 4) = pk;
+      out[static_cast<int64_t>(r) * ldo + head * HD + e] = f2bf(L > 0.f ? O / L : 0.f);
     } else {
       const int64_t base = (static_cast<int64_t>(r) * Hq + head) * nsplit + split;
-      *reinterpret_cast<float4*>(ws_o + base * HD + lane * 4) =
-          make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
-      if (lane == 0) ws_ml[base] = make_float2(m_run[a], l_run[a]);
+      ws_o[base * HD + e] = O;
+      if (e == 0) ws_ml[base] = make_float2(M, L);
     }
   }
 }
@@ -447,27 +480,34 @@ __global__ void attn_decode_combine_kernel(const float* __restrict__ ws_o,
 
 int64_t attn_decode_workspace_bytes(int R, int Hq, int max_ctx, int hd) {
   const int pages = (max_ctx + PAGE - 1) / PAGE;
-  const int nsplit = std::max(1, (pages + PAGES_PER_SPLIT - 1) / PAGES_PER_SPLIT);
+  const int nsplit = std::max(1, (pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
   if (nsplit == 1) return 0;
   return static_cast<int64_t>(R) * Hq * nsplit * (hd * 4 + 8);
 }
 
 int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16* k_cache,
-                       const __nv_bfloat16* v_cache, int block_size, const int32_t* block_table,
-                       int max_blocks, const int32_t* ctx_len, int R, int max_ctx, int Hq, int Hkv,
-                       int hd, float scale, __nv_bfloat16* out, int64_t ldo, void* ws,
-                       int64_t ws_bytes, cudaStream_t st) {
+                       const __nv_bfloat16* v_cache, int64_t num_blocks, int block_size,
+                       const int32_t* block_table, int max_blocks, const int32_t* ctx_len, int R,
+                       int max_ctx, int Hq, int Hkv, int hd, float scale, __nv_bfloat16* out,
+                       int64_t ldo, void* ws, int64_t ws_bytes, cudaStream_t st) {
   if (R <= 0) return PL_OK;
   if (hd != HD) return set_error(PL_ERR_CONFIG, "attention: head_dim must be 128 (got %d)", hd);
   if (block_size != PAGE) return set_error(PL_ERR_CONFIG, "attention: KV block size must be 64");
   if (Hkv <= 0 || Hq % Hkv) return set_error(PL_ERR_CONFIG, "attention: Hq must be a multiple of Hkv");
+  if (num_blocks <= 0) return set_error(PL_ERR_CONFIG, "attention: num_blocks must be > 0");
+  if (ldq % 8) return set_error(PL_ERR_CONFIG, "attention: ldq % 8");
   const int G = Hq / Hkv;
   const int pages = (max_ctx + PAGE - 1) / PAGE;
-  const int nsplit = std::max(1, (pages + PAGES_PER_SPLIT - 1) / PAGES_PER_SPLIT);
+  const int nsplit = std::max(1, (pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
   const int64_t need = attn_decode_workspace_bytes(R, Hq, max_ctx, hd);
   if (need > 0 && (ws_bytes < need || !ws))
     return set_error(PL_ERR_CONFIG, "attn_decode: workspace too small (%lld < %lld)",
                      (long long)ws_bytes, (long long)need);
+  CUtensorMap mk, mv;
+  int rc;
+  const int64_t rows = num_blocks * Hkv * PAGE;
+  if ((rc = make_tma_2d(&mk, k_cache, rows, HD, HD, 64))) return rc;
+  if ((rc = make_tma_2d(&mv, v_cache, rows, HD, HD, 64))) return rc;
   float* ws_o = reinterpret_cast<float*>(ws);
   float2* ws_ml = need > 0 ? reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(ws) +
                                                        static_cast<int64_t>(R) * Hq * nsplit * hd * 4)
@@ -484,9 +524,8 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
       if (e != cudaSuccess) return set_cuda_error(e, "attn_decode smem attribute");             \
       attr = true;                                                                              \
     }                                                                                           \
-    attn_decode_kernel<GG><<<grid, 128, smem, st>>>(q, ldq, k_cache, v_cache, block_table,      \
-                                                    max_blocks, ctx_len, Hkv, sl2, out, ldo,    \
-                                                    ws_o, ws_ml);                               \
+    attn_decode_kernel<GG><<<grid, 128, smem, st>>>(mk, mv, q, ldq, block_table, max_blocks,    \
+                                                    ctx_len, Hkv, sl2, out, ldo, ws_o, ws_ml);  \
     break;                                                                                      \
   }
   switch (G) {
@@ -498,7 +537,7 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
       return set_error(PL_ERR_CONFIG, "attn_decode: GQA group %d unsupported (1,2,4,8)", G);
   }
 #undef PL_DECODE_CASE
-  int rc = check_launch("attn_decode_kernel");
+  rc = check_launch("attn_decode_kernel");
   if (rc || nsplit == 1) return rc;
   attn_decode_combine_kernel<<<dim3(Hq, R), HD, 0, st>>>(ws_o, ws_ml, Hq, nsplit, out, ldo);
   return check_launch("attn_decode_combine_kernel");

@@ -13,9 +13,11 @@
 //          every token's result independent of the batch it rides in.
 //   !SWAP (prefill): tokens are the A operand (M = 128 rows), features are N = 256.
 //
-// Warp roles (128 threads): warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA
-// issuer, warp 2 = TMEM allocator; afterwards all four warps run the epilogue,
-// warp w owning TMEM lanes [32w, 32w+32).
+// Persistent and warp-specialized (192 threads, one CTA per SM): warp 0 lane 0
+// = TMA producer running a STAGES-deep smem ring continuously across work items,
+// warp 1 = TMEM allocator + MMA issuer (lane 0), warps 2-5 = epilogue, warp w
+// owning TMEM lanes [32(w%4), +32).  The accumulator is double-buffered in
+// TMEM so the epilogue of item i overlaps the main loop of item i+1.
 //
 // Epilogues (rounding points follow HF modeling_llama.py: every bf16 tensor op
 // rounds its fp32 result to bf16):
@@ -24,7 +26,8 @@
 //   RESIDUAL  out = bf16(bf16(acc) + residual[t, n])     (o_proj / down_proj + residual, :313-331)
 //   SWIGLU    W rows interleaved in 64-row blocks [gate 64 | up 64]:
 //             out[t, j] = bf16(bf16(silu(bf16(g))) * bf16(u))   (LlamaMLP, :182-184)
-//   PARTIAL   fp32 partial sums per split (reduced by gemm_splitk_reduce)
+//   split-K   fp32 partials per split; the last split to finish a tile (arrival
+//             counter) sums them in split order and applies the epilogue
 //   ARGMAX    per token (max logit, index) over this CTA's 128 vocabulary rows
 #include <cudaTypedefs.h>
 
@@ -41,54 +44,72 @@ constexpr int BM = 128;         // MMA M (A-operand rows per CTA)
 constexpr int A_TILE_BYTES = BM * BK * 2;
 
 struct GemmArgs {
-  int T;          // tokens (logical rows of out)
-  int N;          // output features of the GEMM (rows of W)
-  int num_kb;     // K / 64
+  int T;             // tokens (logical rows of out)
+  int N;             // output features of the GEMM (rows of W)
+  int num_kb;        // K / 64
   int kb_per_split;
+  int splits;
+  int tiles_m;       // 128-row tiles of the A operand
+  int num_items;     // tiles_m * tiles_n * splits
   int epi;
   __nv_bfloat16* C;
   int64_t ldc;
   const __nv_bfloat16* bias;
   const __nv_bfloat16* residual;
   int64_t ldr;
-  float* partial;     // [splits][T][N]
+  float* partial;     // [splits][N][Tp] fp32 (split-K), Tp = T rounded up to the BN tile
+  int Tp;
+  int* counters;      // [tiles] arrival counters, zero between launches
   float2* argmax_ws;  // [N/128 tiles][T] (value, index-as-float-bits)
 };
 
-template <int BN, int STAGES>
+constexpr int kStageBudget = 200 * 1024;
+
+template <int BN>
 struct GemmSmem {
   static constexpr int B_TILE_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_TILE_BYTES + B_TILE_BYTES;
+  static constexpr int STAGES = (kStageBudget / STAGE_BYTES) > 10 ? 10 : (kStageBudget / STAGE_BYTES);
   static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
-  // full[S], empty[S], done, tmem slot, + epilogue scratch
-  static constexpr int SCRATCH_OFFSET = BAR_OFFSET + 8 * (2 * STAGES + 1) + 16;
-  static constexpr int SCRATCH_BYTES = 64 * 16 * 4 * 2;  // swiglu exchange / argmax
+  // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem slot + flag
+  static constexpr int SCRATCH_OFFSET = BAR_OFFSET + 8 * (2 * STAGES + 4) + 16;
+  static constexpr int SCRATCH_BYTES = 64 * 16 * 4;  // swiglu exchange / argmax partials
   static constexpr int TOTAL = SCRATCH_OFFSET + SCRATCH_BYTES + 1024;  // + alignment slack
 };
 
 PL_DEV float silu_f(float x) { return x / (1.0f + expf(-x)); }
+PL_DEV void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-template <int BN, bool SWAP, int STAGES>
-__global__ void __launch_bounds__(128, 1)
+// Final (non-partial) epilogue for one accumulator element.
+PL_DEV void store_out(const GemmArgs& a, int epi, int t, int n, float acc) {
+  if (epi == EPI_RESIDUAL)
+    a.C[(int64_t)t * a.ldc + n] = f2bf(rbf(acc) + bf2f(a.residual[(int64_t)t * a.ldr + n]));
+  else if (epi == EPI_BIAS)
+    a.C[(int64_t)t * a.ldc + n] = f2bf(acc + bf2f(a.bias[n]));
+  else
+    a.C[(int64_t)t * a.ldc + n] = f2bf(acc);
+}
+
+template <int BN, bool SWAP>
+__global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs args) {
-  using L = GemmSmem<BN, STAGES>;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  using L = GemmSmem<BN>;
+  constexpr int STAGES = L::STAGES;
+  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFFSET);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
   float* scratch = reinterpret_cast<float*>(smem + L::SCRATCH_OFFSET);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int bm = blockIdx.x, bn = blockIdx.y, split = blockIdx.z;
-  const int kb0 = split * args.kb_per_split;
-  const int kb1 = min(args.num_kb, kb0 + args.kb_per_split);
-  const int nkb = kb1 - kb0;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
@@ -97,264 +118,327 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  auto item_coords = [&](int item, int& m_tile, int& n_tile, int& split, int& kb0, int& nkb) {
+    split = item % args.splits;
+    const int tile = item / args.splits;
+    m_tile = tile % args.tiles_m;
+    n_tile = tile / args.tiles_m;
+    kb0 = split * args.kb_per_split;
+    nkb = min(args.num_kb, kb0 + args.kb_per_split) - kb0;
+  };
+
   if (warp == 0) {
-    if (lane == 0 && nkb > 0) {
-      // weights stream through once; activations are re-read by every weight tile
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
+    // ------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();   // weights stream through once
+      const uint64_t pol_x = policy_evict_last();    // activations are re-read per weight tile
       const uint64_t polA = SWAP ? pol_w : pol_x;
       const uint64_t polB = SWAP ? pol_x : pol_w;
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * L::STAGE_BYTES;
-        uint8_t* sb = sa + A_TILE_BYTES;
-        mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
-        const int kc = (kb0 + i) * BK;
-        tma_load_2d(sa, &tmA, &full[s], kc, bm * BM, polA);
-        tma_load_2d(sb, &tmB, &full[s], kc, bn * BN, polB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < args.num_items; item += gridDim.x) {
+        int m_tile, n_tile, split, kb0, nkb;
+        item_coords(item, m_tile, n_tile, split, kb0, nkb);
+        for (int i = 0; i < nkb; ++i) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
+          const int kc = (kb0 + i) * BK;
+          tma_load_2d(sa, &tmA, &full[stage], kc, m_tile * BM, polA);
+          tma_load_2d(sa + A_TILE_BYTES, &tmB, &full[stage], kc, n_tile * BN, polB);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0 && nkb > 0) {
+    // ------------------------------------------------------- MMA issuer
+    if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int item = blockIdx.x; item < args.num_items; item += gridDim.x) {
+        int m_tile, n_tile, split, kb0, nkb;
+        item_coords(item, m_tile, n_tile, split, kb0, nkb);
+        mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
-        const uint32_t sb = sa + A_TILE_BYTES;
-        const uint64_t da = umma_desc_sw128(sa);
-        const uint64_t db = umma_desc_sw128(sb);
+        const uint32_t d = tmem + acc * BN;
+        for (int i = 0; i < nkb; ++i) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * L::STAGE_BYTES);
+          const uint64_t da = umma_desc_sw128(sa);
+          const uint64_t db = umma_desc_sw128(sa + A_TILE_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          // +32 bytes per K=16 step inside the swizzle atom (encoded >> 4)
-          umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
+          for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+            umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        umma_commit(&empty[s]);
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
       }
-      umma_commit(done);
     }
     __syncwarp();
-  }
-
-  // ------------------------------------------------------------ epilogue
-  if (nkb > 0) {
-    mbar_wait(done, 0);
-  }
-  __syncwarp();
-  tc_fence_after();
-
-  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-  const int row = warp * 32 + lane;  // TMEM lane owned by this thread
-  const int epi = args.epi;
-
-  if constexpr (SWAP) {
-    // lane <-> feature n, column <-> token t
-    const int n = bm * BM + row;
-    if (epi == EPI_SWIGLU) {
-      // rows [0,64) gate, [64,128) up of the same 64 output features
-      const int j = bm * 64 + (row & 63);
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem + lane_base + c0, r);
-        tmem_ld_wait();
-        if (warp >= 2) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) scratch[c * 64 + (row - 64)] = __uint_as_float(r[c]);
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp < 2) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const int t = bn * BN + c0 + c;
-            if (t < args.T && nkb > 0) {
-              const float g = rbf(__uint_as_float(r[c]));
-              const float u = rbf(scratch[c * 64 + row]);
-              args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(g)) * u);
-            }
-          }
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-      }
-    } else if (epi == EPI_ARGMAX) {
-      float2* red = reinterpret_cast<float2*>(scratch);  // [4 warps][16 cols]
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem + lane_base + c0, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float v = (n < args.N && nkb > 0) ? __uint_as_float(r[c]) : -INFINITY;
-          int idx = n;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, v, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-            if (ov > v || (ov == v && oi < idx)) {
-              v = ov;
-              idx = oi;
-            }
-          }
-          if (lane == 0) red[warp * 16 + c] = make_float2(v, __int_as_float(idx));
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x < 16) {
-          const int c = threadIdx.x;
-          float2 best = red[c];
-          for (int w = 1; w < 4; ++w) {
-            const float2 o = red[w * 16 + c];
-            if (o.x > best.x || (o.x == best.x && __float_as_int(o.y) < __float_as_int(best.y)))
-              best = o;
-          }
-          const int t = bn * BN + c0 + c;
-          if (t < args.T) args.argmax_ws[(int64_t)bm * args.T + t] = best;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-      }
-    } else {
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem + lane_base + c0, r);
-        tmem_ld_wait();
-        if (n < args.N) {
-          const float b = (epi == EPI_BIAS) ? bf2f(args.bias[n]) : 0.f;
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const int t = bn * BN + c0 + c;
-            if (t >= args.T) break;
-            const float acc = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
-            if (epi == EPI_PARTIAL) {
-              args.partial[((int64_t)split * args.T + t) * args.N + n] = acc;
-            } else if (epi == EPI_RESIDUAL) {
-              const float res = bf2f(args.residual[(int64_t)t * args.ldr + n]);
-              args.C[(int64_t)t * args.ldc + n] = f2bf(rbf(acc) + res);
-            } else {
-              args.C[(int64_t)t * args.ldc + n] = f2bf(acc + b);
-            }
-          }
-        }
-      }
-    }
   } else {
-    // lane <-> token t, column <-> feature n
-    const int t = bm * BM + row;
-    const bool tv = t < args.T;
-    if (epi == EPI_SWIGLU) {
-      // columns [p*128, p*128+64) gate, [p*128+64, p*128+128) up
-      for (int p = 0; p < BN / 128; ++p) {
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-          uint32_t g[16], u[16];
-          tmem_ld16(tmem + lane_base + p * 128 + c0, g);
-          tmem_ld16(tmem + lane_base + p * 128 + 64 + c0, u);
-          tmem_ld_wait();
-          const int j0 = (bn * BN) / 2 + p * 64 + c0;
-          if (tv && (bn * BN + p * 128) < args.N) {
+    // ------------------------------------------------------- epilogue (warps 2..5)
+    const int quarter = warp & 3;                 // TMEM lanes [32q, 32q + 32)
+    const int row = quarter * 32 + lane;
+    const int ep = threadIdx.x - 64;              // 0..127
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const int epi = args.epi;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int item = blockIdx.x; item < args.num_items; item += gridDim.x) {
+      int m_tile, n_tile, split, kb0, nkb;
+      item_coords(item, m_tile, n_tile, split, kb0, nkb);
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const uint32_t tcol = tmem + lane_base + acc * BN;
+
+      if constexpr (SWAP) {
+        // lane <-> feature n, column <-> token t
+        const int n = m_tile * BM + row;
+        const int t_base = n_tile * BN;
+        if (args.splits > 1) {
+          // partials are token-contiguous per feature row: [split][N][Tp]
+          float* prow = args.partial + ((int64_t)split * args.N + n) * args.Tp + t_base;
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tcol + c0, r);
+            tmem_ld_wait();
+            if (n < args.N && t_base + c0 < args.T) {
+              float4* dst = reinterpret_cast<float4*>(prow + c0);
+#pragma unroll
+              for (int c = 0; c < 16; c += 4)
+                dst[c / 4] = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
+                                         __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+            }
+          }
+        } else if (epi == EPI_SWIGLU) {
+          // rows [0,64) gate, [64,128) up of the same 64 output features
+          const int j = m_tile * 64 + (row & 63);
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tcol + c0, r);
+            tmem_ld_wait();
+            if (row >= 64) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) scratch[c * 64 + (row - 64)] = __uint_as_float(r[c]);
+            }
+            epi_sync();
+            if (row < 64) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const int t = t_base + c0 + c;
+                if (t < args.T) {
+                  const float g = rbf(__uint_as_float(r[c]));
+                  const float u = rbf(scratch[c * 64 + row]);
+                  args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(g)) * u);
+                }
+              }
+            }
+            epi_sync();
+          }
+        } else if (epi == EPI_ARGMAX) {
+          float2* red = reinterpret_cast<float2*>(scratch);  // [4 quarters][16 cols]
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tcol + c0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              float v = (n < args.N) ? __uint_as_float(r[c]) : -INFINITY;
+              int idx = n;
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+                if (ov > v || (ov == v && oi < idx)) {
+                  v = ov;
+                  idx = oi;
+                }
+              }
+              if (lane == 0) red[quarter * 16 + c] = make_float2(v, __int_as_float(idx));
+            }
+            epi_sync();
+            if (ep < 16) {
+              float2 best = red[ep];
+              for (int q = 1; q < 4; ++q) {
+                const float2 o = red[q * 16 + ep];
+                if (o.x > best.x || (o.x == best.x && __float_as_int(o.y) < __float_as_int(best.y)))
+                  best = o;
+              }
+              const int t = t_base + c0 + ep;
+              if (t < args.T) args.argmax_ws[(int64_t)m_tile * args.T + t] = best;
+            }
+            epi_sync();
+          }
+        } else {
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tcol + c0, r);
+            tmem_ld_wait();
+            if (n < args.N) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const int t = t_base + c0 + c;
+                if (t < args.T) store_out(args, epi, t, n, __uint_as_float(r[c]));
+              }
+            }
+          }
+        }
+      } else {
+        // lane <-> token t, column <-> feature n   (splits == 1 on this path)
+        const int t = m_tile * BM + row;
+        const bool tv = t < args.T;
+        if (epi == EPI_SWIGLU) {
+          for (int p = 0; p < BN / 128; ++p) {
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+              uint32_t g[16], u[16];
+              tmem_ld16(tcol + p * 128 + c0, g);
+              tmem_ld16(tcol + p * 128 + 64 + c0, u);
+              tmem_ld_wait();
+              const int j0 = (n_tile * BN) / 2 + p * 64 + c0;
+              if (tv && (n_tile * BN + p * 128) < args.N) {
+                uint32_t packed[8];
+#pragma unroll
+                for (int c = 0; c < 16; c += 2) {
+                  const float g0 = rbf(__uint_as_float(g[c])), g1 = rbf(__uint_as_float(g[c + 1]));
+                  const float u0 = rbf(__uint_as_float(u[c])), u1 = rbf(__uint_as_float(u[c + 1]));
+                  packed[c / 2] = pack_bf16x2(rbf(silu_f(g0)) * u0, rbf(silu_f(g1)) * u1);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + j0);
+                dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+                dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+              }
+            }
+          }
+        } else {
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tcol + c0, r);
+            tmem_ld_wait();
+            const int n0 = n_tile * BN + c0;
+            if (!tv || n0 >= args.N) continue;
+            float v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(r[c]);
+            if (epi == EPI_BIAS) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) v[c] += bf2f(args.bias[n0 + c]);
+            } else if (epi == EPI_RESIDUAL) {
+              const uint4* rp = reinterpret_cast<const uint4*>(args.residual + (int64_t)t * args.ldr + n0);
+              const uint4 r0 = rp[0], r1 = rp[1];
+              const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+              for (int c = 0; c < 16; c += 2) {
+                const float2 rv = unpack_bf16x2(rr[c / 2]);
+                v[c] = rbf(v[c]) + rv.x;
+                v[c + 1] = rbf(v[c + 1]) + rv.y;
+              }
+            }
             uint32_t packed[8];
 #pragma unroll
-            for (int c = 0; c < 16; c += 2) {
-              const float g0 = rbf(__uint_as_float(g[c])), g1 = rbf(__uint_as_float(g[c + 1]));
-              const float u0 = rbf(__uint_as_float(u[c])), u1 = rbf(__uint_as_float(u[c + 1]));
-              packed[c / 2] = pack_bf16x2(rbf(silu_f(g0)) * u0, rbf(silu_f(g1)) * u1);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + j0);
+            for (int c = 0; c < 16; c += 2) packed[c / 2] = pack_bf16x2(v[c], v[c + 1]);
+            uint4* dst = reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + n0);
             dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
             dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
           }
         }
       }
-    } else {
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem + lane_base + c0, r);
-        tmem_ld_wait();
-        const int n0 = bn * BN + c0;
-        if (!tv || n0 >= args.N) continue;
-        if (epi == EPI_PARTIAL) {
-          float4* dst =
-              reinterpret_cast<float4*>(args.partial + ((int64_t)split * args.T + t) * args.N + n0);
+      // accumulator drained: hand the TMEM buffer back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+
+      if constexpr (SWAP) {
+        if (args.splits > 1) {
+          // Deterministic split-K fix-up: the last split to arrive sums all partials
+          // of the tile in split order (never in arrival order) and applies the epilogue.
+          const int tile = item / args.splits;
+          __threadfence();
+          epi_sync();
+          if (ep == 0) *flag = (atomicAdd(&args.counters[tile], 1) == args.splits - 1);
+          epi_sync();
+          if (*flag) {
+            __threadfence();
+            const int n = m_tile * BM + row;
+            const int t_base = n_tile * BN;
+            const int t_end = min(args.T, t_base + BN);
+            // 16 tokens at a time: splits x 4 independent 16-byte L2 loads in flight
+            for (int c0 = 0; c0 < BN && t_base + c0 < t_end; c0 += 16) {
+              float sum[16], sum_u[16];
 #pragma unroll
-          for (int c = 0; c < 16; c += 4)
-            dst[c / 4] = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
-                                     __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
-          continue;
-        }
-        float v[16];
+              for (int c = 0; c < 16; ++c) sum[c] = sum_u[c] = 0.f;
+              const bool swiglu = epi == EPI_SWIGLU;
+              const bool active = swiglu ? row < 64 : n < args.N;
+              if (active) {
+                for (int s = 0; s < args.splits; ++s) {
+                  const float4* src = reinterpret_cast<const float4*>(
+                      args.partial + ((int64_t)s * args.N + n) * args.Tp + t_base + c0);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(r[c]);
-        if (epi == EPI_BIAS) {
+                  for (int v = 0; v < 4; ++v) {
+                    const float4 x = __ldcg(src + v);
+                    sum[4 * v] += x.x; sum[4 * v + 1] += x.y; sum[4 * v + 2] += x.z; sum[4 * v + 3] += x.w;
+                  }
+                  if (swiglu) {
+                    const float4* su = src + (64 * args.Tp) / 4;   // the up row, 64 rows below
 #pragma unroll
-          for (int c = 0; c < 16; ++c) v[c] += bf2f(args.bias[n0 + c]);
-        } else if (epi == EPI_RESIDUAL) {
-          const uint4* rp = reinterpret_cast<const uint4*>(args.residual + (int64_t)t * args.ldr + n0);
-          const uint4 r0 = rp[0], r1 = rp[1];
-          const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+                    for (int v = 0; v < 4; ++v) {
+                      const float4 x = __ldcg(su + v);
+                      sum_u[4 * v] += x.x; sum_u[4 * v + 1] += x.y; sum_u[4 * v + 2] += x.z; sum_u[4 * v + 3] += x.w;
+                    }
+                  }
+                }
 #pragma unroll
-          for (int c = 0; c < 16; c += 2) {
-            const float2 rv = unpack_bf16x2(rr[c / 2]);
-            v[c] = rbf(v[c]) + rv.x;
-            v[c + 1] = rbf(v[c + 1]) + rv.y;
+                for (int c = 0; c < 16; ++c) {
+                  const int t = t_base + c0 + c;
+                  if (t >= t_end) break;
+                  if (swiglu)
+                    args.C[(int64_t)t * args.ldc + m_tile * 64 + row] =
+                        f2bf(rbf(silu_f(rbf(sum[c]))) * rbf(sum_u[c]));
+                  else
+                    store_out(args, epi, t, n, sum[c]);
+                }
+              }
+            }
+            if (ep == 0) args.counters[tile] = 0;
           }
+          epi_sync();
         }
-        uint32_t packed[8];
-#pragma unroll
-        for (int c = 0; c < 16; c += 2) packed[c / 2] = pack_bf16x2(v[c], v[c + 1]);
-        uint4* dst = reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + n0);
-        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
       }
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem);
-}
-
-// Sum split-K partials in split order (deterministic) and apply the epilogue.
-__global__ void gemm_splitk_reduce_kernel(const float* __restrict__ partial, int splits, int T,
-                                          int N, int epi, __nv_bfloat16* __restrict__ C,
-                                          int64_t ldc, const __nv_bfloat16* __restrict__ bias,
-                                          const __nv_bfloat16* __restrict__ residual,
-                                          int64_t ldr) {
-  const int n_out = (epi == EPI_SWIGLU) ? N / 2 : N;
-  const int64_t total = (int64_t)T * n_out;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int t = static_cast<int>(i / n_out);
-    const int j = static_cast<int>(i % n_out);
-    if (epi == EPI_SWIGLU) {
-      const int ng = (j / 64) * 128 + (j % 64);
-      const int nu = ng + 64;
-      float g = 0.f, u = 0.f;
-      for (int s = 0; s < splits; ++s) {
-        g += partial[((int64_t)s * T + t) * N + ng];
-        u += partial[((int64_t)s * T + t) * N + nu];
-      }
-      C[(int64_t)t * ldc + j] = f2bf(rbf(silu_f(rbf(g))) * rbf(u));
-    } else {
-      float acc = 0.f;
-      for (int s = 0; s < splits; ++s) acc += partial[((int64_t)s * T + t) * N + j];
-      if (epi == EPI_RESIDUAL)
-        C[(int64_t)t * ldc + j] = f2bf(rbf(acc) + bf2f(residual[(int64_t)t * ldr + j]));
-      else if (epi == EPI_BIAS)
-        C[(int64_t)t * ldc + j] = f2bf(acc + bf2f(bias[j]));
-      else
-        C[(int64_t)t * ldc + j] = f2bf(acc);
-    }
-  }
+  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
 // Per token: reduce the per-tile (max, index) pairs, lowest index on ties.
@@ -469,49 +553,79 @@ int make_map(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int6
   return PL_OK;
 }
 
-template <int BN, bool SWAP, int STAGES>
-int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, dim3 grid,
+template <int BN, bool SWAP>
+int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid,
               cudaStream_t st) {
-  constexpr int smem = GemmSmem<BN, STAGES>::TOTAL;
+  constexpr int smem = GemmSmem<BN>::TOTAL;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, SWAP, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, SWAP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
     attr_set = true;
   }
-  gemm_tc_kernel<BN, SWAP, STAGES><<<grid, 128, smem, st>>>(ma, mb, a);
+  gemm_tc_kernel<BN, SWAP><<<grid, 192, smem, st>>>(ma, mb, a);
   return check_launch("gemm_tc_kernel");
 }
 
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+bool use_swap(int64_t T, int epi) { return T <= 256 || epi == EPI_ARGMAX; }
+
+int swap_bn(int64_t T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
+
 }  // namespace
 
+int make_tma_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                int box_rows) {
+  return make_map(out, ptr, rows, cols, ld, box_rows);
+}
+
+// Split-K factor for the decode (SWAP) path, from the weight shape (N, K) only so a
+// token's result never depends on the batch it rides in: balance tiles*splits work items
+// over the persistent grid (one CTA per SM) with >= 4 k-blocks per split.
 int gemm_num_splits(int64_t N, int64_t K, bool swap) {
-  // Split-K depends on the weight shape only (batch invariance): aim for
-  // ~2 resident CTAs on each of the 148 SMs while keeping >= 8 k-blocks/split.
   if (!swap) return 1;
   const int64_t tiles = (N + BM - 1) / BM;
   const int64_t kb = K / BK;
+  const int sms = 148;
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= 16; ++s) {
-    if (kb / s < 8 && s > 1) break;
-    const int64_t ctas = tiles * s;
-    const double waves = static_cast<double>(ctas) / 296.0;
-    const double eff = waves / std::ceil(waves) * std::min(1.0, waves);
-    if (eff > best_eff + 0.02) {
+    const int64_t per = (kb + s - 1) / s;
+    if (s > 1 && per < 4) break;
+    const int64_t eff_s = (kb + per - 1) / per;  // no empty splits
+    const int64_t items = tiles * eff_s;
+    const double rounds = std::ceil(static_cast<double>(items) / sms);
+    const double eff = static_cast<double>(items) / (rounds * sms);
+    if (eff > best_eff + 0.03) {
       best_eff = eff;
-      best = s;
+      best = static_cast<int>(eff_s);
     }
   }
   return best;
 }
 
 int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi) {
-  const bool swap = T <= 256 || epi == EPI_ARGMAX;
+  const bool swap = use_swap(T, epi);
   if (epi == EPI_ARGMAX) return ((N + BM - 1) / BM) * T * 8;
   const int splits = gemm_num_splits(N, K, swap);
-  return splits > 1 ? static_cast<int64_t>(splits) * T * N * 4 : 0;
+  if (splits <= 1) return 0;
+  const int64_t bn = swap_bn(T);
+  const int64_t tiles_n = (T + bn - 1) / bn;
+  const int64_t tiles = ((N + BM - 1) / BM) * tiles_n;
+  return align256(tiles * 4) + static_cast<int64_t>(splits) * N * (tiles_n * bn) * 4;
 }
 
 int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int64_t ldw,
@@ -527,10 +641,10 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(W)) & 15)
     return set_error(PL_ERR_CONFIG, "gemm: operands must be 16-byte aligned");
   if ((ldx % 8) || (ldw % 8)) return set_error(PL_ERR_CONFIG, "gemm: ld must be a multiple of 8");
-  const bool swap = T <= 256 || epi == EPI_ARGMAX;
+  const bool swap = use_swap(T, epi);
   if (epi == EPI_ARGMAX && T > 256)
     return set_error(PL_ERR_CONFIG, "gemm argmax: at most 256 rows per call");
-  if (!swap && epi != EPI_PARTIAL && (N % 16 || ldc % 8 || (epi == EPI_RESIDUAL && ldr % 8)))
+  if (!swap && (N % 16 || ldc % 8 || (epi == EPI_RESIDUAL && ldr % 8)))
     return set_error(PL_ERR_CONFIG, "gemm: N and leading dims must be multiples of 16/8");
 
   GemmArgs a{};
@@ -543,60 +657,50 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   a.bias = bias;
   a.residual = residual;
   a.ldr = ldr;
-
-  const int splits = (epi == EPI_ARGMAX) ? 1 : gemm_num_splits(N, K, swap);
-  a.kb_per_split = (a.num_kb + splits - 1) / splits;
-  const int final_epi = epi;
+  a.splits = (epi == EPI_ARGMAX) ? 1 : gemm_num_splits(N, K, swap);
+  a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
+  const int bn = swap ? swap_bn(T) : 256;
+  a.tiles_m = static_cast<int>(swap ? (N + BM - 1) / BM : (T + BM - 1) / BM);
+  const int tiles_n = static_cast<int>(swap ? (T + bn - 1) / bn : (N + bn - 1) / bn);
+  a.num_items = a.tiles_m * tiles_n * a.splits;
+  a.Tp = tiles_n * bn;
+  const int64_t need = gemm_workspace_bytes(T, N, K, epi);
+  if (need > 0 && (ws_bytes < need || !ws))
+    return set_error(PL_ERR_CONFIG, "gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
+                     (long long)need);
   if (epi == EPI_ARGMAX) {
-    const int64_t need = ((N + BM - 1) / BM) * T * 8;
-    if (ws_bytes < need || !ws) return set_error(PL_ERR_CONFIG, "gemm argmax: workspace too small");
     a.argmax_ws = reinterpret_cast<float2*>(ws);
-  } else if (splits > 1) {
-    const int64_t need = static_cast<int64_t>(splits) * T * N * 4;
-    if (ws_bytes < need || !ws)
-      return set_error(PL_ERR_CONFIG, "gemm: split-K workspace too small (%lld < %lld)",
-                       (long long)ws_bytes, (long long)need);
-    a.partial = reinterpret_cast<float*>(ws);
-    a.epi = EPI_PARTIAL;
+  } else if (a.splits > 1) {
+    a.counters = reinterpret_cast<int*>(ws);
+    a.partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) +
+                                         align256(static_cast<int64_t>(a.tiles_m) * tiles_n * 4));
   }
+  const int grid = std::min(a.num_items, num_sms());
 
   CUtensorMap ma, mb;
   int rc;
   if (swap) {
-    const int bn = T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256;
     if ((rc = make_map(&ma, W, N, K, ldw, BM))) return rc;
     if ((rc = make_map(&mb, X, T, K, ldx, bn))) return rc;
-    dim3 grid((N + BM - 1) / BM, (T + bn - 1) / bn, splits);
     switch (bn) {
-      case 16: rc = launch_tc<16, true, 6>(ma, mb, a, grid, st); break;
-      case 32: rc = launch_tc<32, true, 5>(ma, mb, a, grid, st); break;
-      case 64: rc = launch_tc<64, true, 4>(ma, mb, a, grid, st); break;
-      case 128: rc = launch_tc<128, true, 4>(ma, mb, a, grid, st); break;
-      default: rc = launch_tc<256, true, 4>(ma, mb, a, grid, st); break;
+      case 16: rc = launch_tc<16, true>(ma, mb, a, grid, st); break;
+      case 32: rc = launch_tc<32, true>(ma, mb, a, grid, st); break;
+      case 64: rc = launch_tc<64, true>(ma, mb, a, grid, st); break;
+      case 128: rc = launch_tc<128, true>(ma, mb, a, grid, st); break;
+      default: rc = launch_tc<256, true>(ma, mb, a, grid, st); break;
     }
   } else {
-    constexpr int BNP = 256;
     if ((rc = make_map(&ma, X, T, K, ldx, BM))) return rc;
-    if ((rc = make_map(&mb, W, N, K, ldw, BNP))) return rc;
-    dim3 grid((T + BM - 1) / BM, (N + BNP - 1) / BNP, splits);
-    rc = launch_tc<BNP, false, 4>(ma, mb, a, grid, st);
+    if ((rc = make_map(&mb, W, N, K, ldw, 256))) return rc;
+    rc = launch_tc<256, false>(ma, mb, a, grid, st);
   }
   if (rc) return rc;
 
-  if (final_epi == EPI_ARGMAX) {
+  if (epi == EPI_ARGMAX) {
     const int tiles = static_cast<int>((N + BM - 1) / BM);
     argmax_reduce_kernel<<<static_cast<unsigned>(T), 256, 0, st>>>(
         reinterpret_cast<const float2*>(ws), tiles, static_cast<int>(T), argmax_out, nullptr);
     return check_launch("argmax_reduce_kernel");
-  }
-  if (splits > 1) {
-    const int64_t n_out = (final_epi == EPI_SWIGLU) ? N / 2 : N;
-    const int64_t total = T * n_out;
-    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-    gemm_splitk_reduce_kernel<<<blocks, 256, 0, st>>>(a.partial, splits, static_cast<int>(T),
-                                                      static_cast<int>(N), final_epi, C, ldc, bias,
-                                                      residual, ldr);
-    return check_launch("gemm_splitk_reduce_kernel");
   }
   return PL_OK;
 }

@@ -1,6 +1,7 @@
 // Internal declarations shared by the libb200link translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -27,6 +28,9 @@ int set_cuda_error(cudaError_t e, const char* what);
 int check_launch(const char* what);
 
 // gemm_tc.cu
+// cached 2-D bf16 TMA descriptor: [rows, cols] row-major (ld elements), box {64, box_rows}, SW128
+int make_tma_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                int box_rows);
 int gemm_num_splits(int64_t N, int64_t K, bool swap);
 int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi);
 int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int64_t ldw,
@@ -57,7 +61,8 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
                         int64_t ldo, cudaStream_t st);
 int64_t attn_decode_workspace_bytes(int R, int Hq, int max_ctx, int hd);
 int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16* k_cache,
-                       const __nv_bfloat16* v_cache, int block_size, const int32_t* block_table,
+                       const __nv_bfloat16* v_cache, int64_t num_blocks, int block_size,
+                       const int32_t* block_table,
                        int max_blocks, const int32_t* ctx_len, int R, int max_ctx, int Hq, int Hkv,
                        int hd, float scale, __nv_bfloat16* out, int64_t ldo, void* ws,
                        int64_t ws_bytes, cudaStream_t st);

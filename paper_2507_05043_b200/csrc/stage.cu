@@ -164,7 +164,8 @@ struct Stage {
         return rc;
       if (decode) {
         rc = attn_decode_launch(qkv, qkv_dim, static_cast<const __nv_bfloat16*>(w.k_cache),
-                                static_cast<const __nv_bfloat16*>(w.v_cache), c.block_size, bt,
+                                static_cast<const __nv_bfloat16*>(w.v_cache), c.num_blocks,
+                                c.block_size, bt,
                                 c.max_blocks_per_req, ctx, R, mb.max_ctx, c.Hq, c.Hkv, c.hd, scale, o,
                                 attn_dim, ws + L.attn_ws, L.total - L.attn_ws, st);
       } else {
@@ -231,6 +232,9 @@ int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* laye
   if (!workspace || workspace_bytes < L.total)
     return set_error(PL_ERR_CONFIG, "stage_create: workspace %lld < required %lld",
                      (long long)workspace_bytes, (long long)L.total);
+  // split-K arrival counters live in the workspace and must start at zero
+  cudaError_t e = cudaMemset(workspace, 0, static_cast<size_t>(L.total));
+  if (e != cudaSuccess) return set_cuda_error(e, "stage workspace memset");
   Stage* s = new Stage();
   s->cfg = *cfg;
   s->layers.assign(layers, layers + cfg->num_layers);

@@ -103,7 +103,7 @@ def create_link_comms(placement: Placement) -> dict:
 
 class B200PipelineEngine(PipelineDriver):
     def __init__(self, cfg, cluster, stage_profiles, *, decoder: DecoderSpec, seed: int = 0,
-                 devices: list | None = None, prompts: dict | None = None):
+                 devices: list | None = None, prompts: dict | None = None, throttle: bool = False):
         if cfg.model.hidden_dim != decoder.d or cfg.model.dtype_bytes != 2:
             raise pipelink.ConfigError("cfg.model must describe the decoder's bf16 residual stream "
                                        "(use DecoderSpec.model_spec())")
@@ -115,7 +115,8 @@ class B200PipelineEngine(PipelineDriver):
             world, rank = torch.distributed.get_world_size(), torch.distributed.get_rank()
         self.placement = Placement(S, world, rank, devices)
         comms = create_link_comms(self.placement) if world > 1 else {}
-        self.gpu = GpuBackend(decoder, cfg, self.placement, seed=seed, prompts=prompts, comms=comms)
+        self.gpu = GpuBackend(decoder, cfg, self.placement, seed=seed, prompts=prompts, comms=comms,
+                              throttle=throttle)
         super().__init__(cfg, cluster, stage_profiles, backend=self.gpu)
         self._comms = comms
 

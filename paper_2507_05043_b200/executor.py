@@ -121,6 +121,7 @@ class StageExecutor:
         cfg.num_layers = self.hi - self.lo
         cfg.vocab, cfg.eps = s.vocab, s.eps
         cfg.block_size, cfg.max_blocks_per_req, cfg.max_pos = BLOCK_SIZE, self.max_blocks, self.max_pos
+        cfg.num_blocks = self.num_blocks
         cfg.is_first, cfg.is_last = int(self.is_first), int(self.is_last)
         cfg.max_tokens, cfg.max_reqs, cfg.max_ctx = self.max_tokens, self.max_reqs, self.max_ctx
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731

@@ -75,7 +75,7 @@ def gemm(x: torch.Tensor, w: torch.Tensor, epilogue: int = EPI_NONE,
     if K != Kw:
         raise N.ConfigError(f"gemm: K mismatch {K} vs {Kw}")
     ws_bytes = N.lib().pl_gemm_workspace_bytes(T, Nw, K, epilogue)
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
+    ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)  # split-K counters start at 0
     ids = None
     if epilogue == EPI_ARGMAX:
         ids = torch.empty(T, dtype=torch.int64, device=x.device)
@@ -118,7 +118,8 @@ def attn_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     out = out if out is not None else torch.empty(R, Hq * hd, dtype=BF16, device=q.device)
     ws_bytes = N.lib().pl_attn_decode_workspace_bytes(R, Hq, max_ctx, hd)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
-    N.call("pl_attn_decode", _ptr(q), q.stride(0), _ptr(k_cache), _ptr(v_cache), block_size,
+    N.call("pl_attn_decode", _ptr(q), q.stride(0), _ptr(k_cache), _ptr(v_cache), k_cache.shape[0],
+           block_size,
            _ptr(block_table), block_table.shape[1], _ptr(ctx_len), R, max_ctx, Hq, Hkv, hd,
            float(hd ** -0.5), _ptr(out), out.stride(0), _ptr(ws), ws_bytes, _stream())
     return out

@@ -214,4 +214,5 @@ def test_attn_decode_paged(ops, ctx, Hq, Hkv):
         k = kc[pages].permute(0, 2, 1, 3).reshape(-1, Hkv, hd)[: ctx[r]]
         v = vc[pages].permute(0, 2, 1, 3).reshape(-1, Hkv, hd)[: ctx[r]]
         refs.append(OD.attention_ref(q[r].reshape(1, Hq, hd), k, v, None))
-    close_bf16(out, torch.cat(refs), rel=2.0 ** -7, atol=2e-3)
+    # P is rounded to bf16 for the tensor-core P.V (as in the prefill kernel)
+    close_bf16(out, torch.cat(refs), rel=2.0 ** -6, atol=4e-3)

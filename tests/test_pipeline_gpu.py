@@ -86,7 +86,8 @@ def test_config1_standard_init_tie_band():
         chosen = logits.gather(1, gen[:, None]).squeeze(1)
         span = (logits.max() - logits.min()).item()
         tol = 0.02 + 0.02 * span
-        assert (chosen >= best - tol).all(), f"request {r.id}: token outside the tie band"
+        gap = (best - chosen).max().item()
+        assert (chosen >= best - tol).all(), f"request {r.id}: token {gap:.4f} below the max (band {tol:.4f})"
         exact += (logits.argmax(-1) == gen).sum().item()
         total += gen.numel()
     assert exact / total >= 0.9, f"only {exact}/{total} exact"
@@ -126,6 +127,55 @@ def test_stage_logits_within_tolerance():
     top2 = ref.topk(2, -1).values
     clear = (top2[:, 0] - top2[:, 1]) > 0.02 + 0.02 * span
     assert torch.equal(ids_gpu[clear], ref.argmax(-1)[clear])
+    exe.close()
+
+
+@pytest.mark.parametrize("spec", [TINY, TINY.with_(Hq=8, Hkv=2, d=1024, ffn=1536, vocab=2048)])
+def test_decode_logits_within_tolerance(spec):
+    """Prefill then teacher-forced decode steps through the paged decode path
+    (split-K GEMMs at small T, tensor-core decode attention): logits vs the oracle."""
+    lens = [100, 37, 64]
+    R, T = len(lens), sum(lens)
+    steps = 5
+    exe = StageExecutor(spec, 0, (0, spec.num_layers), True, True, torch.device("cuda", 0), seed=0,
+                        max_tokens=T, max_reqs=R, max_ctx=256, num_blocks=3 * 4, n_slots=1)
+    mb_ = exe.max_blocks
+    rows = np.arange(R * mb_, dtype=np.int32).reshape(R, -1)
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    pos = np.concatenate([np.arange(n) for n in lens])
+    req_of = np.repeat(np.arange(R), lens)
+    slots = rows[req_of, pos // 64] * 64 + pos % 64
+    ids = np.concatenate([prompt_tokens(0, i, n, spec.vocab) for i, n in enumerate(lens)])
+    meta = build_meta(T, R, mb_, pos, slots, req_of, cu, lens, cu[1:] - 1, rows)
+    exe.meta_dev[: meta.size].copy_(torch.from_numpy(meta))
+    exe.ids_dev[:T].copy_(torch.from_numpy(ids))
+    torch.cuda.synchronize()
+    exe.forward(0, T, R, False, max(lens), max(lens))
+    exe.stream.synchronize()
+
+    model = OD.OracleModel(OD.OracleSpec.from_spec(spec), seed=0, max_pos=256)
+    caches = model.new_cache(R)
+    toks = [torch.from_numpy(ids[cu[i]:cu[i + 1]]) for i in range(R)]
+    ref = model.forward(toks, [torch.arange(n) for n in lens], caches)
+    last_token = torch.zeros(R, dtype=torch.int64, device="cuda")
+    worst = 0.0
+    for k in range(steps):
+        nxt = ref.argmax(-1)                         # teacher forcing with the oracle's tokens
+        last_token.copy_(nxt)
+        p = np.array([lens[i] + k for i in range(R)])
+        dslots = rows[np.arange(R), p // 64] * 64 + p % 64
+        meta = build_meta(R, R, mb_, p, dslots, np.arange(R), np.arange(R + 1), p + 1, np.arange(R), rows)
+        exe.meta_dev[: meta.size].copy_(torch.from_numpy(meta))
+        torch.cuda.synchronize()
+        exe.forward(0, R, R, True, 1, int(p.max()) + 1, last_token=last_token)
+        exe.stream.synchronize()
+        hn = ops.rmsnorm(exe.hidden[0][:R].clone(), exe.final_norm, spec.eps)
+        got = ops.gemm(hn, exe.lm_head).float().cpu()
+        ref = model.forward([nxt[i:i + 1] for i in range(R)], [torch.tensor([p[i]]) for i in range(R)], caches)
+        span = (ref.max() - ref.min()).item()
+        err = (got - ref).abs().max().item()
+        worst = max(worst, err / (0.02 + 0.02 * span))
+        assert err <= 0.02 + 0.02 * span, f"step {k}: max |dlogit| {err:.4f} (span {span:.3f})"
     exe.close()
 
 
