@@ -84,9 +84,7 @@ PL_API int32_t pl_rmsnorm(const void* x, int64_t ldx, const int32_t* row_idx, co
                    int64_t rows, int32_t d, void* out, int64_t ldo, void* stream);
 
 /* C[T, N] = epilogue(X[T, K] . W[N, K]^T) on tcgen05 tensor cores.  workspace:
- * pl_gemm_workspace_bytes(T, N, K, epilogue) bytes (split-K arrival counters +
- * partials / argmax); zero it once before first use -- every call leaves its
- * counters at zero again. */
+ * pl_gemm_workspace_bytes(T, N, K, epilogue) bytes (split-K or argmax partials). */
 PL_API int64_t pl_gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t epilogue);
 PL_API int32_t pl_gemm(const void* X, int64_t ldx, const void* W, int64_t ldw, const void* bias, void* C,
                 int64_t ldc, const void* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,

@@ -138,6 +138,7 @@ class OracleSpec:
     bias_scale: float = 0.02
     peaked: bool = False
     lm_alpha: float = 4.0
+    peaked_embed_scale: float = 8.0
 
     @classmethod
     def from_spec(cls, spec) -> "OracleSpec":
@@ -182,7 +183,7 @@ def make_layer(spec: OracleSpec, layer: int, seed: int) -> LayerW:
 
 
 def make_embed(spec: OracleSpec, seed: int) -> torch.Tensor:
-    scale = 1.0 if spec.peaked else spec.embed_scale
+    scale = spec.peaked_embed_scale if spec.peaked else spec.embed_scale
     return hash_tensor((spec.vocab, spec.d), seed, T_EMBED, scale)
 
 

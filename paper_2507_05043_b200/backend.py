@@ -205,6 +205,8 @@ class GpuBackend(Backend):
         self.fb_events: list = []   # (event, mb request ids)
         self.mb_log: list = []      # (phase, R, sum of contexts) per admitted micro-batch
         self.first_decode_ev = None
+        self.busy_events: list = []  # (stage, mb id, start event, end event) on the device clock
+        self.mb_requests: dict = {}  # mb id -> request ids
         self.prompts = {}
         for r in reqs:
             if self.user_prompts is not None and r.id in self.user_prompts:
@@ -224,6 +226,7 @@ class GpuBackend(Backend):
             self._start_gates()
 
     def admit(self, mb, now_ns: int) -> None:
+        self.mb_requests[mb.id] = mb.request_ids
         slot = self.free_slots.pop()
         R = len(mb.request_ids)
         decode = mb.phase is BatchPhase.DECODE
@@ -301,10 +304,13 @@ class GpuBackend(Backend):
             ib[: rec.ids.nbytes].numpy()[:] = rec.ids.view(np.uint8)
             lib.pl_memcpy_async(exe.ids_dev.data_ptr(), ib.data_ptr(), rec.ids.nbytes, st.cuda_stream)
             self.ids_ring[s].mark(j, st)
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_start.record(st)
         exe.forward(k, rec.T, rec.R, rec.decode, rec.max_seqlen, rec.max_ctx,
                     last_token=self.last_token if (s == 0) else None)
-        ev = torch.cuda.Event()
+        ev = torch.cuda.Event(enable_timing=True)
         ev.record(st)
+        self.busy_events.append((s, mb.id, t_start, ev))
         self.ev_comp[s][k] = ev
         q.append(ev)
         if self.S == 1:
@@ -429,12 +435,19 @@ class GpuBackend(Backend):
             ends[s].synchronize()
         self.run_time_s = max((self.t0[s].elapsed_time(ends[s]) / 1e3 for s in self.exe), default=0.0)
         self.tokens = None
+        self.fb_times_s, self.decode_start_s = [], None
         if 0 in self.exe:
             gen = self.gen_tokens.cpu().numpy()
             self.tokens = {r.id: gen[self.rid_index[r.id], : r.tokens_emitted].copy()
                            for r in result.requests}
             t0 = self.t0[0]
             self.fb_times_s = [t0.elapsed_time(ev) / 1e3 for ev, _ in self.fb_events]
+        # real per-stage busy intervals (ns on each device's clock, origin = run start)
+        self.busy_real_ns = {}
+        for s, mb_id, a, b in self.busy_events:
+            t0s = self.t0[s]
+            self.busy_real_ns.setdefault(s, []).append(
+                (mb_id, round(t0s.elapsed_time(a) * 1e6), round(t0s.elapsed_time(b) * 1e6)))
             self.decode_start_s = (t0.elapsed_time(self.first_decode_ev) / 1e3
                                    if self.first_decode_ev is not None else None)
 

@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -25,6 +26,14 @@ int set_error(int code, const char* fmt, ...) {
 
 int set_cuda_error(cudaError_t e, const char* what) {
   return set_error(PL_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("PL_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 int check_launch(const char* what) {

@@ -64,6 +64,8 @@ __global__ void __launch_bounds__(128, 2)
                         const int32_t* __restrict__ cu_seqlens, int Hq, int Hkv, float scale_log2,
                         __nv_bfloat16* __restrict__ out, int64_t ldo) {
   extern __shared__ uint8_t smem_raw[];
+  pdl_trigger();
+  pdl_wait();
   uint8_t* sQ = smem_raw;                 // 16 KB
   uint8_t* sK = smem_raw + 16384;         // 2 x 16 KB
   uint8_t* sV = smem_raw + 16384 * 3;     // 2 x 16 KB
@@ -241,9 +243,8 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
     attr = true;
   }
   dim3 grid((max_seqlen + 63) / 64, Hq, R);
-  attn_prefill_kernel<<<grid, 128, smem, st>>>(qkv, ldqkv, cu_seqlens, Hq, Hkv, scale * LOG2E, out,
-                                               ldo);
-  return check_launch("attn_prefill_kernel");
+  return launch_k("attn_prefill_kernel", attn_prefill_kernel, grid, dim3(128), smem, st, qkv, ldqkv,
+                  cu_seqlens, Hq, Hkv, scale * LOG2E, out, ldo);
 }
 
 // ======================================================= decode (paged)
@@ -315,6 +316,8 @@ __global__ void __launch_bounds__(128)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
@@ -463,6 +466,8 @@ __global__ void __launch_bounds__(128)
 __global__ void attn_decode_combine_kernel(const float* __restrict__ ws_o,
                                            const float2* __restrict__ ws_ml, int Hq, int nsplit,
                                            __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  pdl_trigger();
+  pdl_wait();
   const int head = blockIdx.x, r = blockIdx.y, e = threadIdx.x;
   const int64_t base = (static_cast<int64_t>(r) * Hq + head) * nsplit;
   float M = -INFINITY;
@@ -524,8 +529,8 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
       if (e != cudaSuccess) return set_cuda_error(e, "attn_decode smem attribute");             \
       attr = true;                                                                              \
     }                                                                                           \
-    attn_decode_kernel<GG><<<grid, 128, smem, st>>>(mk, mv, q, ldq, block_table, max_blocks,    \
-                                                    ctx_len, Hkv, sl2, out, ldo, ws_o, ws_ml);  \
+    rc = launch_k("attn_decode_kernel", attn_decode_kernel<GG>, grid, dim3(128), smem, st, mk,  \
+                  mv, q, ldq, block_table, max_blocks, ctx_len, Hkv, sl2, out, ldo, ws_o, ws_ml); \
     break;                                                                                      \
   }
   switch (G) {
@@ -537,10 +542,9 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
       return set_error(PL_ERR_CONFIG, "attn_decode: GQA group %d unsupported (1,2,4,8)", G);
   }
 #undef PL_DECODE_CASE
-  rc = check_launch("attn_decode_kernel");
   if (rc || nsplit == 1) return rc;
-  attn_decode_combine_kernel<<<dim3(Hq, R), HD, 0, st>>>(ws_o, ws_ml, Hq, nsplit, out, ldo);
-  return check_launch("attn_decode_combine_kernel");
+  return launch_k("attn_decode_combine_kernel", attn_decode_combine_kernel, dim3(Hq, R), dim3(HD), 0,
+                  st, ws_o, ws_ml, Hq, nsplit, out, ldo);
 }
 
 }  // namespace pl

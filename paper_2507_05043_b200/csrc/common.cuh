@@ -87,6 +87,15 @@ PL_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// ------------------------------------------------ programmatic dependent launch
+// Every kernel triggers its dependents as soon as it starts and waits for its
+// predecessor only right before touching data the predecessor produced (or
+// consumes): prologues (barrier init, TMEM alloc, descriptor prefetch, weight
+// prefetch) overlap the previous kernel's tail.  Both are no-ops when the
+// kernel was launched without the PDL attribute.
+PL_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+PL_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 PL_DEV uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

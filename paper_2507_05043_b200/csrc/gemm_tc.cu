@@ -26,11 +26,12 @@
 //   RESIDUAL  out = bf16(bf16(acc) + residual[t, n])     (o_proj / down_proj + residual, :313-331)
 //   SWIGLU    W rows interleaved in 64-row blocks [gate 64 | up 64]:
 //             out[t, j] = bf16(bf16(silu(bf16(g))) * bf16(u))   (LlamaMLP, :182-184)
-//   split-K   fp32 partials per split; the last split to finish a tile (arrival
-//             counter) sums them in split order and applies the epilogue
+//   split-K   token-contiguous fp32 partials per split, summed in split order by
+//             gemm_splitk_reduce_kernel, which applies the epilogue
 //   ARGMAX    per token (max logit, index) over this CTA's 128 vocabulary rows
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -59,17 +60,24 @@ struct GemmArgs {
   int64_t ldr;
   float* partial;     // [splits][N][Tp] fp32 (split-K), Tp = T rounded up to the BN tile
   int Tp;
-  int* counters;      // [tiles] arrival counters, zero between launches
   float2* argmax_ws;  // [N/128 tiles][T] (value, index-as-float-bits)
 };
 
-constexpr int kStageBudget = 200 * 1024;
+// Decode tiles (BN <= 128) run 2 CTAs per SM with a shallower ring each (two
+// independent epilogues per SM); BN = 256 tiles run one CTA per SM.
+template <int BN, int CTAS = (BN <= 128 ? 2 : 1)>
+struct GemmCfg {
+  static constexpr int STAGE_BYTES = A_TILE_BYTES + BN * BK * 2;
+  static constexpr int CTAS_PER_SM = CTAS;
+  static constexpr int BUDGET = CTAS_PER_SM == 2 ? 100 * 1024 : 196 * 1024;
+  static constexpr int STAGES = BUDGET / STAGE_BYTES;
+};
 
-template <int BN>
+template <int BN, int CTAS>
 struct GemmSmem {
   static constexpr int B_TILE_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_TILE_BYTES + B_TILE_BYTES;
-  static constexpr int STAGES = (kStageBudget / STAGE_BYTES) > 10 ? 10 : (kStageBudget / STAGE_BYTES);
+  static constexpr int STAGES = GemmCfg<BN, CTAS>::STAGES;
   static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
   // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem slot + flag
   static constexpr int SCRATCH_OFFSET = BAR_OFFSET + 8 * (2 * STAGES + 4) + 16;
@@ -90,11 +98,11 @@ PL_DEV void store_out(const GemmArgs& a, int epi, int t, int n, float acc) {
     a.C[(int64_t)t * a.ldc + n] = f2bf(acc);
 }
 
-template <int BN, bool SWAP>
-__global__ void __launch_bounds__(192, 1)
+template <int BN, bool SWAP, int CTAS>
+__global__ void __launch_bounds__(192, CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs args) {
-  using L = GemmSmem<BN>;
+  using L = GemmSmem<BN, CTAS>;
   constexpr int STAGES = L::STAGES;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
   extern __shared__ uint8_t smem_raw[];
@@ -105,7 +113,6 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
   float* scratch = reinterpret_cast<float*>(smem + L::SCRATCH_OFFSET);
 
   const int warp = threadIdx.x >> 5;
@@ -129,6 +136,10 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  // the epilogue writes buffers the previous kernel may still read (split-K partials,
+  // the residual stream): wait for it before any global write
+  if (warp >= 2) pdl_wait();
 
   auto item_coords = [&](int item, int& m_tile, int& n_tile, int& split, int& kb0, int& nkb) {
     split = item % args.splits;
@@ -148,10 +159,34 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t polB = SWAP ? pol_x : pol_w;
       int stage = 0;
       uint32_t phase = 0;
+      bool first = true;
       for (int item = blockIdx.x; item < args.num_items; item += gridDim.x) {
         int m_tile, n_tile, split, kb0, nkb;
         item_coords(item, m_tile, n_tile, split, kb0, nkb);
-        for (int i = 0; i < nkb; ++i) {
+        int i = 0;
+        if (first) {
+          // Weights never depend on the previous kernel: stream the first ring's worth
+          // of weight tiles before waiting on it (PDL), then the activation tiles.
+          first = false;
+          const int pre = min(nkb, STAGES);
+          for (; i < pre; ++i) {
+            uint8_t* sa = smem + i * L::STAGE_BYTES;
+            mbar_arrive_expect_tx(&full[i], L::STAGE_BYTES);
+            const int kc = (kb0 + i) * BK;
+            if (SWAP) tma_load_2d(sa, &tmA, &full[i], kc, m_tile * BM, polA);
+            else tma_load_2d(sa + A_TILE_BYTES, &tmB, &full[i], kc, n_tile * BN, polB);
+          }
+          pdl_wait();
+          for (int j = 0; j < pre; ++j) {
+            uint8_t* sa = smem + j * L::STAGE_BYTES;
+            const int kc = (kb0 + j) * BK;
+            if (SWAP) tma_load_2d(sa + A_TILE_BYTES, &tmB, &full[j], kc, n_tile * BN, polB);
+            else tma_load_2d(sa, &tmA, &full[j], kc, m_tile * BM, polA);
+          }
+          stage = pre % STAGES;
+          phase = (pre == STAGES) ? 1 : 0;
+        }
+        for (; i < nkb; ++i) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
@@ -164,6 +199,7 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
+      if (first) pdl_wait();
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -377,62 +413,6 @@ __global__ void __launch_bounds__(192, 1)
         aphase ^= 1;
       }
 
-      if constexpr (SWAP) {
-        if (args.splits > 1) {
-          // Deterministic split-K fix-up: the last split to arrive sums all partials
-          // of the tile in split order (never in arrival order) and applies the epilogue.
-          const int tile = item / args.splits;
-          __threadfence();
-          epi_sync();
-          if (ep == 0) *flag = (atomicAdd(&args.counters[tile], 1) == args.splits - 1);
-          epi_sync();
-          if (*flag) {
-            __threadfence();
-            const int n = m_tile * BM + row;
-            const int t_base = n_tile * BN;
-            const int t_end = min(args.T, t_base + BN);
-            // 16 tokens at a time: splits x 4 independent 16-byte L2 loads in flight
-            for (int c0 = 0; c0 < BN && t_base + c0 < t_end; c0 += 16) {
-              float sum[16], sum_u[16];
-#pragma unroll
-              for (int c = 0; c < 16; ++c) sum[c] = sum_u[c] = 0.f;
-              const bool swiglu = epi == EPI_SWIGLU;
-              const bool active = swiglu ? row < 64 : n < args.N;
-              if (active) {
-                for (int s = 0; s < args.splits; ++s) {
-                  const float4* src = reinterpret_cast<const float4*>(
-                      args.partial + ((int64_t)s * args.N + n) * args.Tp + t_base + c0);
-#pragma unroll
-                  for (int v = 0; v < 4; ++v) {
-                    const float4 x = __ldcg(src + v);
-                    sum[4 * v] += x.x; sum[4 * v + 1] += x.y; sum[4 * v + 2] += x.z; sum[4 * v + 3] += x.w;
-                  }
-                  if (swiglu) {
-                    const float4* su = src + (64 * args.Tp) / 4;   // the up row, 64 rows below
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                      const float4 x = __ldcg(su + v);
-                      sum_u[4 * v] += x.x; sum_u[4 * v + 1] += x.y; sum_u[4 * v + 2] += x.z; sum_u[4 * v + 3] += x.w;
-                    }
-                  }
-                }
-#pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                  const int t = t_base + c0 + c;
-                  if (t >= t_end) break;
-                  if (swiglu)
-                    args.C[(int64_t)t * args.ldc + m_tile * 64 + row] =
-                        f2bf(rbf(silu_f(rbf(sum[c]))) * rbf(sum_u[c]));
-                  else
-                    store_out(args, epi, t, n, sum[c]);
-                }
-              }
-            }
-            if (ep == 0) args.counters[tile] = 0;
-          }
-          epi_sync();
-        }
-      }
     }
   }
 
@@ -441,9 +421,61 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
+// Split-K reduction + epilogue.  partial: [splits][N][Tp] fp32 (token-contiguous),
+// summed in split order (deterministic).  Each thread owns one output feature and
+// 4 consecutive tokens: splits independent 16-byte loads in flight.
+__global__ void __launch_bounds__(256)
+    gemm_splitk_reduce_kernel(const float* __restrict__ partial, int splits, int T, int Tp, int N,
+                              int epi, __nv_bfloat16* __restrict__ C, int64_t ldc,
+                              const __nv_bfloat16* __restrict__ bias,
+                              const __nv_bfloat16* __restrict__ residual, int64_t ldr) {
+  pdl_trigger();
+  pdl_wait();
+  const int n_out = (epi == EPI_SWIGLU) ? N / 2 : N;
+  const int tq = (T + 3) / 4;
+  const int64_t total = static_cast<int64_t>(n_out) * tq;
+  const int64_t split_stride = static_cast<int64_t>(N) * Tp / 4;  // in float4
+  const float4* P = reinterpret_cast<const float4*>(partial);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(i % n_out);   // consecutive threads -> consecutive features
+    const int t0 = static_cast<int>(i / n_out) * 4;
+    const int n = (epi == EPI_SWIGLU) ? (j / 64) * 128 + (j % 64) : j;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), up = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* p = P + (static_cast<int64_t>(n) * Tp + t0) / 4;
+#pragma unroll 4
+    for (int s = 0; s < splits; ++s) {
+      const float4 x = p[s * split_stride];
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      if (epi == EPI_SWIGLU) {
+        const float4 u = p[s * split_stride + 64 * Tp / 4];
+        up.x += u.x; up.y += u.y; up.z += u.z; up.w += u.w;
+      }
+    }
+    const float av[4] = {acc.x, acc.y, acc.z, acc.w};
+    const float uv[4] = {up.x, up.y, up.z, up.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = t0 + k;
+      if (t >= T) break;
+      const int64_t o = static_cast<int64_t>(t) * ldc + j;
+      if (epi == EPI_SWIGLU)
+        C[o] = f2bf(rbf(silu_f(rbf(av[k]))) * rbf(uv[k]));
+      else if (epi == EPI_RESIDUAL)
+        C[o] = f2bf(rbf(av[k]) + bf2f(residual[static_cast<int64_t>(t) * ldr + j]));
+      else if (epi == EPI_BIAS)
+        C[o] = f2bf(av[k] + bf2f(bias[j]));
+      else
+        C[o] = f2bf(av[k]);
+    }
+  }
+}
+
 // Per token: reduce the per-tile (max, index) pairs, lowest index on ties.
 __global__ void argmax_reduce_kernel(const float2* __restrict__ ws, int tiles, int T,
                                      int64_t* __restrict__ out_ids, float* __restrict__ out_max) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -553,19 +585,19 @@ int make_map(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int6
   return PL_OK;
 }
 
-template <int BN, bool SWAP>
+template <int BN, bool SWAP, int CTAS = (BN <= 128 ? 2 : 1)>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid,
               cudaStream_t st) {
-  constexpr int smem = GemmSmem<BN>::TOTAL;
+  constexpr int smem = GemmSmem<BN, CTAS>::TOTAL;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, SWAP>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, SWAP, CTAS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
     attr_set = true;
   }
-  gemm_tc_kernel<BN, SWAP><<<grid, 192, smem, st>>>(ma, mb, a);
-  return check_launch("gemm_tc_kernel");
+  return launch_k("gemm_tc_kernel", gemm_tc_kernel<BN, SWAP, CTAS>, dim3(grid), dim3(192), smem, st, ma, mb,
+                  a);
 }
 
 int num_sms() {
@@ -593,30 +625,27 @@ int make_tma_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, i
 }
 
 // Split-K factor for the decode (SWAP) path, from the weight shape (N, K) only so a
-// token's result never depends on the batch it rides in: balance tiles*splits work items
-// over the persistent grid (one CTA per SM) with >= 4 k-blocks per split.
+// token's result never depends on the batch it rides in.  Decode GEMMs are HBM
+// streams: a CTA with a 4-6 deep TMA ring pulls ~2x its fair share of bandwidth,
+// so the only goal is to give every SM at least one work item -- any extra split
+// is pure partial-sum traffic.  Smallest split with tiles*splits >= #SMs, each
+// split keeping >= 4 k-blocks.
 int gemm_num_splits(int64_t N, int64_t K, bool swap) {
   if (!swap) return 1;
   const int64_t tiles = (N + BM - 1) / BM;
   const int64_t kb = K / BK;
-  const int sms = 148;
+  const int64_t sms = 148;
   int best = 1;
-  double best_eff = 0.0;
   for (int s = 1; s <= 16; ++s) {
     const int64_t per = (kb + s - 1) / s;
     if (s > 1 && per < 4) break;
-    const int64_t eff_s = (kb + per - 1) / per;  // no empty splits
-    const int64_t items = tiles * eff_s;
-    const double rounds = std::ceil(static_cast<double>(items) / sms);
-    const double eff = static_cast<double>(items) / (rounds * sms);
-    if (eff > best_eff + 0.03) {
-      best_eff = eff;
-      best = static_cast<int>(eff_s);
-    }
+    best = static_cast<int>((kb + per - 1) / per);  // no empty splits
+    if (tiles * best >= sms) break;
   }
   return best;
 }
 
+// Workspace = split-K partials [splits][N][Tp] fp32, or argmax partials [tiles][T].
 int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi) {
   const bool swap = use_swap(T, epi);
   if (epi == EPI_ARGMAX) return ((N + BM - 1) / BM) * T * 8;
@@ -624,8 +653,7 @@ int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi) {
   if (splits <= 1) return 0;
   const int64_t bn = swap_bn(T);
   const int64_t tiles_n = (T + bn - 1) / bn;
-  const int64_t tiles = ((N + BM - 1) / BM) * tiles_n;
-  return align256(tiles * 4) + static_cast<int64_t>(splits) * N * (tiles_n * bn) * 4;
+  return static_cast<int64_t>(splits) * N * (tiles_n * bn) * 4;
 }
 
 int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int64_t ldw,
@@ -671,11 +699,12 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   if (epi == EPI_ARGMAX) {
     a.argmax_ws = reinterpret_cast<float2*>(ws);
   } else if (a.splits > 1) {
-    a.counters = reinterpret_cast<int*>(ws);
-    a.partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) +
-                                         align256(static_cast<int64_t>(a.tiles_m) * tiles_n * 4));
+    a.partial = reinterpret_cast<float*>(ws);
   }
-  const int grid = std::min(a.num_items, num_sms());
+  // PL_GEMM_WIDE=1: one CTA per SM with a deep (~196 KB) ring instead of two shallower ones
+  static const bool wide = [] { const char* v = getenv("PL_GEMM_WIDE"); return v && v[0] == '1'; }();
+  const int per_sm = (swap && bn <= 128 && !wide) ? 2 : 1;
+  const int grid = std::min(a.num_items, num_sms() * per_sm);
 
   CUtensorMap ma, mb;
   int rc;
@@ -683,10 +712,10 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     if ((rc = make_map(&ma, W, N, K, ldw, BM))) return rc;
     if ((rc = make_map(&mb, X, T, K, ldx, bn))) return rc;
     switch (bn) {
-      case 16: rc = launch_tc<16, true>(ma, mb, a, grid, st); break;
-      case 32: rc = launch_tc<32, true>(ma, mb, a, grid, st); break;
-      case 64: rc = launch_tc<64, true>(ma, mb, a, grid, st); break;
-      case 128: rc = launch_tc<128, true>(ma, mb, a, grid, st); break;
+      case 16: rc = wide ? launch_tc<16, true, 1>(ma, mb, a, grid, st) : launch_tc<16, true>(ma, mb, a, grid, st); break;
+      case 32: rc = wide ? launch_tc<32, true, 1>(ma, mb, a, grid, st) : launch_tc<32, true>(ma, mb, a, grid, st); break;
+      case 64: rc = wide ? launch_tc<64, true, 1>(ma, mb, a, grid, st) : launch_tc<64, true>(ma, mb, a, grid, st); break;
+      case 128: rc = wide ? launch_tc<128, true, 1>(ma, mb, a, grid, st) : launch_tc<128, true>(ma, mb, a, grid, st); break;
       default: rc = launch_tc<256, true>(ma, mb, a, grid, st); break;
     }
   } else {
@@ -698,9 +727,16 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
 
   if (epi == EPI_ARGMAX) {
     const int tiles = static_cast<int>((N + BM - 1) / BM);
-    argmax_reduce_kernel<<<static_cast<unsigned>(T), 256, 0, st>>>(
-        reinterpret_cast<const float2*>(ws), tiles, static_cast<int>(T), argmax_out, nullptr);
-    return check_launch("argmax_reduce_kernel");
+    return launch_k("argmax_reduce_kernel", argmax_reduce_kernel, dim3(static_cast<unsigned>(T)),
+                    dim3(256), 0, st, a.argmax_ws, tiles, static_cast<int>(T), argmax_out,
+                    static_cast<float*>(nullptr));
+  }
+  if (a.splits > 1) {
+    const int64_t n_out = (epi == EPI_SWIGLU) ? N / 2 : N;
+    const int64_t total = n_out * ((T + 3) / 4);
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    return launch_k("gemm_splitk_reduce_kernel", gemm_splitk_reduce_kernel, dim3(blocks), dim3(256), 0,
+                    st, a.partial, a.splits, a.T, a.Tp, a.N, epi, C, ldc, bias, residual, ldr);
   }
   return PL_OK;
 }

@@ -48,6 +48,8 @@ __global__ void embed_kernel(const int64_t* __restrict__ ids, const int32_t* __r
                              const int64_t* __restrict__ last_token,
                              const __nv_bfloat16* __restrict__ table, int64_t vocab, int d,
                              __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   int64_t id = ids ? ids[t] : last_token[req_slot[t]];
   if (id < 0 || id >= vocab) id = 0;  // defensive: never read outside the table
@@ -63,9 +65,8 @@ int embed_launch(const int64_t* ids, const int32_t* req_slot, const int64_t* las
   if (d % 8) return set_error(PL_ERR_CONFIG, "embed: d must be a multiple of 8");
   if (!ids && (!req_slot || !last_token))
     return set_error(PL_ERR_CONFIG, "embed: need ids or (req_slot, last_token)");
-  embed_kernel<<<static_cast<unsigned>(T), 128, 0, st>>>(ids, req_slot, last_token, table, vocab,
-                                                         d, out);
-  return check_launch("embed_kernel");
+  return launch_k("embed_kernel", embed_kernel, dim3(static_cast<unsigned>(T)), dim3(128), 0, st,
+                  ids, req_slot, last_token, table, vocab, d, out);
 }
 
 // -------------------------------------------------------------- rmsnorm ---
@@ -79,6 +80,8 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const __nv_bfloat16* __res
                                                       float eps, int d,
                                                       __nv_bfloat16* __restrict__ out,
                                                       int64_t ldo) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int64_t src_row = row_idx ? row_idx[r] : r;
   const uint4* xs = reinterpret_cast<const uint4*>(x + src_row * ldx);
@@ -133,13 +136,10 @@ int rmsnorm_launch(const __nv_bfloat16* x, int64_t ldx, const int32_t* row_idx,
   if (d % 8 || ldx % 8 || ldo % 8 || d > 16384)
     return set_error(PL_ERR_CONFIG, "rmsnorm: d and leading dims must be multiples of 8, d<=16384");
   const int vpt = (d / 8 + 127) / 128;
-  const unsigned g = static_cast<unsigned>(rows);
-  if (vpt <= 1) rmsnorm_kernel<1><<<g, 128, 0, st>>>(x, ldx, row_idx, w, eps, d, out, ldo);
-  else if (vpt <= 2) rmsnorm_kernel<2><<<g, 128, 0, st>>>(x, ldx, row_idx, w, eps, d, out, ldo);
-  else if (vpt <= 4) rmsnorm_kernel<4><<<g, 128, 0, st>>>(x, ldx, row_idx, w, eps, d, out, ldo);
-  else if (vpt <= 8) rmsnorm_kernel<8><<<g, 128, 0, st>>>(x, ldx, row_idx, w, eps, d, out, ldo);
-  else rmsnorm_kernel<16><<<g, 128, 0, st>>>(x, ldx, row_idx, w, eps, d, out, ldo);
-  return check_launch("rmsnorm_kernel");
+  const dim3 g(static_cast<unsigned>(rows));
+  auto k = vpt <= 1 ? rmsnorm_kernel<1> : vpt <= 2 ? rmsnorm_kernel<2> : vpt <= 4 ? rmsnorm_kernel<4>
+         : vpt <= 8 ? rmsnorm_kernel<8> : rmsnorm_kernel<16>;
+  return launch_k("rmsnorm_kernel", k, g, dim3(128), 0, st, x, ldx, row_idx, w, eps, d, out, ldo);
 }
 
 // ------------------------------------------------------ rope + KV append ---
@@ -155,6 +155,8 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int64_t ldqkv,
                                __nv_bfloat16* __restrict__ k_cache,
                                __nv_bfloat16* __restrict__ v_cache, int block_size, int Hq, int Hkv,
                                int hd) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const int half = hd / 2;
   const int vec_per_head = half / 8;
@@ -217,10 +219,8 @@ int rope_kv_launch(__nv_bfloat16* qkv, int64_t ldqkv, const int32_t* pos, const 
   if (hd % 16 || ldqkv % 8) return set_error(PL_ERR_CONFIG, "rope: hd must be a multiple of 16");
   if (slot && (!k_cache || !v_cache || block_size <= 0))
     return set_error(PL_ERR_CONFIG, "rope: caches required when slots are given");
-  rope_kv_kernel<<<static_cast<unsigned>(T), 128, 0, st>>>(qkv, ldqkv, pos, slot, cos_sin, max_pos,
-                                                           k_cache, v_cache, block_size, Hq, Hkv,
-                                                           hd);
-  return check_launch("rope_kv_kernel");
+  return launch_k("rope_kv_kernel", rope_kv_kernel, dim3(static_cast<unsigned>(T)), dim3(128), 0, st,
+                  qkv, ldqkv, pos, slot, cos_sin, max_pos, k_cache, v_cache, block_size, Hq, Hkv, hd);
 }
 
 // -------------------------------------------------------- token scatter ---
@@ -230,6 +230,8 @@ __global__ void token_scatter_kernel(const int64_t* __restrict__ ids,
                                      const int32_t* __restrict__ out_pos, int R,
                                      int64_t* __restrict__ last_token,
                                      int64_t* __restrict__ gen_tokens, int gen_stride) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
   const int64_t id = ids[r];
@@ -242,9 +244,8 @@ int token_scatter_launch(const int64_t* ids, const int32_t* req_slot, const int3
                          int64_t* last_token, int64_t* gen_tokens, int gen_stride,
                          cudaStream_t st) {
   if (R <= 0) return PL_OK;
-  token_scatter_kernel<<<(R + 127) / 128, 128, 0, st>>>(ids, req_slot, out_pos, R, last_token,
-                                                        gen_tokens, gen_stride);
-  return check_launch("token_scatter_kernel");
+  return launch_k("token_scatter_kernel", token_scatter_kernel, dim3((R + 127) / 128), dim3(128), 0,
+                  st, ids, req_slot, out_pos, R, last_token, gen_tokens, gen_stride);
 }
 
 }  // namespace pl

@@ -27,6 +27,29 @@ int set_error(int code, const char* fmt, ...);
 int set_cuda_error(cudaError_t e, const char* what);
 int check_launch(const char* what);
 
+// PDL on/off (env PL_PDL=0 disables programmatic dependent launch)
+bool pdl_enabled();
+
+// Launch with programmatic stream serialization so the kernel may start while its
+// predecessor in the stream drains (see pdl_wait / pdl_trigger in common.cuh).
+template <typename... KArgs, typename... Args>
+int launch_k(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+             cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) return set_cuda_error(e, what);
+  return check_launch(what);
+}
+
 // gemm_tc.cu
 // cached 2-D bf16 TMA descriptor: [rows, cols] row-major (ld elements), box {64, box_rows}, SW128
 int make_tma_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld,

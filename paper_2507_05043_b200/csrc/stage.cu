@@ -232,7 +232,7 @@ int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* laye
   if (!workspace || workspace_bytes < L.total)
     return set_error(PL_ERR_CONFIG, "stage_create: workspace %lld < required %lld",
                      (long long)workspace_bytes, (long long)L.total);
-  // split-K arrival counters live in the workspace and must start at zero
+  // deterministic initial contents (never read before written)
   cudaError_t e = cudaMemset(workspace, 0, static_cast<size_t>(L.total));
   if (e != cudaSuccess) return set_cuda_error(e, "stage workspace memset");
   Stage* s = new Stage();

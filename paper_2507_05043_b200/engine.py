@@ -42,6 +42,7 @@ class B200Stats:
     decode_start_s: float | None = None
     total_tokens: int = 0
     decode_tokens: int = 0
+    real: object = None                 # pipelink RunResult on the device clock
     extra: dict = field(default_factory=dict)
 
     @property
@@ -132,8 +133,43 @@ class B200PipelineEngine(PipelineDriver):
             stats.token_times_s = times
             stats.total_tokens = sum(len(v) for v in g.tokens.values())
             stats.decode_tokens = sum(max(0, len(v) - 1) for v in g.tokens.values())
+        stats.real = self._real_result(result)
         result.b200 = stats
         return result
+
+    def _real_result(self, virtual):
+        """The run re-expressed on the device clock as a reference RunResult, so the
+        unchanged summarize() / measure_bubble() (metrics.py:78-117, engine.py:130-144)
+        report measured TTFT/TPOT/throughput/bubbles.  Stage intervals cover this
+        rank's stages; token times exist on the head rank."""
+        g = self.gpu
+        S = len(self.stage_profiles)
+        busy = [[(a, b) for _, a, b in g.busy_real_ns.get(s, [])] for s in range(S)]
+        first_compute = {}
+        for mb_id, a, _ in g.busy_real_ns.get(0, []):
+            for rid in g.mb_requests.get(mb_id, ()):
+                first_compute.setdefault(rid, a)
+        emissions = []
+        reqs = []
+        times = {}
+        if g.tokens is not None:
+            for t, (_, rids) in zip(g.fb_times_s, g.fb_events):
+                for rid in rids:
+                    emissions.append((round(t * 1e9), rid))
+                    times.setdefault(rid, []).append(t)
+        for r in virtual.requests:
+            c = r.fresh_copy()
+            c.arrival_time = r.arrival_time
+            c.state, c.tokens_emitted = r.state, r.tokens_emitted
+            ts = times.get(r.id)
+            if ts:
+                c.first_token_time, c.finish_time = ts[0], ts[-1]
+            reqs.append(c)
+        end_ns = round(g.run_time_s * 1e9)
+        return pipelink.engine.RunResult(
+            requests=reqs, events=[], link_events=[], decisions=virtual.decisions, stage_busy_ns=busy,
+            token_emissions=sorted(emissions), first_compute_ns=first_compute, end_ns=end_ns,
+            all_finished=virtual.all_finished)
 
     def prepare(self, trace) -> None:
         """Allocate weights, KV cache and buffers for `trace` ahead of the first run."""

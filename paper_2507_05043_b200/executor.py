@@ -91,7 +91,7 @@ class StageExecutor:
                 }
                 self.layers.append(L)
             self.embed = self.final_norm = self.lm_head = None
-            embed_scale = 1.0 if s.peaked else s.embed_scale
+            embed_scale = s.peaked_embed_scale if s.peaked else s.embed_scale
             if self.is_first:
                 self.embed = ops.fill_hash_(e(s.vocab, s.d), seed, T_EMBED, embed_scale)
             if self.is_last:

@@ -33,6 +33,18 @@ def _need_cuda(*ts: torch.Tensor | None) -> None:
             raise N.ConfigError("libb200link kernels take CUDA tensors only (no CPU fallback)")
 
 
+_WS: dict = {}
+
+
+def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
+    """Per-device scratch reused across calls (stream-ordered on the current stream)."""
+    buf = _WS.get(device)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WS[device] = buf
+    return buf
+
+
 def fill_hash_(t: torch.Tensor, seed: int, tensor_id: int, scale: float, offset: float = 0.0,
                stream=None) -> torch.Tensor:
     _need_cuda(t)
@@ -75,7 +87,7 @@ def gemm(x: torch.Tensor, w: torch.Tensor, epilogue: int = EPI_NONE,
     if K != Kw:
         raise N.ConfigError(f"gemm: K mismatch {K} vs {Kw}")
     ws_bytes = N.lib().pl_gemm_workspace_bytes(T, Nw, K, epilogue)
-    ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)  # split-K counters start at 0
+    ws = _workspace(x.device, ws_bytes)
     ids = None
     if epilogue == EPI_ARGMAX:
         ids = torch.empty(T, dtype=torch.int64, device=x.device)

@@ -61,10 +61,13 @@ class DecoderSpec:
     embed_scale: float = 0.02 * math.sqrt(3.0)
     norm_jitter: float = 0.05
     bias_scale: float = 0.02
-    # "peaked" init: lm_head[v] = lm_alpha * embed[(v + 1) % vocab], large embed;
-    # argmax margins dwarf bf16 rounding so greedy ids are robustly identical.
+    # "peaked" init: embed ~ U(+-peaked_embed_scale), lm_head[v] = lm_alpha * embed[(v+1) % V].
+    # The token embedding then dominates the residual stream through all layers
+    # (|e|^2 = d*s^2/3 vs max_v <layer contributions, e_v>), so argmax margins dwarf
+    # bf16/accumulation-order differences and greedy ids are robustly identical.
     peaked: bool = False
     lm_alpha: float = 4.0
+    peaked_embed_scale: float = 8.0
 
     def __post_init__(self) -> None:
         if self.Hq % self.Hkv:

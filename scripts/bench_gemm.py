@@ -1,0 +1,70 @@
+"""Micro-benchmark of the decode GEMMs / attention at model shapes (CUDA events).
+
+    python scripts/bench_gemm.py [--T 64] [--model l3|q2]
+
+Weights rotate over enough copies to exceed the 126 MB L2, so every call
+streams its weights from HBM.  Prints one JSON line per kernel with the
+average launch time and achieved GB/s of algorithmic bytes.
+"""
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch  # noqa: E402
+
+from paper_2507_05043_b200 import LLAMA3_8B, QWEN2_72B, ops  # noqa: E402
+
+
+def timeit(fn, iters=50, warm=5):
+    for _ in range(warm):
+        fn(0)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for i in range(iters):
+        fn(i)
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / iters * 1e3  # us
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--T", type=int, nargs="+", default=[8, 16, 32, 64])
+    ap.add_argument("--model", default="l3")
+    a = ap.parse_args()
+    spec = {"l3": LLAMA3_8B, "q2": QWEN2_72B}[a.model]
+    dev = torch.device("cuda", 0)
+    shapes = {"qkv": (spec.qkv_dim, spec.d, ops.EPI_NONE), "o": (spec.d, spec.attn_dim, ops.EPI_RESIDUAL),
+              "gate_up": (2 * spec.ffn, spec.d, ops.EPI_SWIGLU), "down": (spec.d, spec.ffn, ops.EPI_RESIDUAL),
+              "lm_head": (spec.vocab, spec.d, ops.EPI_ARGMAX)}
+    for name, (N, K, epi) in shapes.items():
+        wbytes = N * K * 2
+        copies = max(1, -(-300_000_000 // wbytes))
+        ws = [torch.randn(N, K, device=dev).to(torch.bfloat16) * 0.02 for _ in range(copies)]
+        for T in a.T:
+            x = torch.randn(T, K, device=dev).to(torch.bfloat16)
+            res = torch.randn(T, N, device=dev).to(torch.bfloat16) if epi == ops.EPI_RESIDUAL else None
+            out = torch.empty(T, N // 2 if epi == ops.EPI_SWIGLU else N, device=dev, dtype=torch.bfloat16)
+
+            def fn(i):
+                if epi == ops.EPI_RESIDUAL:
+                    ops.gemm(x, ws[i % copies], epi, residual=res, out=res)
+                elif epi == ops.EPI_ARGMAX:
+                    ops.gemm(x, ws[i % copies], epi)
+                else:
+                    ops.gemm(x, ws[i % copies], epi, out=out)
+
+            us = timeit(fn)
+            print(json.dumps({"kernel": name, "T": T, "N": N, "K": K, "us": round(us, 2),
+                              "GBps": round(wbytes / us / 1e3, 1)}), flush=True)
+        del ws
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

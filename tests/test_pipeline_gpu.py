@@ -208,3 +208,21 @@ def test_llama3_shape_truncated_tokens_identical():
     _, _, want = oracle_greedy(spec, trace)
     for i, r in enumerate(trace.requests):
         assert np.array_equal(res.b200.tokens[r.id], want[i].numpy())
+
+
+def test_real_clock_run_result_feeds_reference_metrics():
+    """RunResult on the device clock: summarize()/measure_bubble() apply unchanged."""
+    spec = TINY.with_(peaked=True)
+    cfg, cluster, plan, trace = config1(spec, S=2, n_req=6, in_len=64, out_len=8)
+    res = run_gpu(spec, cfg, cluster, plan, trace)
+    real = res.b200.real
+    rep = pipelink.summarize(real.requests)
+    assert rep.total_tokens == 6 * 8
+    assert 0 < rep.ttft_p50_s <= rep.span_s <= res.b200.run_time_s + 1e-6
+    for s in range(2):
+        assert real.stage_busy_ns[s], "no real busy intervals"
+        b = pipelink.measure_bubble(real, s, 0.0, real.end_ns / 1e9)
+        assert 0.0 <= b < 1.0
+    # per-request tokens are emitted in order on the device clock
+    for rid, ts in res.b200.token_times_s.items():
+        assert ts == sorted(ts) and len(ts) == 8
