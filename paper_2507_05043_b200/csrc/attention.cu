@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(128)
                        const int32_t* __restrict__ block_table, int max_blocks,
                        const int32_t* __restrict__ ctx_len, int Hkv, float scale_log2,
                        __nv_bfloat16* __restrict__ out, int64_t ldo, float* __restrict__ ws_o,
-                       float2* __restrict__ ws_ml) {
+                       float2* __restrict__ ws_ml, int* __restrict__ counters) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -460,34 +460,43 @@ __global__ void __launch_bounds__(128)
       if (e == 0) ws_ml[base] = make_float2(M, L);
     }
   }
-}
+  if (nsplit == 1) return;
 
-// Merge the per-split partial softmax states in split order.
-__global__ void attn_decode_combine_kernel(const float* __restrict__ ws_o,
-                                           const float2* __restrict__ ws_ml, int Hq, int nsplit,
-                                           __nv_bfloat16* __restrict__ out, int64_t ldo) {
-  pdl_trigger();
-  pdl_wait();
-  const int head = blockIdx.x, r = blockIdx.y, e = threadIdx.x;
-  const int64_t base = (static_cast<int64_t>(r) * Hq + head) * nsplit;
-  float M = -INFINITY;
-  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, ws_ml[base + s].x);
-  float Lsum = 0.f, o = 0.f;
-  for (int s = 0; s < nsplit; ++s) {
-    const float2 ml = ws_ml[base + s];
-    if (ml.x == -INFINITY) continue;
-    const float w = exp2f(ml.x - M);
-    Lsum += ml.y * w;
-    o += ws_o[(base + s) * HD + e] * w;
+  // Split merge fused in: the last split CTA of this (request, kv head) to finish
+  // combines every split's state in split order (deterministic) and resets the counter.
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&counters[r * Hkv + kh], 1) == nsplit - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int head = kh * G + g;
+    const int64_t base = (static_cast<int64_t>(r) * Hq + head) * nsplit;
+    float M = -INFINITY;
+    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(&ws_ml[base + s]).x);
+    float Lsum = 0.f, o = 0.f;
+    for (int s = 0; s < nsplit; ++s) {
+      const float2 ml = __ldcg(&ws_ml[base + s]);
+      if (ml.x == -INFINITY) continue;
+      const float w = exp2f(ml.x - M);
+      Lsum += ml.y * w;
+      o += __ldcg(&ws_o[(base + s) * HD + e]) * w;
+    }
+    out[static_cast<int64_t>(r) * ldo + head * HD + e] = f2bf(Lsum > 0.f ? o / Lsum : 0.f);
   }
-  out[static_cast<int64_t>(r) * ldo + head * HD + e] = f2bf(Lsum > 0.f ? o / Lsum : 0.f);
+  if (threadIdx.x == 0) counters[r * Hkv + kh] = 0;
 }
 
+// Workspace: [R*Hkv arrival counters, zero between launches | o partials | (m, l)].
 int64_t attn_decode_workspace_bytes(int R, int Hq, int max_ctx, int hd) {
   const int pages = (max_ctx + PAGE - 1) / PAGE;
   const int nsplit = std::max(1, (pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
   if (nsplit == 1) return 0;
-  return static_cast<int64_t>(R) * Hq * nsplit * (hd * 4 + 8);
+  const int64_t counters = ((static_cast<int64_t>(R) * Hq * 4 + 255) / 256) * 256;
+  return counters + static_cast<int64_t>(R) * Hq * nsplit * (hd * 4 + 8);
 }
 
 int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16* k_cache,
@@ -513,8 +522,12 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
   const int64_t rows = num_blocks * Hkv * PAGE;
   if ((rc = make_tma_2d(&mk, k_cache, rows, HD, HD, 64))) return rc;
   if ((rc = make_tma_2d(&mv, v_cache, rows, HD, HD, 64))) return rc;
-  float* ws_o = reinterpret_cast<float*>(ws);
-  float2* ws_ml = need > 0 ? reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(ws) +
+  // counters are sized for R*Hq (>= R*Hkv) so the layout only depends on (R, Hq, max_ctx)
+  const int64_t counter_bytes = ((static_cast<int64_t>(R) * Hq * 4 + 255) / 256) * 256;
+  int* counters = need > 0 ? reinterpret_cast<int*>(ws) : nullptr;
+  float* ws_o = need > 0 ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + counter_bytes)
+                         : nullptr;
+  float2* ws_ml = need > 0 ? reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(ws_o) +
                                                        static_cast<int64_t>(R) * Hq * nsplit * hd * 4)
                            : nullptr;
   dim3 grid(Hkv, R, nsplit);
@@ -530,7 +543,8 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
       attr = true;                                                                              \
     }                                                                                           \
     rc = launch_k("attn_decode_kernel", attn_decode_kernel<GG>, grid, dim3(128), smem, st, mk,  \
-                  mv, q, ldq, block_table, max_blocks, ctx_len, Hkv, sl2, out, ldo, ws_o, ws_ml); \
+                  mv, q, ldq, block_table, max_blocks, ctx_len, Hkv, sl2, out, ldo, ws_o, ws_ml,  \
+                  counters);                                                                    \
     break;                                                                                      \
   }
   switch (G) {
@@ -542,9 +556,7 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
       return set_error(PL_ERR_CONFIG, "attn_decode: GQA group %d unsupported (1,2,4,8)", G);
   }
 #undef PL_DECODE_CASE
-  if (rc || nsplit == 1) return rc;
-  return launch_k("attn_decode_combine_kernel", attn_decode_combine_kernel, dim3(Hq, R), dim3(HD), 0,
-                  st, ws_o, ws_ml, Hq, nsplit, out, ldo);
+  return rc;
 }
 
 }  // namespace pl

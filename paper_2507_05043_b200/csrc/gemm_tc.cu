@@ -58,8 +58,10 @@ struct GemmArgs {
   const __nv_bfloat16* bias;
   const __nv_bfloat16* residual;
   int64_t ldr;
-  float* partial;     // [splits][N][Tp] fp32 (split-K), Tp = T rounded up to the BN tile
-  int Tp;
+  float* partial;     // split-K partials, fp32: pmode 0 [splits][N][Tp], pmode 1 [splits][T][N]
+  int Tp;             // T rounded up to the BN tile
+  int pmode;
+  int l2_prefetch;    // weight k-blocks warmed in L2 beyond the smem ring before the PDL wait
   float2* argmax_ws;  // [N/128 tiles][T] (value, index-as-float-bits)
 };
 
@@ -176,6 +178,12 @@ __global__ void __launch_bounds__(192, CTAS)
             if (SWAP) tma_load_2d(sa, &tmA, &full[i], kc, m_tile * BM, polA);
             else tma_load_2d(sa + A_TILE_BYTES, &tmB, &full[i], kc, n_tile * BN, polB);
           }
+          // ...and warm L2 with the next weight tiles beyond the ring, so HBM keeps
+          // streaming this kernel's weights while the predecessor drains
+          if (SWAP) {
+            const int pf_end = min(nkb, pre + args.l2_prefetch);
+            for (int j = pre; j < pf_end; ++j) tma_prefetch_l2_2d(&tmA, (kb0 + j) * BK, m_tile * BM);
+          }
           pdl_wait();
           for (int j = 0; j < pre; ++j) {
             uint8_t* sa = smem + j * L::STAGE_BYTES;
@@ -257,7 +265,22 @@ __global__ void __launch_bounds__(192, CTAS)
         // lane <-> feature n, column <-> token t
         const int n = m_tile * BM + row;
         const int t_base = n_tile * BN;
-        if (args.splits > 1) {
+        if (args.splits > 1 && args.pmode == 1) {
+          // feature-contiguous partials [split][T][N] (per-token fused reductions)
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tcol + c0, r);
+            tmem_ld_wait();
+            if (n < args.N) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const int t = t_base + c0 + c;
+                if (t < args.T)
+                  args.partial[((int64_t)split * args.T + t) * args.N + n] = __uint_as_float(r[c]);
+              }
+            }
+          }
+        } else if (args.splits > 1) {
           // partials are token-contiguous per feature row: [split][N][Tp]
           float* prow = args.partial + ((int64_t)split * args.N + n) * args.Tp + t_base;
           for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -471,6 +494,127 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Fused decode epilogue 1: split-K reduce + residual add + the NEXT RMSNorm, one CTA
+// per token row (partials feature-contiguous, [splits][T][N]):
+//   h[t]  = bf16(bf16(sum_s partial) + h[t])             (residual, modeling_llama.py:313-331)
+//   a[t]  = bf16(w * bf16(h[t] * rsqrt(mean(h[t]^2)+eps)))   (RMSNorm, :62-67)
+template <int VPT>  // float4 chunks per thread (N <= 1024 * VPT)
+__global__ void __launch_bounds__(256)
+    reduce_residual_norm_kernel(const float* __restrict__ partial, int splits, int T, int N,
+                                __nv_bfloat16* __restrict__ h, int64_t ldh,
+                                const __nv_bfloat16* __restrict__ w, float eps,
+                                __nv_bfloat16* __restrict__ a, int64_t lda) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x;
+  float hv[VPT][4];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int f = (threadIdx.x + 256 * k) * 4;
+    if (f >= N) continue;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* p = reinterpret_cast<const float4*>(partial + static_cast<int64_t>(t) * N + f);
+    const int64_t stride = static_cast<int64_t>(T) * N / 4;
+    for (int s = 0; s < splits; ++s) {
+      const float4 x = p[s * stride];
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    uint2* hp = reinterpret_cast<uint2*>(h + static_cast<int64_t>(t) * ldh + f);
+    const uint2 old = *hp;
+    const float2 o0 = unpack_bf16x2(old.x), o1 = unpack_bf16x2(old.y);
+    hv[k][0] = rbf(rbf(acc.x) + o0.x);
+    hv[k][1] = rbf(rbf(acc.y) + o0.y);
+    hv[k][2] = rbf(rbf(acc.z) + o1.x);
+    hv[k][3] = rbf(rbf(acc.w) + o1.y);
+    *hp = make_uint2(pack_bf16x2(hv[k][0], hv[k][1]), pack_bf16x2(hv[k][2], hv[k][3]));
+    ss += hv[k][0] * hv[k][0] + hv[k][1] * hv[k][1] + hv[k][2] * hv[k][2] + hv[k][3] * hv[k][3];
+  }
+  __shared__ float red[8];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) tot += red[i];
+  const float inv = 1.0f / sqrtf(tot / static_cast<float>(N) + eps);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int f = (threadIdx.x + 256 * k) * 4;
+    if (f >= N) continue;
+    const uint2 wv = *reinterpret_cast<const uint2*>(w + f);
+    const float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y);
+    *reinterpret_cast<uint2*>(a + static_cast<int64_t>(t) * lda + f) =
+        make_uint2(pack_bf16x2(w0.x * rbf(hv[k][0] * inv), w0.y * rbf(hv[k][1] * inv)),
+                   pack_bf16x2(w1.x * rbf(hv[k][2] * inv), w1.y * rbf(hv[k][3] * inv)));
+  }
+}
+
+// Fused decode epilogue 2: QKV split-K reduce (+ Qwen2 bias) + neox RoPE on q and k
+// (HF per-op bf16 rounding, as rope_kv_kernel) + paged K/V append.  One thread per
+// (head, rotary pair i, 4 tokens); partials token-contiguous, [splits][N][Tp].
+__global__ void __launch_bounds__(256)
+    reduce_qkv_rope_kernel(const float* __restrict__ partial, int splits, int T, int Tp, int N,
+                           const __nv_bfloat16* __restrict__ bias, __nv_bfloat16* __restrict__ qkv,
+                           int64_t ldqkv, const int32_t* __restrict__ pos,
+                           const int32_t* __restrict__ slot, const __nv_bfloat16* __restrict__ cos_sin,
+                           int max_pos, __nv_bfloat16* __restrict__ k_cache,
+                           __nv_bfloat16* __restrict__ v_cache, int block_size, int Hq, int Hkv) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int HDIM = 128, HALF = 64;
+  const int heads = Hq + 2 * Hkv;
+  const int tq = (T + 3) / 4;
+  const int64_t total = static_cast<int64_t>(heads) * HALF * tq;
+  const int64_t split_stride = static_cast<int64_t>(N) * Tp / 4;
+  const float4* P = reinterpret_cast<const float4*>(partial);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(idx % HALF);
+    const int hh = static_cast<int>((idx / HALF) % heads);
+    const int t0 = static_cast<int>(idx / (HALF * heads)) * 4;
+    const int n1 = hh * HDIM + i, n2 = n1 + HALF;
+    float4 a1 = make_float4(0.f, 0.f, 0.f, 0.f), a2 = a1;
+    const float4* p1 = P + (static_cast<int64_t>(n1) * Tp + t0) / 4;
+    const float4* p2 = P + (static_cast<int64_t>(n2) * Tp + t0) / 4;
+    for (int s = 0; s < splits; ++s) {
+      const float4 x = p1[s * split_stride], y = p2[s * split_stride];
+      a1.x += x.x; a1.y += x.y; a1.z += x.z; a1.w += x.w;
+      a2.x += y.x; a2.y += y.y; a2.z += y.z; a2.w += y.w;
+    }
+    const float b1 = bias ? bf2f(bias[n1]) : 0.f, b2 = bias ? bf2f(bias[n2]) : 0.f;
+    const float v1[4] = {rbf(a1.x + b1), rbf(a1.y + b1), rbf(a1.z + b1), rbf(a1.w + b1)};
+    const float v2[4] = {rbf(a2.x + b2), rbf(a2.y + b2), rbf(a2.z + b2), rbf(a2.w + b2)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = t0 + k;
+      if (t >= T) break;
+      float o1 = v1[k], o2 = v2[k];
+      if (hh < Hq + Hkv) {
+        int pp = pos[t];
+        pp = pp < 0 ? 0 : (pp >= max_pos ? max_pos - 1 : pp);
+        const float c = bf2f(cos_sin[static_cast<int64_t>(pp) * HDIM + i]);
+        const float sn = bf2f(cos_sin[static_cast<int64_t>(pp) * HDIM + HALF + i]);
+        o1 = rbf(rbf(v1[k] * c) + rbf(-v2[k] * sn));
+        o2 = rbf(rbf(v2[k] * c) + rbf(v1[k] * sn));
+      }
+      __nv_bfloat16* row = qkv + static_cast<int64_t>(t) * ldqkv;
+      row[n1] = f2bf(o1);
+      row[n2] = f2bf(o2);
+      const int sl = slot ? slot[t] : -1;
+      if (hh >= Hq && sl >= 0) {
+        const bool is_k = hh < Hq + Hkv;
+        const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
+        __nv_bfloat16* cache = is_k ? k_cache : v_cache;
+        __nv_bfloat16* dst = cache + ((static_cast<int64_t>(sl / block_size) * Hkv + kh) * block_size +
+                                      sl % block_size) * HDIM;
+        dst[i] = f2bf(o1);
+        dst[i + HALF] = f2bf(o2);
+      }
+    }
+  }
+}
+
 // Per token: reduce the per-tile (max, index) pairs, lowest index on ties.
 __global__ void argmax_reduce_kernel(const float2* __restrict__ ws, int tiles, int T,
                                      int64_t* __restrict__ out_ids, float* __restrict__ out_max) {
@@ -659,7 +803,9 @@ int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi) {
 int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int64_t ldw,
                 const __nv_bfloat16* bias, __nv_bfloat16* C, int64_t ldc,
                 const __nv_bfloat16* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,
-                int epi, void* ws, int64_t ws_bytes, int64_t* argmax_out, cudaStream_t st) {
+                int epi, void* ws, int64_t ws_bytes, int64_t* argmax_out, cudaStream_t st,
+                const FusedEpi* fuse, bool* fused) {
+  if (fused) *fused = false;
   if (T <= 0) return PL_OK;
   if (K % BK != 0 || N <= 0 || K <= 0)
     return set_error(PL_ERR_CONFIG, "gemm: K must be a positive multiple of 64 (K=%lld N=%lld)",
@@ -692,6 +838,16 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   const int tiles_n = static_cast<int>(swap ? (T + bn - 1) / bn : (N + bn - 1) / bn);
   a.num_items = a.tiles_m * tiles_n * a.splits;
   a.Tp = tiles_n * bn;
+  // the fused epilogues only apply on the split-K path (their reduction is the epilogue)
+  const int fkind = (fuse && a.splits > 1 && swap) ? fuse->kind : FUSE_NONE;
+  if (fkind == FUSE_RESIDUAL_NORM && (epi != EPI_RESIDUAL || N > 8192 || N % 4))
+    return set_error(PL_ERR_CONFIG, "gemm: residual+norm fusion needs a RESIDUAL GEMM, N <= 8192");
+  if (fkind == FUSE_QKV_ROPE && (epi != EPI_STORE && epi != EPI_BIAS))
+    return set_error(PL_ERR_CONFIG, "gemm: qkv+rope fusion needs a STORE/BIAS GEMM");
+  a.pmode = fkind == FUSE_RESIDUAL_NORM ? 1 : 0;
+  // L2 warm-up only for weights that comfortably fit the 126 MB L2 (PL_L2PF overrides)
+  static const int l2pf = [] { const char* v = getenv("PL_L2PF"); return v ? atoi(v) : 16; }();
+  a.l2_prefetch = (swap && N * K * 2 <= (64ll << 20)) ? l2pf : 0;
   const int64_t need = gemm_workspace_bytes(T, N, K, epi);
   if (need > 0 && (ws_bytes < need || !ws))
     return set_error(PL_ERR_CONFIG, "gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
@@ -730,6 +886,25 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     return launch_k("argmax_reduce_kernel", argmax_reduce_kernel, dim3(static_cast<unsigned>(T)),
                     dim3(256), 0, st, a.argmax_ws, tiles, static_cast<int>(T), argmax_out,
                     static_cast<float*>(nullptr));
+  }
+  if (fkind == FUSE_RESIDUAL_NORM) {
+    if (fused) *fused = true;
+    const int vpt = static_cast<int>((N + 1023) / 1024);
+    auto k = vpt <= 1 ? reduce_residual_norm_kernel<1> : vpt <= 2 ? reduce_residual_norm_kernel<2>
+           : vpt <= 4 ? reduce_residual_norm_kernel<4> : reduce_residual_norm_kernel<8>;
+    return launch_k("reduce_residual_norm_kernel", k, dim3(static_cast<unsigned>(T)), dim3(256), 0, st,
+                    a.partial, a.splits, a.T, a.N, C, ldc, fuse->norm_w, fuse->eps, fuse->norm_out,
+                    fuse->ld_norm);
+  }
+  if (fkind == FUSE_QKV_ROPE) {
+    if (fused) *fused = true;
+    const int heads = fuse->Hq + 2 * fuse->Hkv;
+    const int64_t total = static_cast<int64_t>(heads) * 64 * ((T + 3) / 4);
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    return launch_k("reduce_qkv_rope_kernel", reduce_qkv_rope_kernel, dim3(blocks), dim3(256), 0, st,
+                    a.partial, a.splits, a.T, a.Tp, a.N, bias, C, ldc, fuse->pos, fuse->slot,
+                    fuse->cos_sin, fuse->max_pos, fuse->k_cache, fuse->v_cache, fuse->block_size,
+                    fuse->Hq, fuse->Hkv);
   }
   if (a.splits > 1) {
     const int64_t n_out = (epi == EPI_SWIGLU) ? N / 2 : N;

@@ -56,10 +56,30 @@ int make_tma_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, i
                 int box_rows);
 int gemm_num_splits(int64_t N, int64_t K, bool swap);
 int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi);
+// Decode-path epilogue fusions applied by the split-K reduction (stage runtime only).
+enum FuseKind : int { FUSE_NONE = 0, FUSE_RESIDUAL_NORM = 1, FUSE_QKV_ROPE = 2 };
+struct FusedEpi {
+  int kind = FUSE_NONE;
+  // FUSE_RESIDUAL_NORM: C (= residual) updated in place, then norm_out = rmsnorm(C) * norm_w
+  const __nv_bfloat16* norm_w = nullptr;
+  float eps = 0.f;
+  __nv_bfloat16* norm_out = nullptr;
+  int64_t ld_norm = 0;
+  // FUSE_QKV_ROPE: RoPE on q,k of C + K/V append to the paged caches
+  const int32_t* pos = nullptr;
+  const int32_t* slot = nullptr;
+  const __nv_bfloat16* cos_sin = nullptr;
+  int max_pos = 0;
+  __nv_bfloat16* k_cache = nullptr;
+  __nv_bfloat16* v_cache = nullptr;
+  int block_size = 0, Hq = 0, Hkv = 0;
+};
+
 int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int64_t ldw,
                 const __nv_bfloat16* bias, __nv_bfloat16* C, int64_t ldc,
                 const __nv_bfloat16* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,
-                int epi, void* ws, int64_t ws_bytes, int64_t* argmax_out, cudaStream_t st);
+                int epi, void* ws, int64_t ws_bytes, int64_t* argmax_out, cudaStream_t st,
+                const FusedEpi* fuse = nullptr, bool* fused = nullptr);
 
 // kernels.cu
 int fill_hash_launch(__nv_bfloat16* dst, int64_t n, uint32_t seed, uint32_t tensor_id,

@@ -16,6 +16,7 @@
 //   hidden = hidden + m . Wd^T                  tcgen05 GEMM, RESIDUAL epilogue
 // First stage: hidden = embed(ids).  Last stage: final norm of each request's
 // last row, lm_head GEMM with fused argmax -> int64 token ids (engine.py:409).
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -142,22 +143,44 @@ struct Stage {
       if (rc) return rc;
     }
 
+    // Decode-path fusions (split-K reductions double as epilogues): QKV reduce + RoPE +
+    // KV append, and residual reduce + the next RMSNorm.  `a_ready` tracks whether the
+    // previous fused reduction already produced this layer's normalized input.
+    static const bool fuse_on = [] { const char* v = getenv("PL_FUSE"); return !(v && v[0] == '0'); }();
+    bool a_ready = false;
     for (int l = 0; l < c.num_layers; ++l) {
       const pl_layer_weights& w = layers[l];
       cudaEvent_t* ev = (l == probe_layer) ? next_probe(mb.phase, T) : nullptr;
       auto mark = [&](int i) {
         if (ev) cudaEventRecord(ev[i], st);
       };
-      if ((rc = rmsnorm_launch(hid, d, nullptr, static_cast<const __nv_bfloat16*>(w.attn_norm), c.eps,
+      if (!a_ready &&
+          (rc = rmsnorm_launch(hid, d, nullptr, static_cast<const __nv_bfloat16*>(w.attn_norm), c.eps,
                                T, c.d, a, d, st)))
         return rc;
       mark(0);
+      FusedEpi qf;
+      if (fuse_on) {
+        qf.kind = FUSE_QKV_ROPE;
+        qf.pos = pos;
+        qf.slot = slot;
+        qf.cos_sin = static_cast<const __nv_bfloat16*>(c.cos_sin);
+        qf.max_pos = c.max_pos;
+        qf.k_cache = static_cast<__nv_bfloat16*>(w.k_cache);
+        qf.v_cache = static_cast<__nv_bfloat16*>(w.v_cache);
+        qf.block_size = c.block_size;
+        qf.Hq = c.Hq;
+        qf.Hkv = c.Hkv;
+      }
+      bool roped = false;
       if ((rc = gemm_launch(a, d, static_cast<const __nv_bfloat16*>(w.w_qkv), d,
                             static_cast<const __nv_bfloat16*>(w.b_qkv), qkv, qkv_dim, nullptr, 0, T,
-                            qkv_dim, d, w.b_qkv ? EPI_BIAS : EPI_STORE, gws, gws_bytes, nullptr, st)))
+                            qkv_dim, d, w.b_qkv ? EPI_BIAS : EPI_STORE, gws, gws_bytes, nullptr, st,
+                            &qf, &roped)))
         return rc;
       mark(1);
-      if ((rc = rope_kv_launch(qkv, qkv_dim, pos, slot, static_cast<const __nv_bfloat16*>(c.cos_sin),
+      if (!roped &&
+          (rc = rope_kv_launch(qkv, qkv_dim, pos, slot, static_cast<const __nv_bfloat16*>(c.cos_sin),
                                c.max_pos, static_cast<__nv_bfloat16*>(w.k_cache),
                                static_cast<__nv_bfloat16*>(w.v_cache), c.block_size, T, c.Hq, c.Hkv,
                                c.hd, st)))
@@ -174,11 +197,26 @@ struct Stage {
       }
       if (rc) return rc;
       mark(2);
+      auto norm_fuse = [&](const void* norm_w) {
+        FusedEpi f;
+        if (fuse_on && norm_w) {
+          f.kind = FUSE_RESIDUAL_NORM;
+          f.norm_w = static_cast<const __nv_bfloat16*>(norm_w);
+          f.eps = c.eps;
+          f.norm_out = a;
+          f.ld_norm = d;
+        }
+        return f;
+      };
+      FusedEpi of = norm_fuse(w.mlp_norm);
+      bool normed = false;
       if ((rc = gemm_launch(o, attn_dim, static_cast<const __nv_bfloat16*>(w.w_o), attn_dim, nullptr,
-                            hid, d, hid, d, T, d, attn_dim, EPI_RESIDUAL, gws, gws_bytes, nullptr, st)))
+                            hid, d, hid, d, T, d, attn_dim, EPI_RESIDUAL, gws, gws_bytes, nullptr, st,
+                            &of, &normed)))
         return rc;
       mark(3);
-      if ((rc = rmsnorm_launch(hid, d, nullptr, static_cast<const __nv_bfloat16*>(w.mlp_norm), c.eps, T,
+      if (!normed &&
+          (rc = rmsnorm_launch(hid, d, nullptr, static_cast<const __nv_bfloat16*>(w.mlp_norm), c.eps, T,
                                c.d, a, d, st)))
         return rc;
       mark(4);
@@ -186,8 +224,11 @@ struct Stage {
                             nullptr, 0, T, 2 * ffn, d, EPI_SWIGLU, gws, gws_bytes, nullptr, st)))
         return rc;
       mark(5);
+      // the next layer's input norm rides on this residual reduction (not across stages)
+      FusedEpi df = norm_fuse(l + 1 < c.num_layers ? layers[l + 1].attn_norm : nullptr);
       if ((rc = gemm_launch(m, ffn, static_cast<const __nv_bfloat16*>(w.w_down), ffn, nullptr, hid, d,
-                            hid, d, T, d, ffn, EPI_RESIDUAL, gws, gws_bytes, nullptr, st)))
+                            hid, d, T, d, ffn, EPI_RESIDUAL, gws, gws_bytes, nullptr, st, &df,
+                            &a_ready)))
         return rc;
       mark(6);
     }

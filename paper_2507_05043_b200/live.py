@@ -1,0 +1,241 @@
+"""Live two-stage pipeline over NVLink with real B200 compute.
+
+Twin of the reference's ``run_socket_demo`` (pipelink/demo.py:52-196): the head
+loop runs the unchanged ``choose_n`` + ``admit_and_batch`` on every step and
+reacts to token feedback as it arrives on the wall clock (no virtual clock), so
+the micro-batch composition is timing dependent exactly as in the reference
+demo; what must match the virtual run is the token
+accounting -- and here also the generated ids.  Differences from the socket
+demo: each stage is a real decoder stage on its own GPU (one process per GPU,
+``torch.distributed`` world of 2), the links are ``DeviceLinkSender`` /
+``DeviceLinkReceiver`` over NCCL, and the forward payload carries the
+micro-batch metadata ahead of the bf16 residual stream (the socket demo
+prefixes a 4-byte request count, demo.py:161-163).
+
+    result = run_device_demo(cfg, cluster, stage_profiles, trace, decoder=TINY)
+    result.tokens_by_request   # {rid: count}   (rank 0)
+    result.tokens              # {rid: ids}     (rank 0)
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import queue
+import time
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._pipelink import pipelink
+from .backend import GpuBackend, Placement
+from .wire import DeviceLinkReceiver, DeviceLinkSender
+
+BatchPhase = pipelink.engine.BatchPhase
+RequestState = pipelink.RequestState
+PayloadClass = pipelink.PayloadClass
+Phase = pipelink.Phase
+HDR = 8  # int32 words: T, R, phase, max_seqlen, max_ctx, slot, meta_len, reserved
+
+
+@dataclass
+class LiveResult:
+    tokens_by_request: dict
+    tokens: dict
+    wall_s: float
+    microbatches: int
+
+
+class _Requests:
+    """The `_requests` view GpuBackend.admit reads (driver stand-in)."""
+
+    def __init__(self, reqs):
+        self._requests = {r.id: r for r in reqs}
+
+
+def _comm_pair():
+    import torch.distributed as dist
+
+    comms = []
+    for src in (0, 1):  # forward link (0 -> 1), return link (1 -> 0)
+        obj = [None]
+        if dist.get_rank() == src:
+            buf = (C.c_uint8 * 128)()
+            N.call("pl_nccl_unique_id", buf, 128)
+            obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=src)
+        uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        N.call("pl_comm_init_rank", uid, 2, 0 if dist.get_rank() == src else 1, C.byref(h))
+        comms.append(h)
+    return comms
+
+
+def run_device_demo(cfg, cluster, stage_profiles, trace, *, decoder, seed: int = 0,
+                    timeout_s: float = 120.0) -> LiveResult | None:
+    import torch.distributed as dist
+
+    if len(cfg.partition.stages) != 2 or not dist.is_initialized() or dist.get_world_size() != 2:
+        raise pipelink.ConfigError("the live demo runs exactly two stages on a world of 2 ranks")
+    rank = dist.get_rank()
+    names = cfg.partition.node_names()
+    link_profiles = [cluster.link(names[0], names[1]), cluster.link(names[1], names[0])]
+    policy = (pipelink.LinkPolicy.DECODE_PRIORITY
+              if cfg.scheduling_policy.value == "decode_priority" else pipelink.LinkPolicy.FCFS)
+    bytes_per_token = cfg.model.hidden_dim * cfg.model.dtype_bytes
+    placement = Placement(2, 2, rank)
+    be = GpuBackend(decoder, cfg, placement, seed=seed)
+    requests = {r.id: r.fresh_copy() for r in trace.requests}
+    view = _Requests(requests.values())
+    be.start(view, trace)
+    exe = be.exe[rank]
+    dev = exe.device
+    comm_fwd, comm_ret = _comm_pair()
+    if rank == 1:
+        _tail(be, exe, comm_fwd, comm_ret, cfg, policy, timeout_s)
+        return None
+    return _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profiles,
+                 link_profiles, bytes_per_token, timeout_s, dev)
+
+
+def _tail(be, exe, comm_fwd, comm_ret, cfg, policy, timeout_s):
+    ret = DeviceLinkSender(comm_ret, 0, cfg.chunk_size, policy, "ret-sender", exe.device)
+    ret.start()
+    stream = exe.stream
+    d = exe.spec.d
+
+    def on_payload(p):
+        hdr = p.body[: HDR * 4].view(torch.int32).cpu().numpy()
+        T, R, phase, max_seqlen, max_ctx, slot, meta_len = (int(x) for x in hdr[:7])
+        meta_b = p.body[HDR * 4: HDR * 4 + meta_len * 4]
+        hid_b = p.body[HDR * 4 + meta_len * 4:]
+        with torch.cuda.stream(stream):
+            stream.wait_stream(torch.cuda.current_stream())
+            exe.meta_dev[:meta_len].view(torch.uint8).copy_(meta_b)
+            exe.hidden[slot][:T].view(torch.uint8).reshape(-1).copy_(hid_b)
+        exe.forward(slot, T, R, phase == 1, max_seqlen, max_ctx)
+        with torch.cuda.stream(stream):
+            ids = exe.out_ids[slot][:R].clone()  # the slot's out_ids are reused later
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        fb = pipelink.Payload(id=p.payload_id, phase_class=PayloadClass.DECODE,
+                              size_bytes=8 * R, micro_batch_id=p.payload_id, enqueue_time=0)
+        ret.send(fb, ids, ready=ev)
+
+    recv = DeviceLinkReceiver(comm_fwd, 0, on_payload, "tail-recv", exe.device)
+    recv.run()  # inline: this thread is the tail stage (demo.py:32-49)
+    ret.close()
+    ret.join(timeout=timeout_s)
+    if recv.failed:
+        raise pipelink.ProtocolError(f"tail receiver failed: {recv.error!r}")
+
+
+def _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profiles, link_profiles,
+          bytes_per_token, timeout_s, dev):
+    fwd = DeviceLinkSender(comm_fwd, 1, cfg.chunk_size, policy, "fwd-sender", dev)
+    feedback: queue.Queue = queue.Queue()
+    head_recv = DeviceLinkReceiver(comm_ret, 1, feedback.put, "head-recv", dev)
+    fwd.start()
+    head_recv.start()
+    pending = deque(requests[r.id] for r in trace.requests)
+    ready: deque = deque()
+    in_flight: dict = {}
+    payload_mb: dict = {}
+    next_mb = next_payload = 0
+    unfinished = len(requests)
+    n_mbs = 0
+    t0 = time.perf_counter()
+    scatter_stream = torch.cuda.Stream(dev)
+
+    def apply_feedback(p) -> int:
+        mb = payload_mb.pop(p.payload_id)
+        in_flight.pop(mb.id)
+        rec = be.mbs[mb.id]
+        ids = p.body.view(torch.int64)
+        be._scatter(rec, ids, scatter_stream)
+        done = 0
+        for rid in mb.request_ids:
+            r = requests[rid]
+            r.tokens_emitted += 1
+            if r.state is RequestState.PREFILL:
+                if r.output_len == 1:
+                    r.state = RequestState.FINISHED
+                    done += 1
+                else:
+                    r.state = RequestState.DECODING
+                    ready.append(r)
+            elif r.state is RequestState.DECODING:
+                if r.tokens_emitted >= r.output_len:
+                    r.state = RequestState.FINISHED
+                    done += 1
+                else:
+                    ready.append(r)
+        be.feedback(mb, 0)
+        return done
+
+    try:
+        while unfinished > 0:
+            dispatched = False
+            if ready or pending:
+                phase = Phase.DECODE if ready else Phase.PREFILL
+                demand = len(ready) + sum(m.batched_tokens for m in in_flight.values()) + \
+                    sum(r.input_len for r in pending)
+                decision = pipelink.choose_n(cfg.controller, stage_profiles, link_profiles, demand, phase,
+                                             bytes_per_token=bytes_per_token)
+                room = decision.n_microbatches - len(in_flight)
+                if room > 0:
+                    batches = pipelink.admit_and_batch(ready, pending, decision, cfg.controller.max_batch_size,
+                                                       room, now_s=0.0, allow_mixed=cfg.allow_mixed_phase,
+                                                       id_start=next_mb)
+                    next_mb += len(batches)
+                    for mb in batches:
+                        for rid in mb.request_ids:
+                            if requests[rid].state is RequestState.QUEUED:
+                                requests[rid].state = RequestState.PREFILL
+                        in_flight[mb.id] = mb
+                        be.admit(mb, 0)
+                        be.compute(0, mb, 0)
+                        rec = be.mbs[mb.id]
+                        body = _forward_body(exe, rec, dev)
+                        pclass = PayloadClass.DECODE if mb.phase is BatchPhase.DECODE else PayloadClass.PREFILL
+                        payload = pipelink.Payload(id=next_payload, phase_class=pclass,
+                                                   size_bytes=body.numel(), micro_batch_id=mb.id,
+                                                   enqueue_time=0)
+                        next_payload += 1
+                        payload_mb[payload.id] = mb
+                        fwd.send(payload, body)
+                        dispatched = True
+                        n_mbs += 1
+            if not dispatched:
+                if not in_flight:
+                    raise pipelink.ProtocolError("demo stalled with no work in flight")
+                unfinished -= apply_feedback(feedback.get(timeout=timeout_s))
+    finally:
+        fwd.close()
+        fwd.join(timeout=timeout_s)
+        head_recv.join(timeout=timeout_s)
+    torch.cuda.synchronize(dev)
+    gen = be.gen_tokens.cpu().numpy()
+    toks = {rid: gen[be.rid_index[rid], : r.tokens_emitted].copy() for rid, r in requests.items()}
+    return LiveResult(tokens_by_request={rid: requests[rid].tokens_emitted for rid in sorted(requests)},
+                      tokens=toks, wall_s=time.perf_counter() - t0, microbatches=n_mbs)
+
+
+def _forward_body(exe, rec, dev) -> torch.Tensor:
+    """[int32 header | int32 metadata | bf16 residual stream] of one micro-batch (device)."""
+    meta = rec.meta
+    hdr = np.array([rec.T, rec.R, 1 if rec.decode else 0, rec.max_seqlen, rec.max_ctx, rec.slot,
+                    meta.size, 0], dtype=np.int32)
+    prefix = np.concatenate([hdr, meta]).view(np.uint8)
+    hid_bytes = rec.T * exe.spec.d * 2
+    body = torch.empty(prefix.size + hid_bytes, dtype=torch.uint8, device=dev)
+    st = exe.stream
+    with torch.cuda.stream(st):
+        body[: prefix.size].copy_(torch.from_numpy(prefix), non_blocking=False)
+        body[prefix.size:].copy_(exe.hidden[rec.slot][: rec.T].view(torch.uint8).reshape(-1))
+    ev = torch.cuda.Event()
+    ev.record(st)
+    ev.synchronize()
+    return body

@@ -129,7 +129,7 @@ def attn_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     R = ctx_len.numel()
     out = out if out is not None else torch.empty(R, Hq * hd, dtype=BF16, device=q.device)
     ws_bytes = N.lib().pl_attn_decode_workspace_bytes(R, Hq, max_ctx, hd)
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
+    ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)  # split counters start at 0
     N.call("pl_attn_decode", _ptr(q), q.stride(0), _ptr(k_cache), _ptr(v_cache), k_cache.shape[0],
            block_size,
            _ptr(block_table), block_table.shape[1], _ptr(ctx_len), R, max_ctx, Hq, Hkv, hd,

@@ -19,14 +19,23 @@ import torch  # noqa: E402
 from paper_2507_05043_b200 import LLAMA3_8B, QWEN2_72B, ops  # noqa: E402
 
 
-def timeit(fn, iters=50, warm=5):
-    for _ in range(warm):
-        fn(0)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+def timeit(fn, iters=40, warm=3):
+    """Device time per call: the calls are captured into one CUDA graph and replayed,
+    so host (Python/ctypes) launch overhead is excluded."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for i in range(warm):
+            fn(i)
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(iters):
+            fn(i)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for i in range(iters):
-        fn(i)
+    g.replay()
     b.record()
     b.synchronize()
     return a.elapsed_time(b) / iters * 1e3  # us

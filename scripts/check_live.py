@@ -1,0 +1,60 @@
+"""Live 2-stage NVLink pipeline (run_device_demo) vs the virtual engine and the CPU oracle.
+
+    torchrun --nproc-per-node 2 scripts/check_live.py
+
+Criterion-11 analog (test_acceptance.py:367-381): per-request token counts of the
+live run equal the virtual run's; additionally the generated ids equal the CPU
+oracle's (margin-engineered init).  Exit code 0 = parity holds.
+"""
+
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dist.init_process_group(backend="cuda:nccl,cpu:gloo")
+    from paper_2507_05043_b200 import TINY, deploy
+    from paper_2507_05043_b200.live import run_device_demo
+    from paper_2507_05043_b200.spec import prompt_tokens
+    import pipelink as PL
+
+    spec = TINY.with_(peaked=True)
+    cluster = deploy.b200_cluster(2)
+    plan = deploy.plan(cluster, spec, 2)
+    cfg = deploy.engine_config(plan, spec, PL.ControllerConfig(max_batched_tokens=256, max_batch_size=8),
+                               chunk_size=4096)
+    trace = PL.Trace(requests=[PL.Request(i, 0.0, 40 + 7 * i, 6 + (i % 5)) for i in range(20)])
+    profiles = [PL.synth_profile(hi - lo, 1e-6, 2e-5, stage_id=i) for i, (_, (lo, hi)) in enumerate(plan.stages)]
+    res = run_device_demo(cfg, cluster, profiles, trace, decoder=spec)
+    ok = True
+    if dist.get_rank() == 0:
+        virtual = PL.PipelineEngine(cfg, cluster, profiles).run(trace)
+        counts_ok = res.tokens_by_request == virtual.tokens_by_request()
+        from oracle import decoder as OD
+
+        model = OD.OracleModel(OD.OracleSpec.from_spec(spec), seed=0, max_pos=256)
+        bad = 0
+        for r in trace.requests:
+            want, _ = model.greedy([torch.from_numpy(prompt_tokens(0, r.id, r.input_len, spec.vocab))],
+                                   r.output_len)
+            bad += not np.array_equal(res.tokens[r.id], want[0].numpy())
+        print(f"live 2-stage NVLink run: {res.microbatches} micro-batches in {res.wall_s:.2f} s; "
+              f"token counts {'==' if counts_ok else '!='} virtual; "
+              f"{len(trace.requests) - bad}/{len(trace.requests)} requests identical to the oracle", flush=True)
+        ok = counts_ok and bad == 0
+    t = torch.tensor([0 if ok else 1])
+    dist.all_reduce(t)
+    dist.destroy_process_group()
+    sys.exit(int(t.item() != 0))
+
+
+if __name__ == "__main__":
+    main()
