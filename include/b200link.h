@@ -49,6 +49,12 @@ typedef enum pl_status {
   PL_ERR_CUDA = 3,     /* CUDA runtime / launch failure      -> PipelinkError */
 } pl_status;
 
+/* Load every kernel of the library into the current device's context now.
+ * CUDA loads modules lazily at first launch by default, and a load can wait on
+ * a running kernel -- an NCCL receive spinning for its peer would deadlock it.
+ * pl_stage_create calls this; call it before any NCCL traffic otherwise. */
+PL_API int32_t pl_preload_kernels(void);
+
 /* GEMM epilogues (see pl_gemm). */
 typedef enum pl_epilogue {
   PL_EPI_NONE = 0,     /* C = bf16(acc)                                      */
@@ -204,6 +210,111 @@ PL_API int32_t pl_gate_until_ns(const uint64_t* t0, uint64_t offset_ns, void* st
 
 /* Host<->device plumbing without a Python round trip. */
 PL_API int32_t pl_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* ------------------------------------------------------------ scheduler --- */
+
+/* Native virtual-clock scheduler: PipelineEngine.run (engine.py:509-600) with
+ * choose_n / _round_terms (controller.py:68-186), admit_and_batch
+ * (engine.py:155-238), LinkQueue (transport.py:70-160), compute_time
+ * (profiles.py:95-121) and transmission_ns / s_to_ns (transport.py:32-33,
+ * 199-200) restated bit-exactly.  Host-only; no GPU needed unless a pipeline
+ * is attached.  Profiles: per (stage, phase) the sorted points
+ * prof_x[prof_off[2s+ph] : prof_off[2s+ph+1]] (tokens) / prof_y (seconds),
+ * phase 0 = prefill, 1 = decode; links: S forward hops then the return hop. */
+typedef struct pl_sched_config {
+  int32_t n_stages, n_links;
+  int64_t max_batched_tokens;
+  int32_t max_batch_size, n_max; /* n_max: effective (ControllerConfig.effective_n_max) */
+  double bubble_epsilon, gain_delta;
+  int32_t fixed_compute;         /* BudgetMode.FIXED_COMPUTE */
+  int32_t decision_stride;
+  int64_t chunk_size;            /* < 0: unchunked (chunk_size None / inf) */
+  int32_t fcfs;                  /* SchedulingPolicy.FCFS */
+  int32_t allow_mixed;
+  int64_t bytes_per_token;       /* hidden_dim * dtype_bytes */
+  int64_t feedback_bytes;        /* TOKEN_FEEDBACK_BYTES (placement.py:16) */
+  const int64_t* prof_off;       /* [2 * n_stages + 1] */
+  const int64_t* prof_x;
+  const double* prof_y;
+  const double* link_latency_s;  /* [n_links] */
+  const double* link_bandwidth;  /* [n_links] bytes/s */
+} pl_sched_config;
+
+typedef struct pl_sched_request {
+  int64_t id, arrival_ns, input_len, output_len; /* arrival_ns = s_to_ns(arrival_time) */
+} pl_sched_request;
+
+PL_API int32_t pl_sched_create(const pl_sched_config* cfg, void** handle);
+PL_API int32_t pl_sched_destroy(void* handle);
+PL_API int32_t pl_sched_choose_n(void* handle, int64_t queued_tokens, int32_t phase, int32_t* n,
+                                 int64_t* budget, double* bubble);
+/* Run the trace (trace order) to completion or horizon_ns (< 0: none).  With a
+ * pipeline (pl_pipeline_create) every decision also issues its GPU work, and
+ * the call returns once the device finished; NULL gives a pure virtual run. */
+PL_API int32_t pl_sched_run(void* handle, const pl_sched_request* reqs, int64_t n_reqs,
+                            int64_t horizon_ns, void* pipeline);
+/* counts[8] = {events, link events, decisions, token emissions, first-compute
+ * entries, busy intervals, end_ns, all_finished}. */
+PL_API int32_t pl_sched_counts(void* handle, int64_t* counts_host);
+/* Logs of the last run (host arrays sized by pl_sched_counts; NULL skips):
+ *   events[4n]    time_ns, EventKind, subject, stage
+ *   links[7n]     time_ns, link, payload, chunk index, bytes, class (0 prefill,
+ *                 1 decode), event (0 enqueue, 1 emit, 2 sent, 3 deliver)
+ *   decisions[3n] iteration, n, token budget; bubbles[n]
+ *   emissions[2n] time_ns, request id;  first_compute[2n] request id, time_ns
+ *   busy[3n]      stage, start_ns, end_ns
+ *   req_state[2r] RequestState (0 queued, 1 prefill, 2 decoding, 3 finished),
+ *                 tokens emitted; req_times[2r] first token / finish seconds
+ *                 (NaN: none), in trace order. */
+PL_API int32_t pl_sched_read(void* handle, int64_t* events, int64_t* links, int64_t* decisions,
+                             double* bubbles, int64_t* emissions, int64_t* first_compute,
+                             int64_t* busy, int64_t* req_state, double* req_times);
+
+/* ------------------------------------------------------------ runtime ----- */
+
+/* The GPU side of a pipeline run on this process (twin of backend.py's
+ * GpuBackend): per stage s a pl_stage handle or NULL when the stage lives on
+ * another rank, its compute stream and buffers; per link the NCCL
+ * communicator when the hop crosses processes (this process is comm-rank 0 on
+ * its outgoing hops, 1 on incoming). */
+typedef struct pl_pipeline_config {
+  int32_t n_stages, n_slots, max_blocks, block_size;
+  int64_t num_blocks;
+  int32_t max_tokens, max_reqs, d;
+  int32_t throttle;      /* gate deliveries at the virtual link timing */
+  int32_t record_links;  /* per-chunk device timestamps */
+  void* const* stage;    /* [n_stages] */
+  void* const* stream;   /* [n_stages] compute streams */
+  const int32_t* device; /* [n_stages] CUDA ordinals */
+  void* const* meta_dev; /* [n_stages] int32 metadata buffers */
+  void* const* ids_dev;  /* [n_stages] int64 prompt-id buffer (head) */
+  void* const* hidden;   /* [n_stages * n_slots] bf16 residual-stream payloads */
+  void* const* out_ids;  /* [n_stages * n_slots] int64 tokens (last stage) */
+  void* const* comm;     /* [n_stages] NCCL communicators or NULL */
+  int64_t* const* ids_recv; /* head: [n_slots] return-hop landing buffers */
+} pl_pipeline_config;
+
+PL_API int32_t pl_pipeline_create(const pl_pipeline_config* cfg, void** handle);
+PL_API int32_t pl_pipeline_destroy(void* handle);
+/* The trace of the next run: prompt ids of request i (trace order) are the
+ * host array prompt_ids[prompt_off[i] : prompt_off[i+1]] (copied); head
+ * outputs last_token [n_requests] and gen_tokens [n_requests, gen_stride]. */
+PL_API int32_t pl_pipeline_set_requests(void* handle, int64_t n_requests, const int64_t* prompt_off_host,
+                                        const int64_t* prompt_ids_host, int64_t* last_token,
+                                        int64_t* gen_tokens, int32_t gen_stride);
+/* counts[5] = {stage forwards, token scatters, chunk records, micro-batches,
+ * request ids of those micro-batches}. */
+PL_API int32_t pl_pipeline_counts(void* handle, int64_t* counts_host);
+/* Device-clock results of the last run (seconds since the run's start event on
+ * the stage's device; NULL skips):  busy[2n] stage, micro-batch / busy_s[2n]
+ * start, end;  fb_mb[n] / fb_s[n] token scatters on the head;  chunks[6n] link,
+ * src stage, payload, index, bytes, class / chunk_s[3n] enqueue, emit, sent;
+ * mb_log[4n] micro-batch, decode, R, work (context sum or tokens) with
+ * request ids mb_req_ids[mb_req_off[i] : mb_req_off[i+1]]. */
+PL_API int32_t pl_pipeline_read(void* handle, double* run_time_s, double* decode_start_s,
+                                int64_t* busy, double* busy_s, int64_t* fb_mb, double* fb_s,
+                                int64_t* chunks, double* chunk_s, int64_t* mb_log,
+                                int64_t* mb_req_off, int64_t* mb_req_ids);
 
 #ifdef __cplusplus
 }

@@ -50,8 +50,31 @@ class MicroBatch(C.Structure):
     ]
 
 
+f64 = C.c_double
+
+
+class SchedConfig(C.Structure):
+    _fields_ = [
+        ("n_stages", i32), ("n_links", i32), ("max_batched_tokens", i64), ("max_batch_size", i32),
+        ("n_max", i32), ("bubble_epsilon", f64), ("gain_delta", f64), ("fixed_compute", i32),
+        ("decision_stride", i32), ("chunk_size", i64), ("fcfs", i32), ("allow_mixed", i32),
+        ("bytes_per_token", i64), ("feedback_bytes", i64), ("prof_off", vp), ("prof_x", vp),
+        ("prof_y", vp), ("link_latency_s", vp), ("link_bandwidth", vp),
+    ]
+
+
+class PipelineConfig(C.Structure):
+    _fields_ = [
+        ("n_stages", i32), ("n_slots", i32), ("max_blocks", i32), ("block_size", i32),
+        ("num_blocks", i64), ("max_tokens", i32), ("max_reqs", i32), ("d", i32), ("throttle", i32),
+        ("record_links", i32), ("stage", vp), ("stream", vp), ("device", vp), ("meta_dev", vp),
+        ("ids_dev", vp), ("hidden", vp), ("out_ids", vp), ("comm", vp), ("ids_recv", vp),
+    ]
+
+
 _SIGS = {
     "pl_abi_version": (i32, []),
+    "pl_preload_kernels": (i32, []),
     "pl_last_error": (C.c_char_p, []),
     "pl_device_sm_count": (i32, [i32]),
     "pl_launch_count": (i64, []),
@@ -82,6 +105,17 @@ _SIGS = {
     "pl_record_globaltimer": (i32, [vp, vp]),
     "pl_gate_until_ns": (i32, [vp, u64, vp]),
     "pl_memcpy_async": (i32, [vp, vp, i64, vp]),
+    "pl_sched_create": (i32, [C.POINTER(SchedConfig), C.POINTER(vp)]),
+    "pl_sched_destroy": (i32, [vp]),
+    "pl_sched_choose_n": (i32, [vp, i64, i32, C.POINTER(i32), C.POINTER(i64), C.POINTER(f64)]),
+    "pl_sched_run": (i32, [vp, vp, i64, i64, vp]),
+    "pl_sched_counts": (i32, [vp, vp]),
+    "pl_sched_read": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "pl_pipeline_create": (i32, [C.POINTER(PipelineConfig), C.POINTER(vp)]),
+    "pl_pipeline_destroy": (i32, [vp]),
+    "pl_pipeline_set_requests": (i32, [vp, i64, vp, vp, vp, vp, i32]),
+    "pl_pipeline_counts": (i32, [vp, vp]),
+    "pl_pipeline_read": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

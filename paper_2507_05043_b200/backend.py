@@ -24,6 +24,7 @@ when both stages live on the same process.
 
 from __future__ import annotations
 
+import ctypes as C
 import os
 from collections import deque
 from dataclasses import dataclass
@@ -116,6 +117,7 @@ class GpuBackend(Backend):
         self.user_prompts = prompts
         self.comms = comms or {}
         self.throttle = throttle
+        self.record_links = False   # per-chunk CUDA events -> realized link log (device clock)
         self.S = placement.n_stages
         self.layer_ranges = [rng for _, rng in cfg.partition.stages]
         self.n_slots = cfg.controller.effective_n_max(self.S)
@@ -182,6 +184,7 @@ class GpuBackend(Backend):
         self._streams_built = True
 
     def close(self) -> None:
+        self._native_close()
         for exe in self.exe.values():
             exe.close()
         self.exe = {}
@@ -206,6 +209,7 @@ class GpuBackend(Backend):
         self.mb_log: list = []      # (phase, R, sum of contexts) per admitted micro-batch
         self.first_decode_ev = None
         self.busy_events: list = []  # (stage, mb id, start event, end event) on the device clock
+        self.chunk_events: list = []  # realized link log (record_links)
         self.mb_requests: dict = {}  # mb id -> request ids
         self.prompts = {}
         for r in reqs:
@@ -310,7 +314,7 @@ class GpuBackend(Backend):
                     last_token=self.last_token if (s == 0) else None)
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(st)
-        self.busy_events.append((s, mb.id, t_start, ev))
+        self.busy_events.append((s, mb.id, t_start, ev))  # ev also marks the payload's enqueue
         self.ev_comp[s][k] = ev
         q.append(ev)
         if self.S == 1:
@@ -335,11 +339,17 @@ class GpuBackend(Backend):
         if dst_local:
             dbuf = (self.ids_recv[k] if is_ret else self.exe[dst].hidden[k]).data_ptr() + offset
             prev_send = self.ev_send[dst][k]
+        if src_local and self.record_links:
+            t_emit = torch.cuda.Event(enable_timing=True)
         if src_local and dst_local:
             # same process: device (or peer) copy on the source's send stream
             if first and prev_send is not None:
                 sst.wait_event(prev_send)
+            if self.record_links:
+                t_emit.record(sst)
             N.check(N.lib().pl_memcpy_async(dbuf, sbuf, size, sst.cuda_stream), "pl_memcpy_async")
+            if self.record_links:
+                self._note_chunk(link, src, k, payload, chunk, t_emit, sst)
             if last:
                 ev = torch.cuda.Event()
                 ev.record(sst)
@@ -348,7 +358,11 @@ class GpuBackend(Backend):
             return
         if src_local:
             comm = self.comms[link]
+            if self.record_links:
+                t_emit.record(sst)
             N.check(N.lib().pl_p2p_send(comm, sbuf, size, 1, sst.cuda_stream), "pl_p2p_send")
+            if self.record_links:
+                self._note_chunk(link, src, k, payload, chunk, t_emit, sst)
             if last:
                 ev = torch.cuda.Event()
                 ev.record(sst)
@@ -363,6 +377,12 @@ class GpuBackend(Backend):
                 ev = torch.cuda.Event()
                 ev.record(rst)
                 self._recv_done(dst, rec, ev, is_ret, self._deliver_ns(link, size, now_ns))
+
+    def _note_chunk(self, link, src, slot, payload, chunk, t_emit, stream) -> None:
+        t_sent = torch.cuda.Event(enable_timing=True)
+        t_sent.record(stream)
+        self.chunk_events.append((link, src, payload.id, chunk.index, chunk.size_bytes,
+                                  chunk.phase_class, self.ev_comp[src][slot], t_emit, t_sent))
 
     def _deliver_ns(self, link: int, size: int, emit_ns: int) -> int:
         """Virtual delivery time of a chunk emitted at emit_ns (engine.py:355, 552-557)."""
@@ -442,6 +462,21 @@ class GpuBackend(Backend):
                            for r in result.requests}
             t0 = self.t0[0]
             self.fb_times_s = [t0.elapsed_time(ev) / 1e3 for ev, _ in self.fb_events]
+        # realized link log on the source device's clock: enqueue = producing forward done,
+        # emit/sent = the chunk's copy or ncclSend start/end on the link stream
+        self.realized_links = []
+        LinkEvent = pipelink.transport.LinkEvent
+        seen = set()
+        for link, src, pid, idx, size, pclass, ev_enq, ev_a, ev_b in self.chunk_events:
+            t0s = self.t0[src]
+            name = self.driver.link_profiles[link].name
+            if (link, pid) not in seen:
+                seen.add((link, pid))
+                self.realized_links.append(LinkEvent(round(t0s.elapsed_time(ev_enq) * 1e6), name, pid, -1,
+                                                     0, pclass, "enqueue"))
+            ta, tb = round(t0s.elapsed_time(ev_a) * 1e6), round(t0s.elapsed_time(ev_b) * 1e6)
+            self.realized_links.append(LinkEvent(ta, name, pid, idx, size, pclass, "emit"))
+            self.realized_links.append(LinkEvent(tb, name, pid, idx, size, pclass, "sent"))
         # real per-stage busy intervals (ns on each device's clock, origin = run start)
         self.busy_real_ns = {}
         for s, mb_id, a, b in self.busy_events:
@@ -450,6 +485,144 @@ class GpuBackend(Backend):
                 (mb_id, round(t0s.elapsed_time(a) * 1e6), round(t0s.elapsed_time(b) * 1e6)))
             self.decode_start_s = (t0.elapsed_time(self.first_decode_ev) / 1e3
                                    if self.first_decode_ev is not None else None)
+
+    # ------------------------------------------------------- native runtime
+    def native_start(self, trace, record_links: bool = False):
+        """Buffers + the native runtime (csrc/runtime.cu) for `trace`; returns the
+        pl_pipeline handle that NativeScheduler.run drives.  The C++ twin of
+        start/admit/compute/emit/feedback above: identical stream/event protocol,
+        no Python on the per-micro-batch path."""
+        self.prepare(trace)
+        reqs = trace.requests
+        self._n_requests = len(reqs)
+        self._max_out = max(r.output_len for r in reqs)
+        self.rid_index = {r.id: i for i, r in enumerate(reqs)}
+        head = self.exe.get(0)
+        if head is not None:
+            with torch.cuda.device(head.device):
+                self.last_token = torch.zeros(self._n_requests, dtype=torch.int64, device=head.device)
+                self.gen_tokens = torch.zeros(self._n_requests, self._max_out, dtype=torch.int64,
+                                              device=head.device)
+        off = np.zeros(len(reqs) + 1, dtype=np.int64)
+        parts = []
+        for i, r in enumerate(reqs):
+            if self.user_prompts is not None and r.id in self.user_prompts:
+                p = np.asarray(self.user_prompts[r.id], dtype=np.int64)
+                if p.shape != (r.input_len,):
+                    raise pipelink.ConfigError(f"prompt of request {r.id} has wrong length")
+            else:
+                p = prompt_tokens(self.seed, r.id, r.input_len, self.spec.vocab)
+            parts.append(p)
+            off[i + 1] = off[i] + r.input_len
+        ids = np.ascontiguousarray(np.concatenate(parts)) if parts else np.zeros(1, dtype=np.int64)
+        h = self._native_handle(record_links)
+        lt = self.last_token.data_ptr() if head is not None else None
+        gen = self.gen_tokens.data_ptr() if head is not None else None
+        stride = self.gen_tokens.stride(0) if head is not None else 1
+        N.check(N.lib().pl_pipeline_set_requests(h, len(reqs), off.ctypes.data, ids.ctypes.data, lt, gen,
+                                                 stride), "pl_pipeline_set_requests")
+        self._native_record = record_links
+        return h
+
+    def _native_handle(self, record_links: bool):
+        key = (self._built_for, bool(record_links), bool(self.throttle))
+        if getattr(self, "_native", None) is not None and self._native[0] == key:
+            return self._native[1]
+        self._native_close()
+        S, K = self.S, self.n_slots
+        arr = lambda n: (C.c_void_p * max(1, n))()  # noqa: E731
+        stage, stream, meta, ids, hidden, out_ids, comm = (arr(S), arr(S), arr(S), arr(S), arr(S * K),
+                                                           arr(S * K), arr(S))
+        dev = (C.c_int32 * S)()
+        keep = []
+        for s, exe in self.exe.items():
+            stage[s] = exe.handle.value
+            stream[s] = exe.stream.cuda_stream
+            dev[s] = exe.device.index if exe.device.index is not None else 0
+            meta[s] = exe.meta_dev.data_ptr()
+            ids[s] = exe.ids_dev.data_ptr() if exe.ids_dev is not None else None
+            for k in range(K):
+                hidden[s * K + k] = exe.hidden[k].data_ptr()
+                if exe.is_last:
+                    out_ids[s * K + k] = exe.out_ids[k].data_ptr()
+        for link, h in self.comms.items():
+            comm[link] = h.value if isinstance(h, C.c_void_p) else h
+        ids_recv = arr(K)
+        head = self.exe.get(0)
+        if head is not None:
+            with torch.cuda.device(head.device):
+                self._native_ids_recv = [torch.zeros(self.max_reqs, dtype=torch.int64, device=head.device)
+                                         for _ in range(K)]
+            for k, t in enumerate(self._native_ids_recv):
+                ids_recv[k] = t.data_ptr()
+        c = N.PipelineConfig()
+        c.n_stages, c.n_slots, c.max_blocks, c.block_size = S, K, self.max_blocks, BLOCK_SIZE
+        c.num_blocks, c.max_tokens, c.max_reqs, c.d = self.num_blocks, self.max_tokens, self.max_reqs, self.spec.d
+        c.throttle, c.record_links = int(self.throttle), int(record_links)
+        c.stage, c.stream, c.device = C.cast(stage, C.c_void_p), C.cast(stream, C.c_void_p), C.cast(dev, C.c_void_p)
+        c.meta_dev, c.ids_dev = C.cast(meta, C.c_void_p), C.cast(ids, C.c_void_p)
+        c.hidden, c.out_ids = C.cast(hidden, C.c_void_p), C.cast(out_ids, C.c_void_p)
+        c.comm, c.ids_recv = C.cast(comm, C.c_void_p), C.cast(ids_recv, C.c_void_p)
+        keep += [stage, stream, dev, meta, ids, hidden, out_ids, comm, ids_recv]
+        h = C.c_void_p()
+        N.check(N.lib().pl_pipeline_create(C.byref(c), C.byref(h)), "pl_pipeline_create")
+        self._native = (key, h, keep)
+        return h
+
+    def _native_close(self) -> None:
+        nat = getattr(self, "_native", None)
+        if nat is not None:
+            N.lib().pl_pipeline_destroy(nat[1])
+            self._native = None
+
+    def native_finish(self, result) -> None:
+        """Device-clock results of the native run, in the attributes finish() sets."""
+        lib = N.lib()
+        h = self._native[1]
+        cnt = np.zeros(5, dtype=np.int64)
+        N.check(lib.pl_pipeline_counts(h, cnt.ctypes.data), "pl_pipeline_counts")
+        nb, nf, nc, nm, nr = (int(x) for x in cnt)
+        busy = np.zeros((nb, 2), dtype=np.int64)
+        busy_s = np.zeros((nb, 2), dtype=np.float64)
+        fb_mb = np.zeros(nf, dtype=np.int64)
+        fb_s = np.zeros(nf, dtype=np.float64)
+        ch = np.zeros((nc, 6), dtype=np.int64)
+        ch_s = np.zeros((nc, 3), dtype=np.float64)
+        mbl = np.zeros((nm, 4), dtype=np.int64)
+        mb_off = np.zeros(nm + 1, dtype=np.int64)
+        mb_ids = np.zeros(max(nr, 1), dtype=np.int64)
+        rt, ds = C.c_double(), C.c_double()
+        p = lambda a: a.ctypes.data if a.size else None  # noqa: E731
+        N.check(lib.pl_pipeline_read(h, C.byref(rt), C.byref(ds), p(busy), p(busy_s), p(fb_mb), p(fb_s), p(ch),
+                                     p(ch_s), p(mbl), p(mb_off), p(mb_ids)), "pl_pipeline_read")
+        self.run_time_s = rt.value
+        self.decode_start_s = None if np.isnan(ds.value) else ds.value
+        self.mb_requests = {int(m): tuple(mb_ids[mb_off[i]:mb_off[i + 1]].tolist())
+                            for i, m in enumerate(mbl[:, 0].tolist())}
+        self.mb_log = [("decode" if d else "prefill", int(R), int(w)) for _, d, R, w in mbl.tolist()]
+        self.busy_real_ns = {}
+        for (s, mb), (a, b) in zip(busy.tolist(), busy_s.tolist()):
+            self.busy_real_ns.setdefault(s, []).append((mb, round(a * 1e9), round(b * 1e9)))
+        self.fb_times_s = fb_s.tolist()
+        self.fb_events = [(None, self.mb_requests.get(m, ())) for m in fb_mb.tolist()]
+        self.tokens = None
+        if 0 in self.exe:
+            gen = self.gen_tokens.cpu().numpy()
+            self.tokens = {r.id: gen[self.rid_index[r.id], : r.tokens_emitted].copy() for r in result.requests}
+        self.realized_links = []
+        if self._native_record:
+            LinkEvent = pipelink.transport.LinkEvent
+            classes = (pipelink.PayloadClass.PREFILL, pipelink.PayloadClass.DECODE)
+            names = [lp.name for lp in self.driver.link_profiles]
+            seen = set()
+            for (link, _src, pid, idx, size, cls), (te, ta, tb) in zip(ch.tolist(), ch_s.tolist()):
+                pclass = classes[cls]
+                if (link, pid) not in seen:
+                    seen.add((link, pid))
+                    self.realized_links.append(LinkEvent(round(te * 1e9), names[link], pid, -1, 0, pclass,
+                                                         "enqueue"))
+                self.realized_links.append(LinkEvent(round(ta * 1e9), names[link], pid, idx, size, pclass, "emit"))
+                self.realized_links.append(LinkEvent(round(tb * 1e9), names[link], pid, idx, size, pclass, "sent"))
 
     # ---------------------------------------------------------- throttle
     def _start_gates(self) -> None:

@@ -49,7 +49,7 @@ def _flags() -> list[str]:
         "-lineinfo",
         "-std=c++17",
         "-Xcompiler",
-        "-fPIC,-fvisibility=hidden",
+        "-fPIC,-fvisibility=hidden,-ffp-contract=off",
         "--expt-relaxed-constexpr",
         f"-I{ROOT / 'include'}",
         f"-I{inc}",

@@ -57,6 +57,14 @@ int32_t pl_abi_version(void) { return PL_ABI_VERSION; }
 
 const char* pl_last_error(void) { return g_err; }
 
+int32_t pl_preload_kernels(void) {
+  int rc = gemm_preload();
+  if (!rc) rc = attention_preload();
+  if (!rc) rc = kernels_preload();
+  if (!rc) rc = transport_preload();
+  return rc;
+}
+
 int64_t pl_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int32_t pl_device_sm_count(int32_t device) {

@@ -11,10 +11,10 @@
 // decode: one query token per request over its paged KV cache
 //   [num_blocks, Hkv, 64, hd].  One CTA per (kv head, request, KV split) serves
 //   the whole GQA group, so each KV page is read from HBM exactly once.  Pages
-//   arrive by TMA into 128-byte-swizzled shared memory; QK^T and PV run on
-//   m16n8k16 tensor cores; a request's context is cut into ceil(pages/8)
-//   even splits, so the reduction order depends on its own context length
-//   only, never on the batch.
+//   arrive by TMA into 128-byte-swizzled shared memory (persistent CTAs, one TMA
+//   producer warp, four tensor-core consumer warps); a request's context is cut
+//   into ceil(pages/8) even splits, so the reduction order depends on its own
+//   context length only, never on the batch.
 #include "common.cuh"
 #include "pl_internal.h"
 
@@ -249,24 +249,34 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
 
 // ======================================================= decode (paged)
 //
-// One CTA per (kv head, request, split of <= 8 pages).  A single thread streams
-// each 64-token K and V page into shared memory with four 2-D TMA boxes
-// (64 dims x 64 tokens, 128-byte swizzle) completing on an mbarrier; the four
-// warps then each take 16 tokens of the page: S = Q K^T and O += P V on
-// m16n8k16 tensor cores with Q = the GQA group padded to 16 rows.  Every warp
-// keeps its own online-softmax state; warps are merged in shared memory and
-// splits by attn_decode_combine_kernel, both in a fixed order.
+// Persistent, warp-specialized paged decode attention (one CTA per SM).  A work
+// item is (request, kv head, split of <= 8 pages); the CTA walks its items in a
+// static round robin.  Warp 0 (one lane) is a TMA producer streaming each 64-token
+// K and V page -- four 2-D boxes of 64 dims x 64 tokens, 128-byte swizzle -- through
+// a 4-deep shared-memory ring continuously across items; warps 1-4 each own 16
+// tokens of every page: S = Q K^T and O += P V on m16n8k16 tensor cores with Q =
+// the GQA group padded to 16 rows (fragments loaded straight from global), per-warp
+// online softmax, warps merged in shared memory.  A request's context is cut into
+// ceil(pages / 8) even splits (its own length only -- batch invariant); the last
+// split CTA to finish merges the splits in split order.  PDL: pages that were
+// complete before this step are streamed before griddepcontrol.wait; only the page
+// holding the newest token waits for the predecessor kernel.
 
 constexpr int PAGE = 64;                 // tokens per KV block
 constexpr int MAX_PAGES_PER_SPLIT = 8;   // <= 512 tokens per split, pages spread evenly
-constexpr int DEC_STAGES = 3;
+constexpr int DEC_STAGES = 4;
 constexpr int HALF_TILE = 64 * 128;      // 64 tokens x 64 dims bf16 (one TMA box)
 constexpr int PAGE_BYTES = 4 * HALF_TILE;  // K lo | K hi | V lo | V hi
+constexpr int DEC_THREADS = 160;         // producer warp + 4 consumer warps
 
+template <int G>
 struct DecodeSmem {
-  static constexpr int Q_OFF = DEC_STAGES * PAGE_BYTES;        // 16 x 128 bf16, 256 B rows
-  static constexpr int BAR_OFF = Q_OFF + 16 * 256;
-  static constexpr int TOTAL = BAR_OFF + 64 + 1024;            // + alignment slack
+  static constexpr int RED_O = DEC_STAGES * PAGE_BYTES;     // [4 warps][G][128] fp32
+  static constexpr int RED_M = RED_O + 4 * G * HD * 4;      // [4][G]
+  static constexpr int RED_L = RED_M + 4 * G * 4;           // [4][G]
+  static constexpr int BAR = RED_L + 4 * G * 4;             // full[S], empty[S]
+  static constexpr int FLAG = BAR + 16 * DEC_STAGES;
+  static constexpr int TOTAL = FLAG + 16 + 1024;            // + alignment slack
 };
 
 // address of 16-byte chunk `c` (0..15) of token row `row` in a (lo|hi) 128B-swizzled pair
@@ -274,220 +284,281 @@ PL_DEV uint32_t kv_addr(uint32_t base, int row, int c) {
   return base + (c >> 3) * HALF_TILE + row * 128 + (((c & 7) ^ (row & 7)) << 4);
 }
 
+struct DecodeArgs {
+  const __nv_bfloat16* q;
+  int64_t ldq;
+  const int32_t* block_table;
+  int max_blocks;
+  const int32_t* ctx_len;
+  int R, Hkv, nsplit;
+  float scale_log2;
+  __nv_bfloat16* out;
+  int64_t ldo;
+  float* ws_o;
+  float2* ws_ml;
+  int* counters;
+};
+
+// pages [p0, p0 + np) of item `it`, and the request's page count
+PL_DEV void decode_item(const DecodeArgs& a, int it, int& r, int& kh, int& split, int& p0, int& np,
+                        int& n_pages, int& ctx) {
+  split = it % a.nsplit;
+  kh = (it / a.nsplit) % a.Hkv;
+  r = it / (a.nsplit * a.Hkv);
+  ctx = a.ctx_len[r];
+  n_pages = (ctx + PAGE - 1) / PAGE;
+  const int ns_r = max(1, (n_pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
+  const int pps = (n_pages + ns_r - 1) / ns_r;
+  p0 = split * pps;
+  np = max(0, min(n_pages, p0 + pps) - p0);
+}
+
 template <int G>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(DEC_THREADS, 1)
     attn_decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                       const __nv_bfloat16* __restrict__ q, int64_t ldq,
-                       const int32_t* __restrict__ block_table, int max_blocks,
-                       const int32_t* __restrict__ ctx_len, int Hkv, float scale_log2,
-                       __nv_bfloat16* __restrict__ out, int64_t ldo, float* __restrict__ ws_o,
-                       float2* __restrict__ ws_ml, int* __restrict__ counters) {
+                       const DecodeArgs args) {
+  using L = DecodeSmem<G>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sQ = smem + DecodeSmem::Q_OFF;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DecodeSmem::BAR_OFF);
-
-  const int kh = blockIdx.x, r = blockIdx.y, split = blockIdx.z, nsplit = gridDim.z;
-  const int Hq = Hkv * G;
-  const int ctx = ctx_len[r];
-  // split layout depends on this request's context only (batch invariance)
-  const int n_pages = (ctx + PAGE - 1) / PAGE;
-  const int ns_r = max(1, (n_pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
-  const int pps = (n_pages + ns_r - 1) / ns_r;
-  const int p0 = split * pps;
-  const int np = max(0, min(n_pages, p0 + pps) - p0);
+  float* red_o = reinterpret_cast<float*>(smem + L::RED_O);
+  float* red_m = reinterpret_cast<float*>(smem + L::RED_M);
+  float* red_l = reinterpret_cast<float*>(smem + L::RED_L);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* empty = full + DEC_STAGES;
+  int* last_flag = reinterpret_cast<int*>(smem + L::FLAG);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t* bt = block_table + static_cast<int64_t>(r) * max_blocks;
+  const int n_items = args.R * args.Hkv * args.nsplit;
 
-  auto issue = [&](int i) {
-    const int st = i % DEC_STAGES;
-    const int row0 = (bt[p0 + i] * Hkv + kh) * PAGE;
-    uint8_t* dst = smem + st * PAGE_BYTES;
-    mbar_arrive_expect_tx(&full[st], PAGE_BYTES);
-    const uint64_t pol = policy_evict_first();
-    tma_load_2d(dst, &tmK, &full[st], 0, row0, pol);
-    tma_load_2d(dst + HALF_TILE, &tmK, &full[st], 64, row0, pol);
-    tma_load_2d(dst + 2 * HALF_TILE, &tmV, &full[st], 0, row0, pol);
-    tma_load_2d(dst + 3 * HALF_TILE, &tmV, &full[st], 64, row0, pol);
-  };
   if (threadIdx.x == 0) {
-    for (int s = 0; s < DEC_STAGES; ++s) mbar_init(&full[s], 1);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int s = 0; s < DEC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
     fence_mbar_init();
   }
   __syncthreads();
   pdl_trigger();
-  pdl_wait();
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    for (int i = 0; i < min(np, DEC_STAGES); ++i) issue(i);
+
+  if (warp == 0) {
+    // ------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      bool waited = false;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        int r, kh, split, p0, np, n_pages, ctx;
+        decode_item(args, it, r, kh, split, p0, np, n_pages, ctx);
+        const int32_t* bt = args.block_table + static_cast<int64_t>(r) * args.max_blocks;
+        for (int i = 0; i < np; ++i) {
+          // the newest token's page was written by the predecessor kernel
+          if (!waited && p0 + i == n_pages - 1) {
+            pdl_wait();
+            waited = true;
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          const int row0 = (bt[p0 + i] * args.Hkv + kh) * PAGE;
+          uint8_t* dst = smem + stage * PAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], PAGE_BYTES);
+          tma_load_2d(dst, &tmK, &full[stage], 0, row0, pol);
+          tma_load_2d(dst + HALF_TILE, &tmK, &full[stage], 64, row0, pol);
+          tma_load_2d(dst + 2 * HALF_TILE, &tmV, &full[stage], 0, row0, pol);
+          tma_load_2d(dst + 3 * HALF_TILE, &tmV, &full[stage], 64, row0, pol);
+          if (++stage == DEC_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (!waited) pdl_wait();
+    }
+    return;
   }
-  // Q tile: rows g < G are the group's query heads, rows G..15 zero
-  for (int c = threadIdx.x; c < 16 * 16; c += 128) {
-    const int row = c >> 4, ch = c & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < G) v = *reinterpret_cast<const uint4*>(q + static_cast<int64_t>(r) * ldq + (kh * G + row) * HD + ch * 8);
-    *reinterpret_cast<uint4*>(sQ + swz(row, ch)) = v;
-  }
-  __syncthreads();
+
+  // --------------------------------------------------------- consumers (warps 1-4)
+  pdl_wait();  // q rows come from the predecessor
+  const int cw = warp - 1;  // consumer warp: tokens [16 cw, 16 cw + 16) of every page
+  const int ct = threadIdx.x - 32;
   const int mi = lane >> 3, ri = lane & 7;
-  uint32_t qf[8][4];
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    int r, kh, split, p0, np, n_pages, ctx;
+    decode_item(args, it, r, kh, split, p0, np, n_pages, ctx);
+    // Q fragments (rows = the group's heads, zero-padded to 16) straight from global
+    uint32_t qf[8][4];
+    {
+      const int r0 = lane >> 2, r1 = r0 + 8;
+      const __nv_bfloat16* qrow = args.q + static_cast<int64_t>(r) * args.ldq + kh * G * HD;
 #pragma unroll
-  for (int ks = 0; ks < 8; ++ks)
-    ldmatrix_x4(qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3],
-                smem_u32(sQ) + swz((mi & 1) * 8 + ri, ks * 2 + (mi >> 1)));
-
-  float o[16][4];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
-
-  for (int i = 0; i < np; ++i) {
-    const int st = i % DEC_STAGES;
-    mbar_wait(&full[st], (i / DEC_STAGES) & 1);
-    const uint32_t kb = smem_u32(smem + st * PAGE_BYTES);
-    const uint32_t vb = kb + 2 * HALF_TILE;
-    float s[2][4];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) s[t][0] = s[t][1] = s[t][2] = s[t][3] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      uint32_t b0, b1, b2, b3;
-      ldmatrix_x4(b0, b1, b2, b3, kv_addr(kb, warp * 16 + (mi >> 1) * 8 + ri, ks * 2 + (mi & 1)));
-      mma_bf16_16816(s[0], qf[ks], b0, b1);
-      mma_bf16_16816(s[1], qf[ks], b2, b3);
-    }
-    const int tok0 = (p0 + i) * PAGE + warp * 16;
-    float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = tok0 + t * 8 + (lane & 3) * 2 + (e & 1);
-        const float v = (j < ctx) ? s[t][e] * scale_log2 : -INFINITY;
-        s[t][e] = v;
-        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      for (int ks = 0; ks < 8; ++ks) {
+        const int c = ks * 16 + (lane & 3) * 2;
+        auto ld = [&](int row, int col) -> uint32_t {
+          return row < G ? *reinterpret_cast<const uint32_t*>(qrow + row * HD + col) : 0u;
+        };
+        qf[ks][0] = ld(r0, c);
+        qf[ks][1] = ld(r1, c);
+        qf[ks][2] = ld(r0, c + 8);
+        qf[ks][3] = ld(r1, c + 8);
       }
-    float corr[2], rs[2] = {0.f, 0.f};
+    }
+    float o[16][4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+
+    for (int i = 0; i < np; ++i) {
+      mbar_wait(&full[stage], phase);
+      const uint32_t kb = smem_u32(smem + stage * PAGE_BYTES);
+      const uint32_t vb = kb + 2 * HALF_TILE;
+      float s[2][4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) s[t][0] = s[t][1] = s[t][2] = s[t][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t b0, b1, b2, b3;
+        ldmatrix_x4(b0, b1, b2, b3, kv_addr(kb, cw * 16 + (mi >> 1) * 8 + ri, ks * 2 + (mi & 1)));
+        mma_bf16_16816(s[0], qf[ks], b0, b1);
+        mma_bf16_16816(s[1], qf[ks], b2, b3);
+      }
+      const int tok0 = (p0 + i) * PAGE + cw * 16;
+      float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = tok0 + t * 8 + (lane & 3) * 2 + (e & 1);
+          const float v = (j < ctx) ? s[t][e] * args.scale_log2 : -INFINITY;
+          s[t][e] = v;
+          mx[e >> 1] = fmaxf(mx[e >> 1], v);
+        }
+      float corr[2], rs[2] = {0.f, 0.f};
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 1));
+        mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 2));
+        const float m_new = fmaxf(m_r[hr], mx[hr]);
+        corr[hr] = (m_new == -INFINITY) ? 1.f : exp2f(m_r[hr] - m_new);
+        m_r[hr] = m_new;
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int hr = e >> 1;
+          const float p = (m_r[hr] == -INFINITY) ? 0.f : exp2f(s[t][e] - m_r[hr]);
+          s[t][e] = p;
+          rs[hr] += p;
+        }
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 1);
+        rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 2);
+        l_r[hr] = l_r[hr] * corr[hr] + rs[hr];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+        o[nt][0] *= corr[0];
+        o[nt][1] *= corr[0];
+        o[nt][2] *= corr[1];
+        o[nt][3] *= corr[1];
+      }
+      uint32_t a[4];
+      a[0] = pack_bf16x2(s[0][0], s[0][1]);
+      a[1] = pack_bf16x2(s[0][2], s[0][3]);
+      a[2] = pack_bf16x2(s[1][0], s[1][1]);
+      a[3] = pack_bf16x2(s[1][2], s[1][3]);
+#pragma unroll
+      for (int nt = 0; nt < 16; nt += 2) {
+        uint32_t b0, b1, b2, b3;
+        ldmatrix_x4_trans(b0, b1, b2, b3, kv_addr(vb, cw * 16 + (mi & 1) * 8 + ri, nt + (mi >> 1)));
+        mma_bf16_16816(o[nt], a, b0, b1);
+        mma_bf16_16816(o[nt + 1], a, b2, b3);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
+      if (++stage == DEC_STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+
+    // merge the four consumer warps (rows >= G are padding)
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
-      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 1));
-      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 2));
-      const float m_new = fmaxf(m_r[hr], mx[hr]);
-      corr[hr] = (m_new == -INFINITY) ? 1.f : exp2f(m_r[hr] - m_new);
-      m_r[hr] = m_new;
-    }
+      const int row = (lane >> 2) + hr * 8;
+      if (row < G) {
+        if ((lane & 3) == 0) {
+          red_m[cw * G + row] = m_r[hr];
+          red_l[cw * G + row] = l_r[hr];
+        }
 #pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int hr = e >> 1;
-        const float p = (m_r[hr] == -INFINITY) ? 0.f : exp2f(s[t][e] - m_r[hr]);
-        s[t][e] = p;
-        rs[hr] += p;
+        for (int nt = 0; nt < 16; ++nt) {
+          const int col = nt * 8 + (lane & 3) * 2;
+          *reinterpret_cast<float2*>(&red_o[(cw * G + row) * HD + col]) =
+              make_float2(o[nt][hr * 2], o[nt][hr * 2 + 1]);
+        }
       }
-#pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 1);
-      rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 2);
-      l_r[hr] = l_r[hr] * corr[hr] + rs[hr];
     }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const int e = ct;  // head dim owned in the merge
+    const int nsplit = args.nsplit;
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      o[nt][0] *= corr[0];
-      o[nt][1] *= corr[0];
-      o[nt][2] *= corr[1];
-      o[nt][3] *= corr[1];
-    }
-    uint32_t a[4];
-    a[0] = pack_bf16x2(s[0][0], s[0][1]);
-    a[1] = pack_bf16x2(s[0][2], s[0][3]);
-    a[2] = pack_bf16x2(s[1][0], s[1][1]);
-    a[3] = pack_bf16x2(s[1][2], s[1][3]);
+    for (int g = 0; g < G; ++g) {
+      float M = -INFINITY;
 #pragma unroll
-    for (int nt = 0; nt < 16; nt += 2) {
-      uint32_t b0, b1, b2, b3;
-      ldmatrix_x4_trans(b0, b1, b2, b3, kv_addr(vb, warp * 16 + (mi & 1) * 8 + ri, nt + (mi >> 1)));
-      mma_bf16_16816(o[nt], a, b0, b1);
-      mma_bf16_16816(o[nt + 1], a, b2, b3);
+      for (int w = 0; w < 4; ++w) M = fmaxf(M, red_m[w * G + g]);
+      float Lsum = 0.f, O = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float mw = red_m[w * G + g];
+        if (mw == -INFINITY) continue;
+        const float f = exp2f(mw - M);
+        Lsum += red_l[w * G + g] * f;
+        O += red_o[(w * G + g) * HD + e] * f;
+      }
+      const int head = kh * G + g;
+      if (nsplit == 1) {
+        args.out[static_cast<int64_t>(r) * args.ldo + head * HD + e] = f2bf(Lsum > 0.f ? O / Lsum : 0.f);
+      } else {
+        const int64_t base = (static_cast<int64_t>(r) * args.Hkv * G + head) * nsplit + split;
+        args.ws_o[base * HD + e] = O;
+        if (e == 0) args.ws_ml[base] = make_float2(M, Lsum);
+      }
     }
-    __syncthreads();  // every warp is done with stage st
-    if (threadIdx.x == 0 && i + DEC_STAGES < np) issue(i + DEC_STAGES);
+    if (nsplit > 1) {
+      // last split of (request, kv head) to finish merges every split in split order
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (ct == 0) *last_flag = atomicAdd(&args.counters[r * args.Hkv + kh], 1) == nsplit - 1;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (*last_flag) {
+        __threadfence();
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int head = kh * G + g;
+          const int64_t base = (static_cast<int64_t>(r) * args.Hkv * G + head) * nsplit;
+          float M = -INFINITY;
+          for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(&args.ws_ml[base + s2]).x);
+          float Lsum = 0.f, O = 0.f;
+          for (int s2 = 0; s2 < nsplit; ++s2) {
+            const float2 ml = __ldcg(&args.ws_ml[base + s2]);
+            if (ml.x == -INFINITY) continue;
+            const float w = exp2f(ml.x - M);
+            Lsum += ml.y * w;
+            O += __ldcg(&args.ws_o[(base + s2) * HD + e]) * w;
+          }
+          args.out[static_cast<int64_t>(r) * args.ldo + head * HD + e] =
+              f2bf(Lsum > 0.f ? O / Lsum : 0.f);
+        }
+        if (ct == 0) args.counters[r * args.Hkv + kh] = 0;
+      }
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // red_* reused by the next item
   }
-
-  // merge the four warps' softmax states (shared memory reused: all loads consumed)
-  float* red_o = reinterpret_cast<float*>(smem);               // [4][16][128]
-  float* red_m = red_o + 4 * 16 * HD;                           // [4][16]
-  float* red_l = red_m + 4 * 16;                                // [4][16]
-  __syncthreads();
-#pragma unroll
-  for (int hr = 0; hr < 2; ++hr) {
-    const int row = (lane >> 2) + hr * 8;
-    if ((lane & 3) == 0) {
-      red_m[warp * 16 + row] = m_r[hr];
-      red_l[warp * 16 + row] = l_r[hr];
-    }
-#pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      const int col = nt * 8 + (lane & 3) * 2;
-      red_o[(warp * 16 + row) * HD + col] = o[nt][hr * 2];
-      red_o[(warp * 16 + row) * HD + col + 1] = o[nt][hr * 2 + 1];
-    }
-  }
-  __syncthreads();
-  const int e = threadIdx.x;
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, red_m[w * 16 + g]);
-    float L = 0.f, O = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = red_m[w * 16 + g];
-      if (mw == -INFINITY) continue;
-      const float f = exp2f(mw - M);
-      L += red_l[w * 16 + g] * f;
-      O += red_o[(w * 16 + g) * HD + e] * f;
-    }
-    const int head = kh * G + g;
-    if (nsplit == 1) {
-      out[static_cast<int64_t>(r) * ldo + head * HD + e] = f2bf(L > 0.f ? O / L : 0.f);
-    } else {
-      const int64_t base = (static_cast<int64_t>(r) * Hq + head) * nsplit + split;
-      ws_o[base * HD + e] = O;
-      if (e == 0) ws_ml[base] = make_float2(M, L);
-    }
-  }
-  if (nsplit == 1) return;
-
-  // Split merge fused in: the last split CTA of this (request, kv head) to finish
-  // combines every split's state in split order (deterministic) and resets the counter.
-  __shared__ int last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&counters[r * Hkv + kh], 1) == nsplit - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const int head = kh * G + g;
-    const int64_t base = (static_cast<int64_t>(r) * Hq + head) * nsplit;
-    float M = -INFINITY;
-    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(&ws_ml[base + s]).x);
-    float Lsum = 0.f, o = 0.f;
-    for (int s = 0; s < nsplit; ++s) {
-      const float2 ml = __ldcg(&ws_ml[base + s]);
-      if (ml.x == -INFINITY) continue;
-      const float w = exp2f(ml.x - M);
-      Lsum += ml.y * w;
-      o += __ldcg(&ws_o[(base + s) * HD + e]) * w;
-    }
-    out[static_cast<int64_t>(r) * ldo + head * HD + e] = f2bf(Lsum > 0.f ? o / Lsum : 0.f);
-  }
-  if (threadIdx.x == 0) counters[r * Hkv + kh] = 0;
 }
 
 // Workspace: [R*Hkv arrival counters, zero between launches | o partials | (m, l)].
@@ -530,11 +601,33 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
   float2* ws_ml = need > 0 ? reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(ws_o) +
                                                        static_cast<int64_t>(R) * Hq * nsplit * hd * 4)
                            : nullptr;
-  dim3 grid(Hkv, R, nsplit);
-  constexpr int smem = DecodeSmem::TOTAL;
-  const float sl2 = scale * LOG2E;
+  DecodeArgs da;
+  da.q = q;
+  da.ldq = ldq;
+  da.block_table = block_table;
+  da.max_blocks = max_blocks;
+  da.ctx_len = ctx_len;
+  da.R = R;
+  da.Hkv = Hkv;
+  da.nsplit = nsplit;
+  da.scale_log2 = scale * LOG2E;
+  da.out = out;
+  da.ldo = ldo;
+  da.ws_o = ws_o;
+  da.ws_ml = ws_ml;
+  da.counters = counters;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int items = R * Hkv * nsplit;
+  const dim3 grid(std::min(items, sms));  // persistent: one CTA per SM
 #define PL_DECODE_CASE(GG)                                                                      \
   case GG: {                                                                                    \
+    constexpr int smem = DecodeSmem<GG>::TOTAL;                                                 \
     static bool attr = false;                                                                   \
     if (!attr) {                                                                                \
       cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<GG>,                              \
@@ -542,9 +635,8 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
       if (e != cudaSuccess) return set_cuda_error(e, "attn_decode smem attribute");             \
       attr = true;                                                                              \
     }                                                                                           \
-    rc = launch_k("attn_decode_kernel", attn_decode_kernel<GG>, grid, dim3(128), smem, st, mk,  \
-                  mv, q, ldq, block_table, max_blocks, ctx_len, Hkv, sl2, out, ldo, ws_o, ws_ml,  \
-                  counters);                                                                    \
+    rc = launch_k("attn_decode_kernel", attn_decode_kernel<GG>, grid, dim3(DEC_THREADS), smem,  \
+                  st, mk, mv, da);                                                              \
     break;                                                                                      \
   }
   switch (G) {
@@ -556,6 +648,25 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
       return set_error(PL_ERR_CONFIG, "attn_decode: GQA group %d unsupported (1,2,4,8)", G);
   }
 #undef PL_DECODE_CASE
+  return rc;
+}
+
+
+// Load every kernel of this file into the context now (lazy module loading would
+// otherwise load it at first launch, which can wait on a spinning NCCL kernel).
+template <typename K>
+static int preload_one(K k, const char* name) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, k);
+  return e == cudaSuccess ? PL_OK : set_cuda_error(e, name);
+}
+
+int attention_preload() {
+  int rc = preload_one(attn_prefill_kernel, "attn_prefill_kernel");
+  if (!rc) rc = preload_one(attn_decode_kernel<1>, "attn_decode_kernel");
+  if (!rc) rc = preload_one(attn_decode_kernel<2>, "attn_decode_kernel");
+  if (!rc) rc = preload_one(attn_decode_kernel<4>, "attn_decode_kernel");
+  if (!rc) rc = preload_one(attn_decode_kernel<8>, "attn_decode_kernel");
   return rc;
 }
 

@@ -916,4 +916,35 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   return PL_OK;
 }
 
+
+// Load every kernel of this file into the context now (lazy module loading would
+// otherwise load it at first launch, which can wait on a spinning NCCL kernel).
+template <typename K>
+static int preload_one(K k, const char* name) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, k);
+  return e == cudaSuccess ? PL_OK : set_cuda_error(e, name);
+}
+
+int gemm_preload() {
+  int rc = preload_one(gemm_tc_kernel<16, true, 2>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_tc_kernel<32, true, 2>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_tc_kernel<64, true, 2>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_tc_kernel<128, true, 2>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_tc_kernel<16, true, 1>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_tc_kernel<32, true, 1>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_tc_kernel<64, true, 1>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_tc_kernel<128, true, 1>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_tc_kernel<256, true, 1>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_tc_kernel<256, false, 1>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(argmax_reduce_kernel, "argmax_reduce_kernel");
+  if (!rc) rc = preload_one(reduce_residual_norm_kernel<1>, "reduce_residual_norm_kernel");
+  if (!rc) rc = preload_one(reduce_residual_norm_kernel<2>, "reduce_residual_norm_kernel");
+  if (!rc) rc = preload_one(reduce_residual_norm_kernel<4>, "reduce_residual_norm_kernel");
+  if (!rc) rc = preload_one(reduce_residual_norm_kernel<8>, "reduce_residual_norm_kernel");
+  if (!rc) rc = preload_one(reduce_qkv_rope_kernel, "reduce_qkv_rope_kernel");
+  if (!rc) rc = preload_one(gemm_splitk_reduce_kernel, "gemm_splitk_reduce_kernel");
+  return rc;
+}
+
 }  // namespace pl

@@ -248,4 +248,27 @@ int token_scatter_launch(const int64_t* ids, const int32_t* req_slot, const int3
                   st, ids, req_slot, out_pos, R, last_token, gen_tokens, gen_stride);
 }
 
+
+// Load every kernel of this file into the context now (lazy module loading would
+// otherwise load it at first launch, which can wait on a spinning NCCL kernel).
+template <typename K>
+static int preload_one(K k, const char* name) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, k);
+  return e == cudaSuccess ? PL_OK : set_cuda_error(e, name);
+}
+
+int kernels_preload() {
+  int rc = preload_one(fill_hash_kernel, "fill_hash_kernel");
+  if (!rc) rc = preload_one(embed_kernel, "embed_kernel");
+  if (!rc) rc = preload_one(rmsnorm_kernel<1>, "rmsnorm_kernel");
+  if (!rc) rc = preload_one(rmsnorm_kernel<2>, "rmsnorm_kernel");
+  if (!rc) rc = preload_one(rmsnorm_kernel<4>, "rmsnorm_kernel");
+  if (!rc) rc = preload_one(rmsnorm_kernel<8>, "rmsnorm_kernel");
+  if (!rc) rc = preload_one(rmsnorm_kernel<16>, "rmsnorm_kernel");
+  if (!rc) rc = preload_one(rope_kv_kernel, "rope_kv_kernel");
+  if (!rc) rc = preload_one(token_scatter_kernel, "token_scatter_kernel");
+  return rc;
+}
+
 }  // namespace pl

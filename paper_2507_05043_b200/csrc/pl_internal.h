@@ -81,6 +81,12 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
                 int epi, void* ws, int64_t ws_bytes, int64_t* argmax_out, cudaStream_t st,
                 const FusedEpi* fuse = nullptr, bool* fused = nullptr);
 
+// per-file eager kernel loading (pl_preload_kernels)
+int attention_preload();
+int kernels_preload();
+int gemm_preload();
+int transport_preload();
+
 // kernels.cu
 int fill_hash_launch(__nv_bfloat16* dst, int64_t n, uint32_t seed, uint32_t tensor_id,
                      float scale, float offset, cudaStream_t st);

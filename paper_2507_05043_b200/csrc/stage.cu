@@ -269,6 +269,8 @@ int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* laye
   if (cfg->is_first && !cfg->embed) return set_error(PL_ERR_CONFIG, "stage_create: first stage needs embed");
   if (cfg->is_last && (!cfg->lm_head || !cfg->final_norm))
     return set_error(PL_ERR_CONFIG, "stage_create: last stage needs lm_head and final_norm");
+  const int prc = pl_preload_kernels();  // no lazy module loads once links are live
+  if (prc) return prc;
   const Layout L = stage_layout(*cfg);
   if (!workspace || workspace_bytes < L.total)
     return set_error(PL_ERR_CONFIG, "stage_create: workspace %lld < required %lld",

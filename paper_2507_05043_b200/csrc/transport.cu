@@ -29,6 +29,22 @@ __global__ void gate_kernel(const uint64_t* t0, uint64_t offset_ns) {
   }
 }
 
+
+// Load every kernel of this file into the context now (lazy module loading would
+// otherwise load it at first launch, which can wait on a spinning NCCL kernel).
+template <typename K>
+static int preload_one(K k, const char* name) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, k);
+  return e == cudaSuccess ? PL_OK : set_cuda_error(e, name);
+}
+
+int transport_preload() {
+  int rc = preload_one(record_globaltimer_kernel, "record_globaltimer_kernel");
+  if (!rc) rc = preload_one(gate_kernel, "gate_kernel");
+  return rc;
+}
+
 }  // namespace pl
 
 using namespace pl;

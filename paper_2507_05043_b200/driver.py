@@ -123,6 +123,13 @@ class PipelineDriver:
         self._decision_cache: dict = {}
         self._compute_ns_cache: dict = {}
 
+    def set_link_profiles(self, link_profiles) -> None:
+        """Swap in measured link estimates (forward hops + return hop, cluster order)."""
+        if len(link_profiles) != len(self.link_profiles):
+            raise pipelink.ConfigError("link profile count must equal the hop count")
+        self.link_profiles = list(link_profiles)
+        self._decision_cache.clear()
+
     def set_stage_profiles(self, stage_profiles) -> None:
         """Swap in measured profiles (startup profiling) before the next run."""
         if len(stage_profiles) != len(self.stage_profiles):

@@ -103,8 +103,13 @@ def create_link_comms(placement: Placement) -> dict:
 
 
 class B200PipelineEngine(PipelineDriver):
+    """``native=True`` (default): the event loop and every per-micro-batch GPU action
+    run in C++ (NativeScheduler + pl_pipeline); ``native=False``: the Python
+    PipelineDriver + GpuBackend twin.  Both produce the identical schedule."""
+
     def __init__(self, cfg, cluster, stage_profiles, *, decoder: DecoderSpec, seed: int = 0,
-                 devices: list | None = None, prompts: dict | None = None, throttle: bool = False):
+                 devices: list | None = None, prompts: dict | None = None, throttle: bool = False,
+                 native: bool = True):
         if cfg.model.hidden_dim != decoder.d or cfg.model.dtype_bytes != 2:
             raise pipelink.ConfigError("cfg.model must describe the decoder's bf16 residual stream "
                                        "(use DecoderSpec.model_spec())")
@@ -120,9 +125,35 @@ class B200PipelineEngine(PipelineDriver):
                               throttle=throttle)
         super().__init__(cfg, cluster, stage_profiles, backend=self.gpu)
         self._comms = comms
+        self.native = native
+        self._sched = None
+
+    def set_stage_profiles(self, stage_profiles) -> None:
+        super().set_stage_profiles(stage_profiles)
+        self._sched = None
+
+    def set_link_profiles(self, link_profiles) -> None:
+        super().set_link_profiles(link_profiles)
+        self._sched = None
+
+    def _native_run(self, trace, horizon_s):
+        from .native import NativeScheduler
+
+        if self._sched is None:
+            self._sched = NativeScheduler(self.cfg, self.stage_profiles, self.link_profiles,
+                                          self.bytes_per_token)
+        g = self.gpu
+        g.driver = self
+        handle = g.native_start(trace, record_links=g.record_links)
+        result = self._sched.run(trace, horizon_s, pipeline=handle)
+        g.native_finish(result)
+        return result
 
     def run(self, trace, horizon_s: float | None = None):
-        result = super().run(trace, horizon_s)
+        if self.native:
+            result = self._native_run(trace, horizon_s)
+        else:
+            result = super().run(trace, horizon_s)
         g = self.gpu
         stats = B200Stats(run_time_s=g.run_time_s, tokens=g.tokens, decode_start_s=g.decode_start_s)
         if g.tokens is not None:
@@ -176,6 +207,9 @@ class B200PipelineEngine(PipelineDriver):
         self.gpu.prepare(trace)
 
     def close(self) -> None:
+        if self._sched is not None:
+            self._sched.close()
+            self._sched = None
         self.gpu.close()
         for h in self._comms.values():
             N.lib().pl_comm_destroy(h)

@@ -70,6 +70,18 @@ def _comm_pair():
         h = C.c_void_p()
         N.call("pl_comm_init_rank", uid, 2, 0 if dist.get_rank() == src else 1, C.byref(h))
         comms.append(h)
+    # Establish both P2P connections now, from one thread, in the same order on both
+    # ranks: NCCL connects lazily on first use, and a connect issued while the other
+    # link's receive kernel spins on the same GPU can wait on that kernel forever.
+    dev = torch.device("cuda", torch.cuda.current_device())
+    buf = torch.zeros(8, dtype=torch.int64, device=dev)
+    st = torch.cuda.Stream(dev)
+    for src, h in zip((0, 1), comms):
+        if dist.get_rank() == src:
+            N.call("pl_p2p_send", h, buf.data_ptr(), 64, 1, st.cuda_stream)
+        else:
+            N.call("pl_p2p_recv", h, buf.data_ptr(), 64, 0, st.cuda_stream)
+        st.synchronize()
     return comms
 
 
@@ -101,7 +113,8 @@ def run_device_demo(cfg, cluster, stage_profiles, trace, *, decoder, seed: int =
 
 
 def _tail(be, exe, comm_fwd, comm_ret, cfg, policy, timeout_s):
-    ret = DeviceLinkSender(comm_ret, 0, cfg.chunk_size, policy, "ret-sender", exe.device)
+    # return link: this rank created it, so it is comm-rank 0 and the head is peer 1
+    ret = DeviceLinkSender(comm_ret, 1, cfg.chunk_size, policy, "ret-sender", exe.device)
     ret.start()
     stream = exe.stream
     d = exe.spec.d
@@ -136,7 +149,7 @@ def _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profi
           bytes_per_token, timeout_s, dev):
     fwd = DeviceLinkSender(comm_fwd, 1, cfg.chunk_size, policy, "fwd-sender", dev)
     feedback: queue.Queue = queue.Queue()
-    head_recv = DeviceLinkReceiver(comm_ret, 1, feedback.put, "head-recv", dev)
+    head_recv = DeviceLinkReceiver(comm_ret, 0, feedback.put, "head-recv", dev)  # tail = comm-rank 0
     fwd.start()
     head_recv.start()
     pending = deque(requests[r.id] for r in trace.requests)

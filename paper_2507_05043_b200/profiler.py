@@ -117,3 +117,71 @@ def gather_profiles(local: dict, n_stages: int) -> list:
         return [pipelink.StageProfile(stage_id=s, layers=layers[s], entries=merged[s])
                 for s in range(n_stages)]
     return [local[s] for s in range(n_stages)]
+
+
+def measure_links(engine, small: int = 4096, large: int = 16 << 20, reps: int = 5) -> list:
+    """Measure every hop of `engine` as a reference LinkProfile (latency_s, bytes/s).
+
+    Same-process hops time a device copy on the source's link stream; hops between
+    ranks time an ncclSend on the source rank's link communicator (the matching
+    ncclRecv is posted by the destination).  latency = time(small message);
+    bandwidth = (large - small) / (time(large) - time(small)).  All ranks iterate
+    the hops in the same order and the results are all-gathered, so every rank's
+    virtual clock sees identical link profiles.
+    """
+    import torch.distributed as dist
+
+    from . import _native as N
+
+    g = engine.gpu
+    pl = g.pl
+    S = pl.n_stages
+    lib = N.lib()
+    measured = {}
+    if S < 2:
+        return []
+    for link in range(S):
+        src = S - 1 if link == S - 1 else link
+        dst = 0 if link == S - 1 else link + 1
+        src_local, dst_local = pl.local(src), pl.local(dst)
+        if not (src_local or dst_local):
+            continue
+        dev = g.exe[src].device if src_local else g.exe[dst].device
+        with torch.cuda.device(dev):
+            sbuf = torch.empty(large, dtype=torch.uint8, device=dev) if src_local else None
+            dbuf = (torch.empty(large, dtype=torch.uint8, device=g.exe[dst].device)
+                    if dst_local else None)
+            st = g.send_stream[src] if src_local else g.recv_stream[dst]
+
+            def once(nbytes):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                if src_local and dst_local:
+                    N.check(lib.pl_memcpy_async(dbuf.data_ptr(), sbuf.data_ptr(), nbytes, st.cuda_stream),
+                            "pl_memcpy_async")
+                elif src_local:
+                    N.check(lib.pl_p2p_send(g.comms[link], sbuf.data_ptr(), nbytes, 1, st.cuda_stream),
+                            "pl_p2p_send")
+                else:
+                    N.check(lib.pl_p2p_recv(g.comms[link], dbuf.data_ptr(), nbytes, 0, st.cuda_stream),
+                            "pl_p2p_recv")
+                b.record(st)
+                b.synchronize()
+                return a.elapsed_time(b) / 1e3
+
+            once(small)
+            t_small = float(np.median([once(small) for _ in range(reps)]))
+            t_large = float(np.median([once(large) for _ in range(reps)]))
+        if src_local:
+            bw = (large - small) / max(t_large - t_small, 1e-9)
+            measured[link] = (round(t_small, 9), float(f"{bw:.4g}"))
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        parts = [None] * dist.get_world_size()
+        dist.all_gather_object(parts, measured)
+        for p in parts:
+            measured.update(p)
+    out = []
+    for link, lp in enumerate(engine.link_profiles):
+        lat, bw = measured[link]
+        out.append(pipelink.LinkProfile(lp.src, lp.dst, lat, bw))
+    return out

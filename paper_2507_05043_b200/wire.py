@@ -9,14 +9,15 @@ Same contract as ``SocketLinkSender`` / ``SocketLinkReceiver``:
 * the sender owns an unchanged reference ``LinkQueue`` (transport.py:70-160) and
   a worker thread drains it one chunk per frame, so decode payloads preempt
   prefill payloads at chunk boundaries exactly as on the socket backend;
-* a frame is a 32-byte header (payload id, chunk index, flags, body bytes) and
-  the chunk's bytes, each one ``ncclSend`` on the sender's stream -- the body
+* a frame is a 40-byte header (payload id, chunk index, flags, chunk bytes,
+  payload bytes) and the chunk's bytes, each one ``ncclSend`` on the sender's stream -- the body
   goes GPU to GPU over NVLink straight from the payload tensor;
 * flags are the socket backend's (``FLAG_LAST`` / ``FLAG_DECODE`` /
   ``FLAG_SHUTDOWN``, wire.py:31-33); ``send`` raises ``ProtocolError`` on a size
   mismatch, a duplicate id or while closing (wire.py:93-105); the sender holds
   the body until its last chunk is on the wire (wire.py:103, 142-146);
-* the receiver reassembles chunks into one device tensor and calls
+* the receiver lands every chunk at its offset of one device tensor (no
+  re-copy, no torch kernel while NCCL kernels spin) and calls
   ``on_payload(ReceivedDevicePayload)`` on its own thread; transport failures
   set ``failed`` (wire.py:160-185).
 
@@ -42,7 +43,8 @@ ProtocolError = pipelink.ProtocolError
 FLAG_LAST = 1
 FLAG_DECODE = 2
 FLAG_SHUTDOWN = 4
-HEADER_WORDS = 4  # int64: payload id, chunk index, flags, body bytes
+HEADER_WORDS = 5  # int64: payload id, chunk index, flags, chunk bytes, payload bytes
+HEADER_BYTES = HEADER_WORDS * 8
 
 
 @dataclass
@@ -105,15 +107,17 @@ class DeviceLinkSender(threading.Thread):
                     return False
                 self._cond.wait()
 
-    def _frame(self, payload_id: int, index: int, flags: int, piece: torch.Tensor | None) -> None:
+    def _frame(self, payload_id: int, index: int, flags: int, piece: torch.Tensor | None,
+               total: int = 0) -> None:
         size = 0 if piece is None else piece.numel()
         self._stream.synchronize()  # the pinned header staging buffer is reused per frame
-        self._hdr_host.numpy()[:] = np.array([payload_id, index, flags, size], dtype=np.int64)
+        self._hdr_host.numpy()[:] = np.array([payload_id, index, flags, size, total], dtype=np.int64)
         lib = N.lib()
         st = self._stream.cuda_stream
-        N.check(lib.pl_memcpy_async(self._hdr_dev.data_ptr(), self._hdr_host.data_ptr(), 32, st),
+        N.check(lib.pl_memcpy_async(self._hdr_dev.data_ptr(), self._hdr_host.data_ptr(), HEADER_BYTES, st),
                 "pl_memcpy_async")
-        N.check(lib.pl_p2p_send(self._comm, self._hdr_dev.data_ptr(), 32, self._peer, st), "pl_p2p_send")
+        N.check(lib.pl_p2p_send(self._comm, self._hdr_dev.data_ptr(), HEADER_BYTES, self._peer, st),
+                "pl_p2p_send")
         if size:
             N.check(lib.pl_p2p_send(self._comm, piece.data_ptr(), size, self._peer, st), "pl_p2p_send")
         self.frames += 1
@@ -131,7 +135,8 @@ class DeviceLinkSender(threading.Thread):
                     self._stream.wait_event(ready)
                 flags = (FLAG_LAST if chunk.is_last else 0) | (
                     FLAG_DECODE if chunk.phase_class is PayloadClass.DECODE else 0)
-                self._frame(chunk.payload_id, chunk.index, flags, body[off:off + chunk.size_bytes])
+                self._frame(chunk.payload_id, chunk.index, flags, body[off:off + chunk.size_bytes],
+                            body.numel())
                 if chunk.is_last:
                     self._stream.synchronize()  # ownership ends once the last chunk is on the wire
                     del self._bodies[chunk.payload_id]
@@ -173,28 +178,35 @@ class DeviceLinkReceiver(threading.Thread):
 
     def _loop(self, lib, st) -> None:
         while True:
-            N.check(lib.pl_p2p_recv(self._comm, self._hdr_dev.data_ptr(), 32, self._peer, st),
+            N.check(lib.pl_p2p_recv(self._comm, self._hdr_dev.data_ptr(), HEADER_BYTES, self._peer, st),
                     "pl_p2p_recv")
-            N.check(lib.pl_memcpy_async(self._hdr_host.data_ptr(), self._hdr_dev.data_ptr(), 32, st),
-                    "pl_memcpy_async")
+            N.check(lib.pl_memcpy_async(self._hdr_host.data_ptr(), self._hdr_dev.data_ptr(), HEADER_BYTES,
+                                        st), "pl_memcpy_async")
             self._stream.synchronize()
-            pid, index, flags, size = (int(v) for v in self._hdr_host.numpy())
+            pid, index, flags, size, total = (int(v) for v in self._hdr_host.numpy())
             if flags & FLAG_SHUTDOWN:
                 self.failed = bool(self._partial)
                 return
-            if size < 0:
-                raise ProtocolError(f"bad frame length {size}")
-            parts = self._partial.setdefault(pid, [])
-            if index != len(parts):
+            if size < 0 or total < size:
+                raise ProtocolError(f"bad frame length {size} of {total}")
+            if index == 0:
+                if pid in self._partial:
+                    raise ProtocolError(f"payload {pid}: duplicate first chunk")
+                self._partial[pid] = [torch.empty(total, dtype=torch.uint8, device=self.device), 0, 0]
+            state = self._partial.get(pid)
+            if state is None or index != state[2]:
                 raise ProtocolError(f"payload {pid}: chunk {index} out of order")
-            piece = torch.empty(size, dtype=torch.uint8, device=self.device)
+            body, off, _ = state
+            if off + size > body.numel():
+                raise ProtocolError(f"payload {pid}: chunks overrun {body.numel()} bytes")
             if size:
-                N.check(lib.pl_p2p_recv(self._comm, piece.data_ptr(), size, self._peer, st),
+                N.check(lib.pl_p2p_recv(self._comm, body.data_ptr() + off, size, self._peer, st),
                         "pl_p2p_recv")
-            parts.append(piece)
+            state[1], state[2] = off + size, index + 1
             if flags & FLAG_LAST:
                 del self._partial[pid]
-                body = parts[0] if len(parts) == 1 else torch.cat(parts)
+                if state[1] != body.numel():
+                    raise ProtocolError(f"payload {pid}: {state[1]} of {body.numel()} bytes arrived")
                 self._stream.synchronize()
                 phase = PayloadClass.DECODE if flags & FLAG_DECODE else PayloadClass.PREFILL
                 self._on_payload(ReceivedDevicePayload(pid, phase, body))

@@ -19,6 +19,9 @@ def main():
     import torch
     import torch.distributed as dist
 
+    import faulthandler
+
+    faulthandler.dump_traceback_later(150, exit=True)  # a hang prints every thread's stack
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     dist.init_process_group(backend="cuda:nccl,cpu:gloo")
     from paper_2507_05043_b200 import TINY, deploy
@@ -57,4 +60,13 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    except SystemExit:
+        raise
+    except BaseException:
+        import traceback
+
+        traceback.print_exc(file=sys.stdout)
+        sys.stdout.flush()
+        raise

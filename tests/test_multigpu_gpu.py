@@ -36,7 +36,7 @@ def torchrun(script, *args, nproc=2, timeout=600):
            *args]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout,
                        env={**os.environ, "PYTHONPATH": str(ROOT)})
-    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert p.returncode == 0, p.stdout[-6000:] + p.stderr[-2000:]
     return p.stdout
 
 

@@ -40,9 +40,9 @@ def config1(spec, S=2, n_req=8, in_len=128, out_len=32, mbt=1024, chunk=pipelink
     return cfg, cluster, plan, deploy.uniform_trace(n_req, in_len, out_len)
 
 
-def run_gpu(spec, cfg, cluster, plan, trace, seed=0):
+def run_gpu(spec, cfg, cluster, plan, trace, seed=0, native=True):
     profiles = synth_profiles(plan)
-    eng = B200PipelineEngine(cfg, cluster, profiles, decoder=spec, seed=seed)
+    eng = B200PipelineEngine(cfg, cluster, profiles, decoder=spec, seed=seed, native=native)
     res = eng.run(trace)
     ref = pipelink.PipelineEngine(cfg, cluster, profiles).run(trace)
     a, b = result_key(ref), result_key(res)
@@ -61,10 +61,12 @@ def oracle_greedy(spec, trace, seed=0, lo=0, hi=None):
     return model, prompts, toks
 
 
-def test_config1_peaked_tokens_identical():
+@pytest.mark.parametrize("native", [True, False], ids=["native", "python"])
+def test_config1_peaked_tokens_identical(native):
+    """Native C++ runtime and the Python driver twin: same schedule, same tokens."""
     spec = TINY.with_(peaked=True)
     cfg, cluster, plan, trace = config1(spec)
-    res = run_gpu(spec, cfg, cluster, plan, trace)
+    res = run_gpu(spec, cfg, cluster, plan, trace, native=native)
     _, _, want = oracle_greedy(spec, trace)
     for i, r in enumerate(trace.requests):
         got = res.b200.tokens[r.id]
@@ -179,11 +181,12 @@ def test_decode_logits_within_tolerance(spec):
     exe.close()
 
 
-@pytest.mark.parametrize("S", [1, 4])
-def test_stage_counts_on_one_gpu(S):
-    spec = TINY.with_(peaked=True)
+@pytest.mark.parametrize("native", [True, False], ids=["native", "python"])
+@pytest.mark.parametrize("S", [1, 4, 8])
+def test_stage_counts_on_one_gpu(S, native):
+    spec = TINY.with_(peaked=True, num_layers=max(4, S))
     cfg, cluster, plan, trace = config1(spec, S=S, n_req=5, in_len=70, out_len=9, mbt=256)
-    res = run_gpu(spec, cfg, cluster, plan, trace)
+    res = run_gpu(spec, cfg, cluster, plan, trace, native=native)
     _, _, want = oracle_greedy(spec, trace)
     for i, r in enumerate(trace.requests):
         assert np.array_equal(res.b200.tokens[r.id], want[i].numpy())
@@ -226,3 +229,34 @@ def test_real_clock_run_result_feeds_reference_metrics():
     # per-request tokens are emitted in order on the device clock
     for rid, ts in res.b200.token_times_s.items():
         assert ts == sorted(ts) and len(ts) == 8
+
+
+def test_realized_link_log_matches_virtual_chunks():
+    """Per-chunk CUDA events on the link streams: the realized chunk sequence on every
+    link is the LinkQueue's (same payloads, indices, sizes, order), chunks never overlap
+    on a link, bytes are conserved and no chunk leaves before its payload exists."""
+    spec = TINY.with_(peaked=True)
+    cfg, cluster, plan, trace = config1(spec, S=2, n_req=6, in_len=300, out_len=5, chunk=16384)
+    profiles = synth_profiles(plan)
+    eng = B200PipelineEngine(cfg, cluster, profiles, decoder=spec)
+    eng.gpu.record_links = True
+    res = eng.run(trace)
+    real = eng.gpu.realized_links
+    for name in {e.link for e in res.link_events}:
+        virt = [(e.payload_id, e.chunk_index, e.size_bytes) for e in res.link_events
+                if e.link == name and e.event == "emit"]
+        emits = [e for e in real if e.link == name and e.event == "emit"]
+        sents = [e for e in real if e.link == name and e.event == "sent"]
+        assert [(e.payload_id, e.chunk_index, e.size_bytes) for e in emits] == virt
+        for a, b in zip(sents, emits[1:]):
+            assert b.time_ns >= a.time_ns, "two chunks in flight on one link"
+        enq = {e.payload_id: e.time_ns for e in real if e.link == name and e.event == "enqueue"}
+        sizes = {}
+        for e in emits:
+            assert e.time_ns >= enq[e.payload_id] - 1000, "chunk left before its payload existed"
+            sizes[e.payload_id] = sizes.get(e.payload_id, 0) + e.size_bytes
+        virt_sizes = {e.payload_id: e.size_bytes for e in res.link_events
+                      if e.link == name and e.event == "enqueue"}
+        assert sizes == virt_sizes
+    assert any(e.chunk_index > 0 for e in real), "prefill payloads were not chunked"
+    eng.close()
