@@ -264,19 +264,27 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
 
 constexpr int PAGE = 64;                 // tokens per KV block
 constexpr int MAX_PAGES_PER_SPLIT = 8;   // <= 512 tokens per split, pages spread evenly
-constexpr int DEC_STAGES = 4;
 constexpr int HALF_TILE = 64 * 128;      // 64 tokens x 64 dims bf16 (one TMA box)
 constexpr int PAGE_BYTES = 4 * HALF_TILE;  // K lo | K hi | V lo | V hi
 constexpr int DEC_THREADS = 160;         // producer warp + 4 consumer warps
+constexpr int Q_PITCH = HD * 2 + 16;     // padded q row in shared memory (conflict-free)
+constexpr int Q_SLOTS = 2;
+
+struct ItemInfo {
+  int r, kh, split, p0, np, ctx, pad0, pad1;
+};
 
 template <int G>
 struct DecodeSmem {
-  static constexpr int RED_O = DEC_STAGES * PAGE_BYTES;     // [4 warps][G][128] fp32
-  static constexpr int RED_M = RED_O + 4 * G * HD * 4;      // [4][G]
-  static constexpr int RED_L = RED_M + 4 * G * 4;           // [4][G]
-  static constexpr int BAR = RED_L + 4 * G * 4;             // full[S], empty[S]
-  static constexpr int FLAG = BAR + 16 * DEC_STAGES;
-  static constexpr int TOTAL = FLAG + 16 + 1024;            // + alignment slack
+  static constexpr int STAGES = G <= 4 ? 3 : 2;               // 2 CTAs per SM either way
+  static constexpr int Q = STAGES * PAGE_BYTES;                // [Q_SLOTS][G][Q_PITCH]
+  static constexpr int INFO = Q + Q_SLOTS * G * Q_PITCH;       // [Q_SLOTS] ItemInfo
+  static constexpr int RED_O = INFO + Q_SLOTS * 32;            // [4 warps][G][128] fp32
+  static constexpr int RED_M = RED_O + 4 * G * HD * 4;         // [4][G]
+  static constexpr int RED_L = RED_M + 4 * G * 4;              // [4][G]
+  static constexpr int BAR = (RED_L + 4 * G * 4 + 7) & ~7;     // full[S], empty[S], qfull[2], qempty[2]
+  static constexpr int FLAG = BAR + 8 * (2 * STAGES + 2 * Q_SLOTS);
+  static constexpr int TOTAL = FLAG + 16 + 1024;               // + alignment slack
 };
 
 // address of 16-byte chunk `c` (0..15) of token row `row` in a (lo|hi) 128B-swizzled pair
@@ -305,7 +313,7 @@ PL_DEV void decode_item(const DecodeArgs& a, int it, int& r, int& kh, int& split
   split = it % a.nsplit;
   kh = (it / a.nsplit) % a.Hkv;
   r = it / (a.nsplit * a.Hkv);
-  ctx = a.ctx_len[r];
+  ctx = __ldg(a.ctx_len + r);
   n_pages = (ctx + PAGE - 1) / PAGE;
   const int ns_r = max(1, (n_pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
   const int pps = (n_pages + ns_r - 1) / ns_r;
@@ -313,19 +321,30 @@ PL_DEV void decode_item(const DecodeArgs& a, int it, int& r, int& kh, int& split
   np = max(0, min(n_pages, p0 + pps) - p0);
 }
 
+// Persistent: 2 CTAs per SM walk the (request, kv head, split) items.  Warp 0 is
+// the producer: per item it fetches the geometry and the (<= 8) block-table
+// entries with one warp-wide load, then streams q (G rows, 1-D bulk copies into a
+// 2-slot ring together with the item geometry) and the K/V pages (4 TMA boxes
+// each) through a STAGES-deep ring.  Warps 1-4 never touch global memory until
+// the output: S = Q K^T and O += P V on m16n8k16 tensor cores with Q = the GQA
+// group padded to 16 rows, per-warp online softmax, warps merged in shared memory.
 template <int G>
-__global__ void __launch_bounds__(DEC_THREADS, 1)
+__global__ void __launch_bounds__(DEC_THREADS, 2)
     attn_decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                        const DecodeArgs args) {
   using L = DecodeSmem<G>;
+  constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   float* red_o = reinterpret_cast<float*>(smem + L::RED_O);
   float* red_m = reinterpret_cast<float*>(smem + L::RED_M);
   float* red_l = reinterpret_cast<float*>(smem + L::RED_L);
+  ItemInfo* info = reinterpret_cast<ItemInfo*>(smem + L::INFO);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR);
-  uint64_t* empty = full + DEC_STAGES;
+  uint64_t* empty = full + STAGES;
+  uint64_t* qfull = empty + STAGES;
+  uint64_t* qempty = qfull + Q_SLOTS;
   int* last_flag = reinterpret_cast<int*>(smem + L::FLAG);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = args.R * args.Hkv * args.nsplit;
@@ -333,9 +352,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    for (int s = 0; s < DEC_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 4);
+    }
+    for (int s = 0; s < Q_SLOTS; ++s) {
+      mbar_init(&qfull[s], 1);
+      mbar_init(&qempty[s], 4);
     }
     fence_mbar_init();
   }
@@ -343,67 +366,97 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
   pdl_trigger();
 
   if (warp == 0) {
-    // ------------------------------------------------------- TMA producer
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
-      bool waited = false;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        int r, kh, split, p0, np, n_pages, ctx;
-        decode_item(args, it, r, kh, split, p0, np, n_pages, ctx);
-        const int32_t* bt = args.block_table + static_cast<int64_t>(r) * args.max_blocks;
-        for (int i = 0; i < np; ++i) {
-          // the newest token's page was written by the predecessor kernel
-          if (!waited && p0 + i == n_pages - 1) {
-            pdl_wait();
-            waited = true;
+    // ------------------------------------------------------- producer warp
+    const uint64_t pol = policy_evict_first();
+    int stage = 0, qs = 0;
+    uint32_t phase = 0, qphase = 0;
+    bool waited = false;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      int r, kh, split, p0, np, n_pages, ctx;
+      decode_item(args, it, r, kh, split, p0, np, n_pages, ctx);
+      const int32_t* bt = args.block_table + static_cast<int64_t>(r) * args.max_blocks;
+      const int mine = lane < np ? __ldg(bt + p0 + lane) : 0;  // np <= MAX_PAGES_PER_SPLIT
+      int pg[MAX_PAGES_PER_SPLIT];
+#pragma unroll
+      for (int i = 0; i < MAX_PAGES_PER_SPLIT; ++i) pg[i] = __shfl_sync(0xffffffffu, mine, i);
+      if (lane == 0) {
+        // pages complete before this step stream ahead of griddepcontrol.wait; the page
+        // holding the newest token (the request's last) and q come from the predecessor
+        const int cold = np - (p0 + np == n_pages ? 1 : 0);
+        const int pre = waited ? 0 : min(cold, STAGES);
+#pragma unroll
+        for (int i = 0; i < MAX_PAGES_PER_SPLIT; ++i) {
+          if (i == pre) {
+            if (!waited) {
+              pdl_wait();
+              waited = true;
+            }
+            mbar_wait(&qempty[qs], qphase ^ 1);
+            info[qs] = ItemInfo{r, kh, split, p0, np, ctx, 0, 0};
+            uint8_t* qd = smem + L::Q + qs * G * Q_PITCH;
+            const __nv_bfloat16* qsrc = args.q + static_cast<int64_t>(r) * args.ldq + kh * G * HD;
+            mbar_arrive_expect_tx(&qfull[qs], G * HD * 2);
+#pragma unroll
+            for (int g = 0; g < G; ++g) bulk_load(qd + g * Q_PITCH, qsrc + g * HD, HD * 2, &qfull[qs]);
+            if (++qs == Q_SLOTS) {
+              qs = 0;
+              qphase ^= 1;
+            }
           }
-          mbar_wait(&empty[stage], phase ^ 1);
-          const int row0 = (bt[p0 + i] * args.Hkv + kh) * PAGE;
-          uint8_t* dst = smem + stage * PAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], PAGE_BYTES);
-          tma_load_2d(dst, &tmK, &full[stage], 0, row0, pol);
-          tma_load_2d(dst + HALF_TILE, &tmK, &full[stage], 64, row0, pol);
-          tma_load_2d(dst + 2 * HALF_TILE, &tmV, &full[stage], 0, row0, pol);
-          tma_load_2d(dst + 3 * HALF_TILE, &tmV, &full[stage], 64, row0, pol);
-          if (++stage == DEC_STAGES) {
-            stage = 0;
-            phase ^= 1;
+          if (i < np) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            const int row0 = (pg[i] * args.Hkv + kh) * PAGE;
+            uint8_t* dst = smem + stage * PAGE_BYTES;
+            mbar_arrive_expect_tx(&full[stage], PAGE_BYTES);
+            tma_load_2d(dst, &tmK, &full[stage], 0, row0, pol);
+            tma_load_2d(dst + HALF_TILE, &tmK, &full[stage], 64, row0, pol);
+            tma_load_2d(dst + 2 * HALF_TILE, &tmV, &full[stage], 0, row0, pol);
+            tma_load_2d(dst + 3 * HALF_TILE, &tmV, &full[stage], 64, row0, pol);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
-      if (!waited) pdl_wait();
+      __syncwarp();
     }
+    if (lane == 0 && !waited) pdl_wait();
     return;
   }
 
   // --------------------------------------------------------- consumers (warps 1-4)
-  pdl_wait();  // q rows come from the predecessor
   const int cw = warp - 1;  // consumer warp: tokens [16 cw, 16 cw + 16) of every page
   const int ct = threadIdx.x - 32;
   const int mi = lane >> 3, ri = lane & 7;
-  int stage = 0;
-  uint32_t phase = 0;
+  int stage = 0, qs = 0;
+  uint32_t phase = 0, qphase = 0;
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-    int r, kh, split, p0, np, n_pages, ctx;
-    decode_item(args, it, r, kh, split, p0, np, n_pages, ctx);
-    // Q fragments (rows = the group's heads, zero-padded to 16) straight from global
+    mbar_wait(&qfull[qs], qphase);
+    const ItemInfo inf = info[qs];
+    const int r = inf.r, kh = inf.kh, split = inf.split, p0 = inf.p0, np = inf.np, ctx = inf.ctx;
+    // Q fragments (rows = the group's heads, zero-padded to 16)
     uint32_t qf[8][4];
     {
+      const uint8_t* qb = smem + L::Q + qs * G * Q_PITCH;
       const int r0 = lane >> 2, r1 = r0 + 8;
-      const __nv_bfloat16* qrow = args.q + static_cast<int64_t>(r) * args.ldq + kh * G * HD;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        const int c = ks * 16 + (lane & 3) * 2;
-        auto ld = [&](int row, int col) -> uint32_t {
-          return row < G ? *reinterpret_cast<const uint32_t*>(qrow + row * HD + col) : 0u;
+        const int c = (ks * 16 + (lane & 3) * 2) * 2;
+        auto ld = [&](int row, int off) -> uint32_t {
+          return row < G ? *reinterpret_cast<const uint32_t*>(qb + row * Q_PITCH + off) : 0u;
         };
         qf[ks][0] = ld(r0, c);
         qf[ks][1] = ld(r1, c);
-        qf[ks][2] = ld(r0, c + 8);
-        qf[ks][3] = ld(r1, c + 8);
+        qf[ks][2] = ld(r0, c + 16);
+        qf[ks][3] = ld(r1, c + 16);
       }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&qempty[qs]);
+    if (++qs == Q_SLOTS) {
+      qs = 0;
+      qphase ^= 1;
     }
     float o[16][4];
 #pragma unroll
@@ -480,7 +533,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
-      if (++stage == DEC_STAGES) {
+      if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
       }
@@ -624,7 +677,7 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
     if (sms <= 0) sms = 148;
   }
   const int items = R * Hkv * nsplit;
-  const dim3 grid(std::min(items, sms));  // persistent: one CTA per SM
+  const dim3 grid(std::min(items, 2 * sms));  // persistent: two CTAs per SM
 #define PL_DECODE_CASE(GG)                                                                      \
   case GG: {                                                                                    \
     constexpr int smem = DecodeSmem<GG>::TOTAL;                                                 \

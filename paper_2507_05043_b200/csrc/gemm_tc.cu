@@ -498,8 +498,10 @@ __global__ void __launch_bounds__(256)
 // per token row (partials feature-contiguous, [splits][T][N]):
 //   h[t]  = bf16(bf16(sum_s partial) + h[t])             (residual, modeling_llama.py:313-331)
 //   a[t]  = bf16(w * bf16(h[t] * rsqrt(mean(h[t]^2)+eps)))   (RMSNorm, :62-67)
-template <int VPT>  // float4 chunks per thread (N <= 1024 * VPT)
-__global__ void __launch_bounds__(256)
+// Up to 1024 threads per row, VPT float4 per thread; the residual row and four
+// splits' partials are in flight at once (latency-bound, not bandwidth-bound).
+template <int VPT>  // float4 chunks per thread
+__global__ void __launch_bounds__(1024)
     reduce_residual_norm_kernel(const float* __restrict__ partial, int splits, int T, int N,
                                 __nv_bfloat16* __restrict__ h, int64_t ldh,
                                 const __nv_bfloat16* __restrict__ w, float eps,
@@ -507,40 +509,64 @@ __global__ void __launch_bounds__(256)
   pdl_trigger();
   pdl_wait();
   const int t = blockIdx.x;
+  const int nt = blockDim.x;
+  uint2 old[VPT];
+  float4 acc[VPT];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int f = (threadIdx.x + nt * k) * 4;
+    acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    old[k] = f < N ? *reinterpret_cast<const uint2*>(h + static_cast<int64_t>(t) * ldh + f) : make_uint2(0, 0);
+  }
+  const int64_t stride = static_cast<int64_t>(T) * N;
+  const float* prow = partial + static_cast<int64_t>(t) * N;
+  for (int s0 = 0; s0 < splits; s0 += 4) {
+    float4 x[4][VPT];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        const int f = (threadIdx.x + nt * k) * 4;
+        x[u][k] = (s0 + u < splits && f < N)
+                      ? __ldcg(reinterpret_cast<const float4*>(prow + (s0 + u) * stride + f))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {  // split order (deterministic)
+        acc[k].x += x[u][k].x;
+        acc[k].y += x[u][k].y;
+        acc[k].z += x[u][k].z;
+        acc[k].w += x[u][k].w;
+      }
+  }
   float hv[VPT][4];
   float ss = 0.f;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int f = (threadIdx.x + 256 * k) * 4;
+    const int f = (threadIdx.x + nt * k) * 4;
     if (f >= N) continue;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4* p = reinterpret_cast<const float4*>(partial + static_cast<int64_t>(t) * N + f);
-    const int64_t stride = static_cast<int64_t>(T) * N / 4;
-    for (int s = 0; s < splits; ++s) {
-      const float4 x = p[s * stride];
-      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
-    }
-    uint2* hp = reinterpret_cast<uint2*>(h + static_cast<int64_t>(t) * ldh + f);
-    const uint2 old = *hp;
-    const float2 o0 = unpack_bf16x2(old.x), o1 = unpack_bf16x2(old.y);
-    hv[k][0] = rbf(rbf(acc.x) + o0.x);
-    hv[k][1] = rbf(rbf(acc.y) + o0.y);
-    hv[k][2] = rbf(rbf(acc.z) + o1.x);
-    hv[k][3] = rbf(rbf(acc.w) + o1.y);
-    *hp = make_uint2(pack_bf16x2(hv[k][0], hv[k][1]), pack_bf16x2(hv[k][2], hv[k][3]));
+    const float2 o0 = unpack_bf16x2(old[k].x), o1 = unpack_bf16x2(old[k].y);
+    hv[k][0] = rbf(rbf(acc[k].x) + o0.x);
+    hv[k][1] = rbf(rbf(acc[k].y) + o0.y);
+    hv[k][2] = rbf(rbf(acc[k].z) + o1.x);
+    hv[k][3] = rbf(rbf(acc[k].w) + o1.y);
+    *reinterpret_cast<uint2*>(h + static_cast<int64_t>(t) * ldh + f) =
+        make_uint2(pack_bf16x2(hv[k][0], hv[k][1]), pack_bf16x2(hv[k][2], hv[k][3]));
     ss += hv[k][0] * hv[k][0] + hv[k][1] * hv[k][1] + hv[k][2] * hv[k][2] + hv[k][3] * hv[k][3];
   }
-  __shared__ float red[8];
+  __shared__ float red[32];
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   float tot = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) tot += red[i];
+  const int nw = nt >> 5;
+  for (int i = 0; i < nw; ++i) tot += red[i];
   const float inv = 1.0f / sqrtf(tot / static_cast<float>(N) + eps);
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int f = (threadIdx.x + 256 * k) * 4;
+    const int f = (threadIdx.x + nt * k) * 4;
     if (f >= N) continue;
     const uint2 wv = *reinterpret_cast<const uint2*>(w + f);
     const float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y);
@@ -577,10 +603,19 @@ __global__ void __launch_bounds__(256)
     float4 a1 = make_float4(0.f, 0.f, 0.f, 0.f), a2 = a1;
     const float4* p1 = P + (static_cast<int64_t>(n1) * Tp + t0) / 4;
     const float4* p2 = P + (static_cast<int64_t>(n2) * Tp + t0) / 4;
-    for (int s = 0; s < splits; ++s) {
-      const float4 x = p1[s * split_stride], y = p2[s * split_stride];
-      a1.x += x.x; a1.y += x.y; a1.z += x.z; a1.w += x.w;
-      a2.x += y.x; a2.y += y.y; a2.z += y.z; a2.w += y.w;
+    for (int s0 = 0; s0 < splits; s0 += 4) {  // four splits' loads in flight, summed in split order
+      float4 x[4], y[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool ok = s0 + u < splits;
+        x[u] = ok ? __ldcg(p1 + (s0 + u) * split_stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+        y[u] = ok ? __ldcg(p2 + (s0 + u) * split_stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a1.x += x[u].x; a1.y += x[u].y; a1.z += x[u].z; a1.w += x[u].w;
+        a2.x += y[u].x; a2.y += y[u].y; a2.z += y[u].z; a2.w += y[u].w;
+      }
     }
     const float b1 = bias ? bf2f(bias[n1]) : 0.f, b2 = bias ? bf2f(bias[n2]) : 0.f;
     const float v1[4] = {rbf(a1.x + b1), rbf(a1.y + b1), rbf(a1.z + b1), rbf(a1.w + b1)};
@@ -889,10 +924,13 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   }
   if (fkind == FUSE_RESIDUAL_NORM) {
     if (fused) *fused = true;
-    const int vpt = static_cast<int>((N + 1023) / 1024);
+    const int64_t vec = N / 4;  // float4 chunks per row
+    const int threads = static_cast<int>(std::min<int64_t>(1024, (vec + 31) / 32 * 32));
+    const int vpt = static_cast<int>((vec + threads - 1) / threads);
+    if (vpt > 8) return set_error(PL_ERR_CONFIG, "residual+norm reduce: N=%lld too large", (long long)N);
     auto k = vpt <= 1 ? reduce_residual_norm_kernel<1> : vpt <= 2 ? reduce_residual_norm_kernel<2>
            : vpt <= 4 ? reduce_residual_norm_kernel<4> : reduce_residual_norm_kernel<8>;
-    return launch_k("reduce_residual_norm_kernel", k, dim3(static_cast<unsigned>(T)), dim3(256), 0, st,
+    return launch_k("reduce_residual_norm_kernel", k, dim3(static_cast<unsigned>(T)), dim3(threads), 0, st,
                     a.partial, a.splits, a.T, a.N, C, ldc, fuse->norm_w, fuse->eps, fuse->norm_out,
                     fuse->ld_norm);
   }
