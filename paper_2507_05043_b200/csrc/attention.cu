@@ -263,7 +263,7 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
 // holding the newest token waits for the predecessor kernel.
 
 constexpr int PAGE = 64;                 // tokens per KV block
-constexpr int MAX_PAGES_PER_SPLIT = 8;   // <= 512 tokens per split, pages spread evenly
+constexpr int MAX_PAGES_PER_SPLIT = 16;  // <= 1024 tokens per split, pages spread evenly
 constexpr int HALF_TILE = 64 * 128;      // 64 tokens x 64 dims bf16 (one TMA box)
 constexpr int PAGE_BYTES = 4 * HALF_TILE;  // K lo | K hi | V lo | V hi
 constexpr int DEC_THREADS = 160;         // producer warp + 4 consumer warps
@@ -307,27 +307,40 @@ struct DecodeArgs {
   int* counters;
 };
 
-// pages [p0, p0 + np) of item `it`, and the request's page count
-PL_DEV void decode_item(const DecodeArgs& a, int it, int& r, int& kh, int& split, int& p0, int& np,
-                        int& n_pages, int& ctx) {
-  split = it % a.nsplit;
-  kh = (it / a.nsplit) % a.Hkv;
-  r = it / (a.nsplit * a.Hkv);
-  ctx = __ldg(a.ctx_len + r);
-  n_pages = (ctx + PAGE - 1) / PAGE;
-  const int ns_r = max(1, (n_pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
-  const int pps = (n_pages + ns_r - 1) / ns_r;
-  p0 = split * pps;
-  np = max(0, min(n_pages, p0 + pps) - p0);
+// Geometry of item `it` given its request's context length: pages [p0, p0 + np)
+// of request r, kv head kh, split `split`; n_pages = the request's page count.
+struct ItemGeom {
+  int r, kh, split, p0, np, n_pages, ctx;
+};
+PL_DEV ItemGeom decode_geom(const DecodeArgs& a, int it, int ctx) {
+  ItemGeom g;
+  g.split = it % a.nsplit;
+  g.kh = (it / a.nsplit) % a.Hkv;
+  g.r = it / (a.nsplit * a.Hkv);
+  g.ctx = ctx;
+  g.n_pages = (ctx + PAGE - 1) / PAGE;
+  const int ns_r = max(1, (g.n_pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
+  const int pps = (g.n_pages + ns_r - 1) / ns_r;
+  g.p0 = g.split * pps;
+  g.np = max(0, min(g.n_pages, g.p0 + pps) - g.p0);
+  return g;
+}
+
+PL_DEV int atomic_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
 // Persistent: 2 CTAs per SM walk the (request, kv head, split) items.  Warp 0 is
-// the producer: per item it fetches the geometry and the (<= 8) block-table
-// entries with one warp-wide load, then streams q (G rows, 1-D bulk copies into a
-// 2-slot ring together with the item geometry) and the K/V pages (4 TMA boxes
-// each) through a STAGES-deep ring.  Warps 1-4 never touch global memory until
-// the output: S = Q K^T and O += P V on m16n8k16 tensor cores with Q = the GQA
-// group padded to 16 rows, per-warp online softmax, warps merged in shared memory.
+// the producer, one item ahead: the context lengths of all of the CTA's items
+// come in one warp-wide load, the next item's block-table entries (<= 8, one per
+// lane) load while the current item's pages stream, and the next item's q (G
+// rows, 1-D bulk copies into a 2-slot ring, with the item geometry) is issued
+// before the current item's pages.  K/V pages (4 TMA boxes each) go through a
+// STAGES-deep ring.  Warps 1-4 never touch global memory until the output:
+// S = Q K^T and O += P V on m16n8k16 tensor cores with Q = the GQA group padded
+// to 16 rows, per-warp online softmax, warps merged in shared memory.
 template <int G>
 __global__ void __launch_bounds__(DEC_THREADS, 2)
     attn_decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -367,89 +380,119 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
 
   if (warp == 0) {
     // ------------------------------------------------------- producer warp
+    if (blockIdx.x >= n_items) {
+      if (lane == 0) pdl_wait();
+      return;
+    }
     const uint64_t pol = policy_evict_first();
     int stage = 0, qs = 0;
     uint32_t phase = 0, qphase = 0;
-    bool waited = false;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      int r, kh, split, p0, np, n_pages, ctx;
-      decode_item(args, it, r, kh, split, p0, np, n_pages, ctx);
-      const int32_t* bt = args.block_table + static_cast<int64_t>(r) * args.max_blocks;
-      const int mine = lane < np ? __ldg(bt + p0 + lane) : 0;  // np <= MAX_PAGES_PER_SPLIT
-      int pg[MAX_PAGES_PER_SPLIT];
-#pragma unroll
-      for (int i = 0; i < MAX_PAGES_PER_SPLIT; ++i) pg[i] = __shfl_sync(0xffffffffu, mine, i);
-      if (lane == 0) {
-        // pages complete before this step stream ahead of griddepcontrol.wait; the page
-        // holding the newest token (the request's last) and q come from the predecessor
-        const int cold = np - (p0 + np == n_pages ? 1 : 0);
-        const int pre = waited ? 0 : min(cold, STAGES);
-#pragma unroll
-        for (int i = 0; i < MAX_PAGES_PER_SPLIT; ++i) {
-          if (i == pre) {
-            if (!waited) {
-              pdl_wait();
-              waited = true;
-            }
-            mbar_wait(&qempty[qs], qphase ^ 1);
-            info[qs] = ItemInfo{r, kh, split, p0, np, ctx, 0, 0};
-            uint8_t* qd = smem + L::Q + qs * G * Q_PITCH;
-            const __nv_bfloat16* qsrc = args.q + static_cast<int64_t>(r) * args.ldq + kh * G * HD;
-            mbar_arrive_expect_tx(&qfull[qs], G * HD * 2);
-#pragma unroll
-            for (int g = 0; g < G; ++g) bulk_load(qd + g * Q_PITCH, qsrc + g * HD, HD * 2, &qfull[qs]);
-            if (++qs == Q_SLOTS) {
-              qs = 0;
-              qphase ^= 1;
-            }
-          }
-          if (i < np) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            const int row0 = (pg[i] * args.Hkv + kh) * PAGE;
-            uint8_t* dst = smem + stage * PAGE_BYTES;
-            mbar_arrive_expect_tx(&full[stage], PAGE_BYTES);
-            tma_load_2d(dst, &tmK, &full[stage], 0, row0, pol);
-            tma_load_2d(dst + HALF_TILE, &tmK, &full[stage], 64, row0, pol);
-            tma_load_2d(dst + 2 * HALF_TILE, &tmV, &full[stage], 0, row0, pol);
-            tma_load_2d(dst + 3 * HALF_TILE, &tmV, &full[stage], 64, row0, pol);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-        }
+    // context lengths of this CTA's items k = 0..31: lane k holds item blockIdx.x + k*grid
+    int ctx_batch = 0, batch_base = -1;
+    auto ctx_of = [&](int k) -> int {  // warp-collective
+      if ((k & ~31) != batch_base) {
+        batch_base = k & ~31;
+        const int itl = blockIdx.x + (batch_base + lane) * gridDim.x;
+        ctx_batch = itl < n_items ? __ldg(args.ctx_len + itl / (args.nsplit * args.Hkv)) : 0;
       }
-      __syncwarp();
+      return __shfl_sync(0xffffffffu, ctx_batch, k & 31);
+    };
+    auto bt_of = [&](const ItemGeom& g) -> int {  // lane i: page p0 + i (warp-collective)
+      return lane < g.np ? __ldg(args.block_table + static_cast<int64_t>(g.r) * args.max_blocks + g.p0 + lane)
+                         : 0;
+    };
+    auto issue_q = [&](const ItemGeom& g) {  // lane 0
+      mbar_wait(&qempty[qs], qphase ^ 1);
+      info[qs] = ItemInfo{g.r, g.kh, g.split, g.p0, g.np, g.ctx, 0, 0};
+      uint8_t* qd = smem + L::Q + qs * G * Q_PITCH;
+      const __nv_bfloat16* qsrc = args.q + static_cast<int64_t>(g.r) * args.ldq + g.kh * G * HD;
+      mbar_arrive_expect_tx(&qfull[qs], G * HD * 2);
+#pragma unroll
+      for (int h = 0; h < G; ++h) bulk_load(qd + h * Q_PITCH, qsrc + h * HD, HD * 2, &qfull[qs]);
+      if (++qs == Q_SLOTS) {
+        qs = 0;
+        qphase ^= 1;
+      }
+    };
+    auto issue_page = [&](int page, int kh) {  // lane 0
+      mbar_wait(&empty[stage], phase ^ 1);
+      const int row0 = (page * args.Hkv + kh) * PAGE;
+      uint8_t* dst = smem + stage * PAGE_BYTES;
+      mbar_arrive_expect_tx(&full[stage], PAGE_BYTES);
+      tma_load_2d(dst, &tmK, &full[stage], 0, row0, pol);
+      tma_load_2d(dst + HALF_TILE, &tmK, &full[stage], 64, row0, pol);
+      tma_load_2d(dst + 2 * HALF_TILE, &tmV, &full[stage], 0, row0, pol);
+      tma_load_2d(dst + 3 * HALF_TILE, &tmV, &full[stage], 64, row0, pol);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    };
+
+    // first item: pages complete before this step stream ahead of griddepcontrol.wait;
+    // the page holding the newest token (the request's last) and q come from the predecessor
+    ItemGeom cur = decode_geom(args, blockIdx.x, ctx_of(0));
+    int cur_bt = bt_of(cur);
+    int pre = 0;
+    {
+      const int cold = cur.np - (cur.p0 + cur.np == cur.n_pages ? 1 : 0);
+      pre = max(0, min(cold, STAGES));
+      for (int i = 0; i < pre; ++i) {
+        const int pg = __shfl_sync(0xffffffffu, cur_bt, i);
+        if (lane == 0) issue_page(pg, cur.kh);
+      }
+      if (lane == 0) {
+        pdl_wait();
+        issue_q(cur);
+      }
     }
-    if (lane == 0 && !waited) pdl_wait();
+    for (int k = 0;; ++k) {
+      const int it = blockIdx.x + k * gridDim.x;
+      const int nx = it + gridDim.x;
+      const bool has_next = nx < n_items;
+      ItemGeom nxt{};
+      int nxt_bt = 0;
+      if (has_next) {
+        nxt = decode_geom(args, nx, ctx_of(k + 1));
+        nxt_bt = bt_of(nxt);  // in flight while this item's pages stream
+        if (lane == 0) issue_q(nxt);
+      }
+      for (int i = pre; i < cur.np; ++i) {
+        const int pg = __shfl_sync(0xffffffffu, cur_bt, i);
+        if (lane == 0) issue_page(pg, cur.kh);
+      }
+      pre = 0;
+      if (!has_next) break;
+      cur = nxt;
+      cur_bt = nxt_bt;
+    }
     return;
   }
 
   // --------------------------------------------------------- consumers (warps 1-4)
+  // Transposed tiles ("swap AB" for small GQA groups): S^T = K Q^T with M = 16
+  // tokens, N = 8 query heads (the group, zero-padded), K = hd; O^T = V^T P^T with
+  // M = 16 head dims, N = 8 heads, K = 16 tokens.  Half the MMAs and half the
+  // accumulator registers of the Q-rows-as-M form when G <= 8.
   const int cw = warp - 1;  // consumer warp: tokens [16 cw, 16 cw + 16) of every page
   const int ct = threadIdx.x - 32;
   const int mi = lane >> 3, ri = lane & 7;
+  const int g8 = lane >> 2, t4 = lane & 3;  // fragment row group / column pair
   int stage = 0, qs = 0;
   uint32_t phase = 0, qphase = 0;
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
     mbar_wait(&qfull[qs], qphase);
     const ItemInfo inf = info[qs];
     const int r = inf.r, kh = inf.kh, split = inf.split, p0 = inf.p0, np = inf.np, ctx = inf.ctx;
-    // Q fragments (rows = the group's heads, zero-padded to 16)
-    uint32_t qf[8][4];
+    // B fragments of Q^T: head g8 (zero when g8 >= G), dims 16 ks + 2 t4 (+8)
+    uint32_t qf[8][2];
     {
-      const uint8_t* qb = smem + L::Q + qs * G * Q_PITCH;
-      const int r0 = lane >> 2, r1 = r0 + 8;
+      const uint8_t* qb = smem + L::Q + qs * G * Q_PITCH + g8 * Q_PITCH;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        const int c = (ks * 16 + (lane & 3) * 2) * 2;
-        auto ld = [&](int row, int off) -> uint32_t {
-          return row < G ? *reinterpret_cast<const uint32_t*>(qb + row * Q_PITCH + off) : 0u;
-        };
-        qf[ks][0] = ld(r0, c);
-        qf[ks][1] = ld(r1, c);
-        qf[ks][2] = ld(r0, c + 16);
-        qf[ks][3] = ld(r1, c + 16);
+        const int off = (ks * 16 + t4 * 2) * 2;
+        qf[ks][0] = g8 < G ? *reinterpret_cast<const uint32_t*>(qb + off) : 0u;
+        qf[ks][1] = g8 < G ? *reinterpret_cast<const uint32_t*>(qb + off + 16) : 0u;
       }
     }
     __syncwarp();
@@ -458,78 +501,69 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
       qs = 0;
       qphase ^= 1;
     }
-    float o[16][4];
+    float o[8][4];  // O^T: dims 16 mt + g8 (+8) x heads 2 t4 (+1)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+    for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};  // heads 2 t4, 2 t4 + 1
 
     for (int i = 0; i < np; ++i) {
       mbar_wait(&full[stage], phase);
       const uint32_t kb = smem_u32(smem + stage * PAGE_BYTES);
       const uint32_t vb = kb + 2 * HALF_TILE;
-      float s[2][4];
-#pragma unroll
-      for (int t = 0; t < 2; ++t) s[t][0] = s[t][1] = s[t][2] = s[t][3] = 0.f;
+      float s[4] = {0.f, 0.f, 0.f, 0.f};  // tokens g8, g8+8 x heads 2 t4, 2 t4 + 1
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        uint32_t b0, b1, b2, b3;
-        ldmatrix_x4(b0, b1, b2, b3, kv_addr(kb, cw * 16 + (mi >> 1) * 8 + ri, ks * 2 + (mi & 1)));
-        mma_bf16_16816(s[0], qf[ks], b0, b1);
-        mma_bf16_16816(s[1], qf[ks], b2, b3);
+        uint32_t a[4];
+        ldmatrix_x4(a[0], a[1], a[2], a[3], kv_addr(kb, cw * 16 + (mi & 1) * 8 + ri, ks * 2 + (mi >> 1)));
+        mma_bf16_16816(s, a, qf[ks][0], qf[ks][1]);
       }
       const int tok0 = (p0 + i) * PAGE + cw * 16;
-      float mx[2] = {-INFINITY, -INFINITY};
+      if (tok0 + 16 <= ctx) {
 #pragma unroll
-      for (int t = 0; t < 2; ++t)
+        for (int e = 0; e < 4; ++e) s[e] *= args.scale_log2;
+      } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = tok0 + t * 8 + (lane & 3) * 2 + (e & 1);
-          const float v = (j < ctx) ? s[t][e] * args.scale_log2 : -INFINITY;
-          s[t][e] = v;
-          mx[e >> 1] = fmaxf(mx[e >> 1], v);
-        }
-      float corr[2], rs[2] = {0.f, 0.f};
+        for (int e = 0; e < 4; ++e) s[e] = (tok0 + g8 + (e >> 1) * 8 < ctx) ? s[e] * args.scale_log2 : -INFINITY;
+      }
+      float corr[2], rs[2];
 #pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 1));
-        mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 2));
-        const float m_new = fmaxf(m_r[hr], mx[hr]);
-        corr[hr] = (m_new == -INFINITY) ? 1.f : exp2f(m_r[hr] - m_new);
-        m_r[hr] = m_new;
+      for (int h = 0; h < 2; ++h) {  // reduce over the 16 tokens: lanes sharing t4
+        float mx = fmaxf(s[h], s[h + 2]);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        const float m_new = fmaxf(m_r[h], mx);
+        corr[h] = (m_new == -INFINITY) ? 1.f : exp2f(m_r[h] - m_new);
+        m_r[h] = m_new;
+        const float pa = (m_new == -INFINITY) ? 0.f : exp2f(s[h] - m_new);
+        const float pb = (m_new == -INFINITY) ? 0.f : exp2f(s[h + 2] - m_new);
+        s[h] = pa;
+        s[h + 2] = pb;
+        rs[h] = pa + pb;
       }
 #pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int hr = e >> 1;
-          const float p = (m_r[hr] == -INFINITY) ? 0.f : exp2f(s[t][e] - m_r[hr]);
-          s[t][e] = p;
-          rs[hr] += p;
-        }
-#pragma unroll
-      for (int hr = 0; hr < 2; ++hr) {
-        rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 1);
-        rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 2);
-        l_r[hr] = l_r[hr] * corr[hr] + rs[hr];
+      for (int h = 0; h < 2; ++h) {
+        rs[h] += __shfl_xor_sync(0xffffffffu, rs[h], 4);
+        rs[h] += __shfl_xor_sync(0xffffffffu, rs[h], 8);
+        rs[h] += __shfl_xor_sync(0xffffffffu, rs[h], 16);
+        l_r[h] = l_r[h] * corr[h] + rs[h];
       }
 #pragma unroll
-      for (int nt = 0; nt < 16; ++nt) {
-        o[nt][0] *= corr[0];
-        o[nt][1] *= corr[0];
-        o[nt][2] *= corr[1];
-        o[nt][3] *= corr[1];
+      for (int mt = 0; mt < 8; ++mt) {
+        o[mt][0] *= corr[0];
+        o[mt][1] *= corr[1];
+        o[mt][2] *= corr[0];
+        o[mt][3] *= corr[1];
       }
-      uint32_t a[4];
-      a[0] = pack_bf16x2(s[0][0], s[0][1]);
-      a[1] = pack_bf16x2(s[0][2], s[0][3]);
-      a[2] = pack_bf16x2(s[1][0], s[1][1]);
-      a[3] = pack_bf16x2(s[1][2], s[1][3]);
+      // P^T as the B operand: transpose the two 8x8 (token x head) blocks in registers
+      uint32_t pb0 = pack_bf16x2(s[0], s[1]), pb1 = pack_bf16x2(s[2], s[3]);
+      asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %0;" : "+r"(pb0));
+      asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %0;" : "+r"(pb1));
 #pragma unroll
-      for (int nt = 0; nt < 16; nt += 2) {
-        uint32_t b0, b1, b2, b3;
-        ldmatrix_x4_trans(b0, b1, b2, b3, kv_addr(vb, cw * 16 + (mi & 1) * 8 + ri, nt + (mi >> 1)));
-        mma_bf16_16816(o[nt], a, b0, b1);
-        mma_bf16_16816(o[nt + 1], a, b2, b3);
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t a[4];
+        ldmatrix_x4_trans(a[0], a[1], a[2], a[3], kv_addr(vb, cw * 16 + (mi >> 1) * 8 + ri, mt * 2 + (mi & 1)));
+        mma_bf16_16816(o[mt], a, pb0, pb1);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
@@ -539,20 +573,19 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
       }
     }
 
-    // merge the four consumer warps (rows >= G are padding)
+    // merge the four consumer warps (heads >= G are padding)
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      const int row = (lane >> 2) + hr * 8;
-      if (row < G) {
-        if ((lane & 3) == 0) {
-          red_m[cw * G + row] = m_r[hr];
-          red_l[cw * G + row] = l_r[hr];
+    for (int h = 0; h < 2; ++h) {
+      const int head = t4 * 2 + h;
+      if (head < G) {
+        if (g8 == 0) {
+          red_m[cw * G + head] = m_r[h];
+          red_l[cw * G + head] = l_r[h];
         }
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt) {
-          const int col = nt * 8 + (lane & 3) * 2;
-          *reinterpret_cast<float2*>(&red_o[(cw * G + row) * HD + col]) =
-              make_float2(o[nt][hr * 2], o[nt][hr * 2 + 1]);
+        for (int mt = 0; mt < 8; ++mt) {
+          red_o[(cw * G + head) * HD + mt * 16 + g8] = o[mt][h];
+          red_o[(cw * G + head) * HD + mt * 16 + g8 + 8] = o[mt][h + 2];
         }
       }
     }
@@ -583,13 +616,14 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
       }
     }
     if (nsplit > 1) {
-      // last split of (request, kv head) to finish merges every split in split order
-      __threadfence();
+      // last split of (request, kv head) to finish merges every split in split order;
+      // one acq_rel atomic orders this CTA's partials (published to thread 0 by the
+      // barrier) before the arrival, and the merger's loads after it
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (ct == 0) *last_flag = atomicAdd(&args.counters[r * args.Hkv + kh], 1) == nsplit - 1;
+      if (ct == 0)
+        *last_flag = atomic_add_acq_rel_gpu(&args.counters[r * args.Hkv + kh], 1) == nsplit - 1;
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*last_flag) {
-        __threadfence();
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const int head = kh * G + g;

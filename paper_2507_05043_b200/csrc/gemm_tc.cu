@@ -14,7 +14,7 @@
 //   !SWAP (prefill): tokens are the A operand (M = 128 rows), features are N = 256.
 //
 // Persistent and warp-specialized (192 threads, one CTA per SM): warp 0 lane 0
-// = TMA producer running a STAGES-deep smem ring continuously across work items,
+// = TMA producer running the A and B smem rings continuously across work items,
 // warp 1 = TMEM allocator + MMA issuer (lane 0), warps 2-5 = epilogue, warp w
 // owning TMEM lanes [32(w%4), +32).  The accumulator is double-buffered in
 // TMEM so the epilogue of item i overlaps the main loop of item i+1.
@@ -67,24 +67,27 @@ struct GemmArgs {
 
 // Decode tiles (BN <= 128) run 2 CTAs per SM with a shallower ring each (two
 // independent epilogues per SM); BN = 256 tiles run one CTA per SM.
-template <int BN, int CTAS = (BN <= 128 ? 2 : 1)>
-struct GemmCfg {
-  static constexpr int STAGE_BYTES = A_TILE_BYTES + BN * BK * 2;
-  static constexpr int CTAS_PER_SM = CTAS;
-  static constexpr int BUDGET = CTAS_PER_SM == 2 ? 100 * 1024 : 196 * 1024;
-  static constexpr int STAGES = BUDGET / STAGE_BYTES;
-};
-
-template <int BN, int CTAS>
+//
+// Two rings: A tiles and B tiles have their own depth.  In the decode (SWAP)
+// orientation A = weights streamed once from HBM and B = the activations,
+// re-read per weight tile from L2 (short latency): the activation ring is 3
+// deep and every other byte of shared memory holds weights in flight -- the
+// kernel is latency-bound on HBM, so weight bytes in flight set its speed.
+// The producer issues B block k only (AS - BS) blocks behind A block k.
+template <int BN, bool SWAP, int CTAS>
 struct GemmSmem {
   static constexpr int B_TILE_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_TILE_BYTES + B_TILE_BYTES;
-  static constexpr int STAGES = GemmCfg<BN, CTAS>::STAGES;
-  static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
-  // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem slot + flag
-  static constexpr int SCRATCH_OFFSET = BAR_OFFSET + 8 * (2 * STAGES + 4) + 16;
+  static constexpr int BUDGET = CTAS == 2 ? 104 * 1024 : 200 * 1024;
+  static constexpr int BS = SWAP ? 3 : BUDGET / (A_TILE_BYTES + B_TILE_BYTES);
+  static constexpr int AS = SWAP ? (BUDGET - BS * B_TILE_BYTES) / A_TILE_BYTES : BS;
+  static constexpr int LAG = AS - BS;  // A (weights, SWAP) run this many k-blocks ahead of B
+  static constexpr int B_OFFSET = AS * A_TILE_BYTES;
+  static constexpr int BAR_OFFSET = B_OFFSET + BS * B_TILE_BYTES;
+  // fullA[AS], emptyA[AS], fullB[BS], emptyB[BS], tmem_full[2], tmem_empty[2], tmem slot + flag
+  static constexpr int SCRATCH_OFFSET = BAR_OFFSET + 8 * (2 * AS + 2 * BS + 4) + 16;
   static constexpr int SCRATCH_BYTES = 64 * 16 * 4;  // swiglu exchange / argmax partials
   static constexpr int TOTAL = SCRATCH_OFFSET + SCRATCH_BYTES + 1024;  // + alignment slack
+  static_assert(AS >= 2 && BS >= 2 && LAG >= 0, "ring too shallow");
 };
 
 PL_DEV float silu_f(float x) { return x / (1.0f + expf(-x)); }
@@ -104,15 +107,17 @@ template <int BN, bool SWAP, int CTAS>
 __global__ void __launch_bounds__(192, CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs args) {
-  using L = GemmSmem<BN, CTAS>;
-  constexpr int STAGES = L::STAGES;
+  using L = GemmSmem<BN, SWAP, CTAS>;
+  constexpr int AS = L::AS, BS = L::BS;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFFSET);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + L::BAR_OFFSET);
+  uint64_t* emptyA = fullA + AS;
+  uint64_t* fullB = emptyA + AS;
+  uint64_t* emptyB = fullB + BS;
+  uint64_t* tfull = emptyB + BS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* scratch = reinterpret_cast<float*>(smem + L::SCRATCH_OFFSET);
@@ -123,9 +128,13 @@ __global__ void __launch_bounds__(192, CTAS)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -159,52 +168,50 @@ __global__ void __launch_bounds__(192, CTAS)
       const uint64_t pol_x = policy_evict_last();    // activations are re-read per weight tile
       const uint64_t polA = SWAP ? pol_w : pol_x;
       const uint64_t polB = SWAP ? pol_x : pol_w;
-      int stage = 0;
-      uint32_t phase = 0;
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      auto issue_a = [&](int kb, int m_tile) {
+        mbar_wait(&emptyA[sa], pa ^ 1);
+        mbar_arrive_expect_tx(&fullA[sa], A_TILE_BYTES);
+        tma_load_2d(smem + sa * A_TILE_BYTES, &tmA, &fullA[sa], kb * BK, m_tile * BM, polA);
+        if (++sa == AS) {
+          sa = 0;
+          pa ^= 1;
+        }
+      };
+      auto issue_b = [&](int kb, int n_tile) {
+        mbar_wait(&emptyB[sb], pb ^ 1);
+        mbar_arrive_expect_tx(&fullB[sb], L::B_TILE_BYTES);
+        tma_load_2d(smem + L::B_OFFSET + sb * L::B_TILE_BYTES, &tmB, &fullB[sb], kb * BK, n_tile * BN, polB);
+        if (++sb == BS) {
+          sb = 0;
+          pb ^= 1;
+        }
+      };
       bool first = true;
       for (int item = blockIdx.x; item < args.num_items; item += gridDim.x) {
         int m_tile, n_tile, split, kb0, nkb;
         item_coords(item, m_tile, n_tile, split, kb0, nkb);
-        int i = 0;
+        int pre = 0;  // weight blocks issued ahead of the PDL wait
         if (first) {
-          // Weights never depend on the previous kernel: stream the first ring's worth
-          // of weight tiles before waiting on it (PDL), then the activation tiles.
+          // Weights never depend on the previous kernel: fill the weight ring before
+          // waiting on it (PDL), and warm L2 with the weight blocks beyond the ring.
           first = false;
-          const int pre = min(nkb, STAGES);
-          for (; i < pre; ++i) {
-            uint8_t* sa = smem + i * L::STAGE_BYTES;
-            mbar_arrive_expect_tx(&full[i], L::STAGE_BYTES);
-            const int kc = (kb0 + i) * BK;
-            if (SWAP) tma_load_2d(sa, &tmA, &full[i], kc, m_tile * BM, polA);
-            else tma_load_2d(sa + A_TILE_BYTES, &tmB, &full[i], kc, n_tile * BN, polB);
+          pre = min(nkb, SWAP ? AS : BS);
+          for (int j = 0; j < pre; ++j) {
+            if (SWAP) issue_a(kb0 + j, m_tile);
+            else issue_b(kb0 + j, n_tile);
           }
-          // ...and warm L2 with the next weight tiles beyond the ring, so HBM keeps
-          // streaming this kernel's weights while the predecessor drains
           if (SWAP) {
             const int pf_end = min(nkb, pre + args.l2_prefetch);
             for (int j = pre; j < pf_end; ++j) tma_prefetch_l2_2d(&tmA, (kb0 + j) * BK, m_tile * BM);
           }
           pdl_wait();
-          for (int j = 0; j < pre; ++j) {
-            uint8_t* sa = smem + j * L::STAGE_BYTES;
-            const int kc = (kb0 + j) * BK;
-            if (SWAP) tma_load_2d(sa + A_TILE_BYTES, &tmB, &full[j], kc, n_tile * BN, polB);
-            else tma_load_2d(sa, &tmA, &full[j], kc, m_tile * BM, polA);
-          }
-          stage = pre % STAGES;
-          phase = (pre == STAGES) ? 1 : 0;
         }
-        for (; i < nkb; ++i) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * L::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], L::STAGE_BYTES);
-          const int kc = (kb0 + i) * BK;
-          tma_load_2d(sa, &tmA, &full[stage], kc, m_tile * BM, polA);
-          tma_load_2d(sa + A_TILE_BYTES, &tmB, &full[stage], kc, n_tile * BN, polB);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        for (int i = 0; i < nkb + L::LAG; ++i) {
+          if (i < nkb && !(SWAP && i < pre)) issue_a(kb0 + i, m_tile);
+          const int j = i - L::LAG;
+          if (j >= 0 && j < nkb && !(!SWAP && j < pre)) issue_b(kb0 + j, n_tile);
         }
       }
       if (first) pdl_wait();
@@ -214,8 +221,8 @@ __global__ void __launch_bounds__(192, CTAS)
     // ------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, aphase = 0;
+      int sa = 0, sb = 0, acc = 0;
+      uint32_t pa = 0, pb = 0, aphase = 0;
       for (int item = blockIdx.x; item < args.num_items; item += gridDim.x) {
         int m_tile, n_tile, split, kb0, nkb;
         item_coords(item, m_tile, n_tile, split, kb0, nkb);
@@ -223,18 +230,23 @@ __global__ void __launch_bounds__(192, CTAS)
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
         for (int i = 0; i < nkb; ++i) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait(&fullA[sa], pa);
+          mbar_wait(&fullB[sb], pb);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * L::STAGE_BYTES);
-          const uint64_t da = umma_desc_sw128(sa);
-          const uint64_t db = umma_desc_sw128(sa + A_TILE_BYTES);
+          const uint64_t da = umma_desc_sw128(smem_u32(smem + sa * A_TILE_BYTES));
+          const uint64_t db = umma_desc_sw128(smem_u32(smem + L::B_OFFSET + sb * L::B_TILE_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
             umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
-          umma_commit(&empty[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+          umma_commit(&emptyA[sa]);
+          umma_commit(&emptyB[sb]);
+          if (++sa == AS) {
+            sa = 0;
+            pa ^= 1;
+          }
+          if (++sb == BS) {
+            sb = 0;
+            pb ^= 1;
           }
         }
         umma_commit(&tfull[acc]);
@@ -767,7 +779,7 @@ int make_map(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int6
 template <int BN, bool SWAP, int CTAS = (BN <= 128 ? 2 : 1)>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid,
               cudaStream_t st) {
-  constexpr int smem = GemmSmem<BN, CTAS>::TOTAL;
+  constexpr int smem = GemmSmem<BN, SWAP, CTAS>::TOTAL;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, SWAP, CTAS>,
@@ -811,6 +823,11 @@ int make_tma_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, i
 // split keeping >= 4 k-blocks.
 int gemm_num_splits(int64_t N, int64_t K, bool swap) {
   if (!swap) return 1;
+  static const int forced = [] {  // experiments only (scripts/bench_gemm.py --splits)
+    const char* v = getenv("PL_SPLITK_FORCE");
+    return v ? atoi(v) : 0;
+  }();
+  if (forced > 0) return static_cast<int>(std::min<int64_t>(forced, K / BK));
   const int64_t tiles = (N + BM - 1) / BM;
   const int64_t kb = K / BK;
   const int64_t sms = 148;
