@@ -184,6 +184,12 @@ PL_API int64_t pl_stage_workspace_bytes(const pl_stage_config* cfg);
 PL_API int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* layers,
                         void* workspace, int64_t workspace_bytes, void** handle);
 PL_API int32_t pl_stage_forward(void* handle, const pl_microbatch* mb, void* stream);
+/* Repack the stage's projection weights (and lm_head) IN PLACE into pre-swizzled
+ * 16 KB tiles [N/128][K/64] -- the shared-memory image of a 128 x 64 TMA box --
+ * so every weight k-block streams as one contiguous bulk copy.  Weights whose N
+ * is not a multiple of 256 stay row-major.  Synchronizes `stream`; afterwards
+ * the weight buffers are only meaningful to this stage. */
+PL_API int32_t pl_stage_pack_weights(void* handle, void* stream);
 PL_API int32_t pl_stage_destroy(void* handle);
 
 /* Live kernel timing for bench.py: CUDA events around the kernel groups of one

@@ -93,6 +93,7 @@ _SIGS = {
     "pl_stage_workspace_bytes": (i64, [C.POINTER(StageConfig)]),
     "pl_stage_create": (i32, [C.POINTER(StageConfig), C.POINTER(LayerWeights), vp, i64, C.POINTER(vp)]),
     "pl_stage_forward": (i32, [vp, C.POINTER(MicroBatch), vp]),
+    "pl_stage_pack_weights": (i32, [vp, vp]),
     "pl_stage_destroy": (i32, [vp]),
     "pl_stage_probe": (i32, [vp, i32]),
     "pl_stage_probe_read": (i32, [vp, C.POINTER(f32), C.POINTER(i32), i32, C.POINTER(i32)]),

@@ -146,7 +146,8 @@ int32_t pl_attn_decode(const void* q, int64_t ldq, const void* k_cache, const vo
 }
 
 int64_t pl_lmhead_workspace_bytes(int32_t R, int64_t vocab) {
-  return gemm_workspace_bytes(R, vocab, 64, EPI_ARGMAX);
+  // d is not an argument: size for the largest stream-K grid (an upper bound for any d)
+  return gemm_workspace_bytes(R, vocab, int64_t(64) << 12, EPI_ARGMAX);
 }
 
 int32_t pl_lmhead_argmax(const void* h, int64_t ldh, const void* W, int64_t vocab, int32_t d,

@@ -137,6 +137,13 @@ PL_DEV void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes, uint
       : "memory");
 }
 
+// Warm L2 with a contiguous range (no destination, no completion).
+PL_DEV void bulk_prefetch_l2(const void* gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gmem)),
+               "r"(bytes)
+               : "memory");
+}
+
 // Warm L2 with a 2-D tile (no shared-memory destination, no completion).
 PL_DEV void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(

@@ -63,6 +63,75 @@ struct GemmArgs {
   int pmode;
   int l2_prefetch;    // weight k-blocks warmed in L2 beyond the smem ring before the PDL wait
   float2* argmax_ws;  // [N/128 tiles][T] (value, index-as-float-bits)
+  // stream-K (decode / SWAP): CTA c owns the flattened (tile, k-block) iterations
+  // [c*base + min(c, extra), +base + (c < extra)); tiles shared by several CTAs are
+  // reduced by the last arriving CTA from per-piece fp32 slots, in k order.
+  const uint8_t* wp;  // pre-packed weights (pl_pack_weight): 16 KB SW128 tile images, [N/128][K/64]
+  int streamk;
+  int sk_base, sk_extra;
+  float* sk_slots;    // [2 * grid][BM][BN] fp32
+  int* sk_counters;   // [tiles_m], zero between launches (the fixer resets its tile)
+};
+
+// One unit of work: k-blocks [kb0, kb0 + nkb) of output tile (m_tile, n_tile).
+struct Piece {
+  int m_tile, n_tile, split, kb0, nkb;
+  int partial;        // stream-K: the tile is shared with other CTAs
+  int slot;           // stream-K: this piece's fp32 slot
+  int c_first, c_last;  // stream-K: CTAs covering the tile (k order)
+};
+
+PL_DEV int sk_start(const GemmArgs& a, int c) { return c * a.sk_base + min(c, a.sk_extra); }
+PL_DEV int sk_cta_of(const GemmArgs& a, int it) {
+  const int big = a.sk_extra * (a.sk_base + 1);
+  return it < big ? it / (a.sk_base + 1) : a.sk_extra + (it - big) / a.sk_base;
+}
+// slot of CTA c's piece in tile t: its second slot when c's range began in an earlier
+// tile (then the piece is c's last), else its first
+PL_DEV int sk_slot(const GemmArgs& a, int c, int tile) {
+  return (sk_start(a, c) < tile * a.num_kb) ? 2 * c + 1 : 2 * c;
+}
+
+// Walks this CTA's pieces in order (identical in the producer, MMA and epilogue roles).
+struct PieceWalk {
+  int it, end;  // stream-K iteration cursor / item cursor
+  PL_DEV void init(const GemmArgs& a) {
+    if (a.streamk) {
+      it = sk_start(a, blockIdx.x);
+      end = it + a.sk_base + (static_cast<int>(blockIdx.x) < a.sk_extra ? 1 : 0);
+    } else {
+      it = blockIdx.x;
+      end = a.num_items;
+    }
+  }
+  PL_DEV bool next(const GemmArgs& a, Piece& p) {
+    if (it >= end) return false;
+    if (a.streamk) {
+      const int tile = it / a.num_kb;
+      const int k0 = it % a.num_kb;
+      const int k1 = min(a.num_kb, k0 + (end - it));
+      p.m_tile = tile;
+      p.n_tile = 0;
+      p.split = 0;
+      p.kb0 = k0;
+      p.nkb = k1 - k0;
+      p.c_first = sk_cta_of(a, tile * a.num_kb);
+      p.c_last = sk_cta_of(a, tile * a.num_kb + a.num_kb - 1);
+      p.partial = p.c_first != p.c_last;
+      p.slot = sk_slot(a, blockIdx.x, tile);
+      it += k1 - k0;
+    } else {
+      p.split = it % a.splits;
+      const int tile = it / a.splits;
+      p.m_tile = tile % a.tiles_m;
+      p.n_tile = tile / a.tiles_m;
+      p.kb0 = p.split * a.kb_per_split;
+      p.nkb = min(a.num_kb, p.kb0 + a.kb_per_split) - p.kb0;
+      p.partial = 0;
+      it += gridDim.x;
+    }
+    return true;
+  }
 };
 
 // Decode tiles (BN <= 128) run 2 CTAs per SM with a shallower ring each (two
@@ -152,15 +221,6 @@ __global__ void __launch_bounds__(192, CTAS)
   // the residual stream): wait for it before any global write
   if (warp >= 2) pdl_wait();
 
-  auto item_coords = [&](int item, int& m_tile, int& n_tile, int& split, int& kb0, int& nkb) {
-    split = item % args.splits;
-    const int tile = item / args.splits;
-    m_tile = tile % args.tiles_m;
-    n_tile = tile / args.tiles_m;
-    kb0 = split * args.kb_per_split;
-    nkb = min(args.num_kb, kb0 + args.kb_per_split) - kb0;
-  };
-
   if (warp == 0) {
     // ------------------------------------------------------- TMA producer
     if (lane == 0) {
@@ -173,7 +233,11 @@ __global__ void __launch_bounds__(192, CTAS)
       auto issue_a = [&](int kb, int m_tile) {
         mbar_wait(&emptyA[sa], pa ^ 1);
         mbar_arrive_expect_tx(&fullA[sa], A_TILE_BYTES);
-        tma_load_2d(smem + sa * A_TILE_BYTES, &tmA, &fullA[sa], kb * BK, m_tile * BM, polA);
+        if (SWAP && args.wp)  // one contiguous 16 KB copy of the pre-swizzled weight tile
+          bulk_load(smem + sa * A_TILE_BYTES, args.wp + ((int64_t)m_tile * args.num_kb + kb) * A_TILE_BYTES,
+                    A_TILE_BYTES, &fullA[sa]);
+        else
+          tma_load_2d(smem + sa * A_TILE_BYTES, &tmA, &fullA[sa], kb * BK, m_tile * BM, polA);
         if (++sa == AS) {
           sa = 0;
           pa ^= 1;
@@ -182,16 +246,27 @@ __global__ void __launch_bounds__(192, CTAS)
       auto issue_b = [&](int kb, int n_tile) {
         mbar_wait(&emptyB[sb], pb ^ 1);
         mbar_arrive_expect_tx(&fullB[sb], L::B_TILE_BYTES);
-        tma_load_2d(smem + L::B_OFFSET + sb * L::B_TILE_BYTES, &tmB, &fullB[sb], kb * BK, n_tile * BN, polB);
+        if (!SWAP && args.wp) {  // BN = 256 weight rows = packed tiles 2n, 2n+1
+          uint8_t* d = smem + L::B_OFFSET + sb * L::B_TILE_BYTES;
+#pragma unroll
+          for (int h = 0; h < BN / BM; ++h)
+            bulk_load(d + h * A_TILE_BYTES,
+                      args.wp + ((int64_t)(n_tile * (BN / BM) + h) * args.num_kb + kb) * A_TILE_BYTES,
+                      A_TILE_BYTES, &fullB[sb]);
+        } else {
+          tma_load_2d(smem + L::B_OFFSET + sb * L::B_TILE_BYTES, &tmB, &fullB[sb], kb * BK, n_tile * BN, polB);
+        }
         if (++sb == BS) {
           sb = 0;
           pb ^= 1;
         }
       };
       bool first = true;
-      for (int item = blockIdx.x; item < args.num_items; item += gridDim.x) {
-        int m_tile, n_tile, split, kb0, nkb;
-        item_coords(item, m_tile, n_tile, split, kb0, nkb);
+      PieceWalk walk;
+      walk.init(args);
+      Piece pc;
+      while (walk.next(args, pc)) {
+        const int m_tile = pc.m_tile, n_tile = pc.n_tile, kb0 = pc.kb0, nkb = pc.nkb;
         int pre = 0;  // weight blocks issued ahead of the PDL wait
         if (first) {
           // Weights never depend on the previous kernel: fill the weight ring before
@@ -204,7 +279,12 @@ __global__ void __launch_bounds__(192, CTAS)
           }
           if (SWAP) {
             const int pf_end = min(nkb, pre + args.l2_prefetch);
-            for (int j = pre; j < pf_end; ++j) tma_prefetch_l2_2d(&tmA, (kb0 + j) * BK, m_tile * BM);
+            for (int j = pre; j < pf_end; ++j) {
+              if (args.wp)
+                bulk_prefetch_l2(args.wp + ((int64_t)m_tile * args.num_kb + kb0 + j) * A_TILE_BYTES, A_TILE_BYTES);
+              else
+                tma_prefetch_l2_2d(&tmA, (kb0 + j) * BK, m_tile * BM);
+            }
           }
           pdl_wait();
         }
@@ -223,9 +303,11 @@ __global__ void __launch_bounds__(192, CTAS)
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
       int sa = 0, sb = 0, acc = 0;
       uint32_t pa = 0, pb = 0, aphase = 0;
-      for (int item = blockIdx.x; item < args.num_items; item += gridDim.x) {
-        int m_tile, n_tile, split, kb0, nkb;
-        item_coords(item, m_tile, n_tile, split, kb0, nkb);
+      PieceWalk walk;
+      walk.init(args);
+      Piece pc;
+      while (walk.next(args, pc)) {
+        const int nkb = pc.nkb;
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
@@ -264,31 +346,166 @@ __global__ void __launch_bounds__(192, CTAS)
     const int ep = threadIdx.x - 64;              // 0..127
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const int epi = args.epi;
+    int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
     int acc = 0;
     uint32_t aphase = 0;
-    for (int item = blockIdx.x; item < args.num_items; item += gridDim.x) {
-      int m_tile, n_tile, split, kb0, nkb;
-      item_coords(item, m_tile, n_tile, split, kb0, nkb);
+    PieceWalk walk;
+    walk.init(args);
+    Piece pc;
+    while (walk.next(args, pc)) {
+      const int m_tile = pc.m_tile, n_tile = pc.n_tile, split = pc.split;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const uint32_t tcol = tmem + lane_base + acc * BN;
+      auto release_tmem = [&]() {  // accumulator drained: hand the TMEM buffer back
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      };
 
       if constexpr (SWAP) {
         // lane <-> feature n, column <-> token t
         const int n = m_tile * BM + row;
         const int t_base = n_tile * BN;
+        // the tile's final epilogue, accumulator values from `fetch(c0, v[16])`
+        auto final_epi = [&](auto fetch) {
+          if (epi == EPI_SWIGLU) {
+            // rows [0,64) gate, [64,128) up of the same 64 output features
+            const int j = m_tile * 64 + (row & 63);
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float v[16];
+              fetch(c0, v);
+              if (row >= 64) {
+#pragma unroll
+                for (int c = 0; c < 16; ++c) scratch[c * 64 + (row - 64)] = v[c];
+              }
+              epi_sync();
+              if (row < 64) {
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                  const int t = t_base + c0 + c;
+                  if (t < args.T) {
+                    const float g = rbf(v[c]);
+                    const float u = rbf(scratch[c * 64 + row]);
+                    args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(g)) * u);
+                  }
+                }
+              }
+              epi_sync();
+            }
+          } else if (epi == EPI_ARGMAX) {
+            float2* red = reinterpret_cast<float2*>(scratch);  // [4 quarters][16 cols]
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float vv[16];
+              fetch(c0, vv);
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                float v = (n < args.N) ? vv[c] : -INFINITY;
+                int idx = n;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                  const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+                  const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+                  if (ov > v || (ov == v && oi < idx)) {
+                    v = ov;
+                    idx = oi;
+                  }
+                }
+                if (lane == 0) red[quarter * 16 + c] = make_float2(v, __int_as_float(idx));
+              }
+              epi_sync();
+              if (ep < 16) {
+                float2 best = red[ep];
+                for (int q = 1; q < 4; ++q) {
+                  const float2 o = red[q * 16 + ep];
+                  if (o.x > best.x || (o.x == best.x && __float_as_int(o.y) < __float_as_int(best.y)))
+                    best = o;
+                }
+                const int t = t_base + c0 + ep;
+                if (t < args.T) args.argmax_ws[(int64_t)m_tile * args.T + t] = best;
+              }
+              epi_sync();
+            }
+          } else {
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float v[16];
+              fetch(c0, v);
+              if (n < args.N) {
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                  const int t = t_base + c0 + c;
+                  if (t < args.T) store_out(args, epi, t, n, v[c]);
+                }
+              }
+            }
+          }
+        };
+        auto fetch_tmem = [&](int c0, float (&v)[16]) {
+          uint32_t r[16];
+          tmem_ld16(tcol + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(r[c]);
+        };
+
+        if (args.streamk && pc.partial) {
+          // stream-K piece of a shared tile: fp32 slot, then the last arriver reduces
+          float* sp = args.sk_slots + (int64_t)pc.slot * (BM * BN) + row * BN;
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16];
+            fetch_tmem(c0, v);
+            float4* d = reinterpret_cast<float4*>(sp + c0);
+#pragma unroll
+            for (int c = 0; c < 16; c += 4) d[c / 4] = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+          }
+          release_tmem();
+          epi_sync();
+          if (ep == 0) {
+            int old;
+            asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;"
+                         : "=r"(old)
+                         : "l"(args.sk_counters + m_tile), "r"(1)
+                         : "memory");
+            *sk_flag = old == pc.c_last - pc.c_first;
+          }
+          epi_sync();
+          if (*sk_flag) {
+            const int tile = m_tile;
+            auto fetch_slots = [&](int c0, float (&v)[16]) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) v[c] = 0.f;
+              for (int cc = pc.c_first; cc <= pc.c_last; ++cc) {  // k order
+                const float4* p = reinterpret_cast<const float4*>(
+                    args.sk_slots + (int64_t)sk_slot(args, cc, tile) * (BM * BN) + row * BN + c0);
+#pragma unroll
+                for (int c = 0; c < 16; c += 4) {
+                  const float4 x = __ldcg(p + c / 4);
+                  v[c] += x.x;
+                  v[c + 1] += x.y;
+                  v[c + 2] += x.z;
+                  v[c + 3] += x.w;
+                }
+              }
+            };
+            final_epi(fetch_slots);
+            if (ep == 0) args.sk_counters[tile] = 0;
+          }
+          continue;
+        }
         if (args.splits > 1 && args.pmode == 1) {
           // feature-contiguous partials [split][T][N] (per-token fused reductions)
           for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t r[16];
-            tmem_ld16(tcol + c0, r);
-            tmem_ld_wait();
+            float v[16];
+            fetch_tmem(c0, v);
             if (n < args.N) {
 #pragma unroll
               for (int c = 0; c < 16; ++c) {
                 const int t = t_base + c0 + c;
-                if (t < args.T)
-                  args.partial[((int64_t)split * args.T + t) * args.N + n] = __uint_as_float(r[c]);
+                if (t < args.T) args.partial[((int64_t)split * args.T + t) * args.N + n] = v[c];
               }
             }
           }
@@ -296,89 +513,16 @@ __global__ void __launch_bounds__(192, CTAS)
           // partials are token-contiguous per feature row: [split][N][Tp]
           float* prow = args.partial + ((int64_t)split * args.N + n) * args.Tp + t_base;
           for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t r[16];
-            tmem_ld16(tcol + c0, r);
-            tmem_ld_wait();
+            float v[16];
+            fetch_tmem(c0, v);
             if (n < args.N && t_base + c0 < args.T) {
               float4* dst = reinterpret_cast<float4*>(prow + c0);
 #pragma unroll
-              for (int c = 0; c < 16; c += 4)
-                dst[c / 4] = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
-                                         __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+              for (int c = 0; c < 16; c += 4) dst[c / 4] = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
             }
-          }
-        } else if (epi == EPI_SWIGLU) {
-          // rows [0,64) gate, [64,128) up of the same 64 output features
-          const int j = m_tile * 64 + (row & 63);
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t r[16];
-            tmem_ld16(tcol + c0, r);
-            tmem_ld_wait();
-            if (row >= 64) {
-#pragma unroll
-              for (int c = 0; c < 16; ++c) scratch[c * 64 + (row - 64)] = __uint_as_float(r[c]);
-            }
-            epi_sync();
-            if (row < 64) {
-#pragma unroll
-              for (int c = 0; c < 16; ++c) {
-                const int t = t_base + c0 + c;
-                if (t < args.T) {
-                  const float g = rbf(__uint_as_float(r[c]));
-                  const float u = rbf(scratch[c * 64 + row]);
-                  args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(g)) * u);
-                }
-              }
-            }
-            epi_sync();
-          }
-        } else if (epi == EPI_ARGMAX) {
-          float2* red = reinterpret_cast<float2*>(scratch);  // [4 quarters][16 cols]
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t r[16];
-            tmem_ld16(tcol + c0, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-              float v = (n < args.N) ? __uint_as_float(r[c]) : -INFINITY;
-              int idx = n;
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-                if (ov > v || (ov == v && oi < idx)) {
-                  v = ov;
-                  idx = oi;
-                }
-              }
-              if (lane == 0) red[quarter * 16 + c] = make_float2(v, __int_as_float(idx));
-            }
-            epi_sync();
-            if (ep < 16) {
-              float2 best = red[ep];
-              for (int q = 1; q < 4; ++q) {
-                const float2 o = red[q * 16 + ep];
-                if (o.x > best.x || (o.x == best.x && __float_as_int(o.y) < __float_as_int(best.y)))
-                  best = o;
-              }
-              const int t = t_base + c0 + ep;
-              if (t < args.T) args.argmax_ws[(int64_t)m_tile * args.T + t] = best;
-            }
-            epi_sync();
           }
         } else {
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t r[16];
-            tmem_ld16(tcol + c0, r);
-            tmem_ld_wait();
-            if (n < args.N) {
-#pragma unroll
-              for (int c = 0; c < 16; ++c) {
-                const int t = t_base + c0 + c;
-                if (t < args.T) store_out(args, epi, t, n, __uint_as_float(r[c]));
-              }
-            }
-          }
+          final_epi(fetch_tmem);
         }
       } else {
         // lane <-> token t, column <-> feature n   (splits == 1 on this path)
@@ -439,14 +583,7 @@ __global__ void __launch_bounds__(192, CTAS)
           }
         }
       }
-      // accumulator drained: hand the TMEM buffer back to the MMA warp
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        aphase ^= 1;
-      }
+      release_tmem();
 
     }
   }
@@ -841,10 +978,39 @@ int gemm_num_splits(int64_t N, int64_t K, bool swap) {
   return best;
 }
 
-// Workspace = split-K partials [splits][N][Tp] fp32, or argmax partials [tiles][T].
+// Stream-K (decode / SWAP path) is opt-in (PL_STREAMK=1): at 296 CTAs the pieces of
+// the small projections are a few k-blocks and the serial last-arriver fix-up costs
+// more than the balance it buys.  Default: uniform split-K + parallel reduce kernels.
+bool streamk_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("PL_STREAMK");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+// Stream-K grid: a constant (two CTAs per SM) so piece boundaries -- and therefore
+// every token's summation order -- depend on (N, K) only, never on T.
+int64_t sk_grid(int64_t N, int64_t K) {
+  const int64_t total = ((N + BM - 1) / BM) * (K / BK);
+  return std::min<int64_t>(2 * num_sms(), total);
+}
+
+// Tile counters sit at the same offset for every stream-K GEMM sharing a workspace
+// (the fixer of each tile zeroes its counter, so they stay zero between launches).
+constexpr int64_t SK_COUNTER_BYTES = 64 * 1024;  // up to 16384 weight tiles
+
+// Workspace (SWAP):  stream-K  [tile counters | argmax partials | 2*grid fp32 slots]
+//                    split-K   [splits][N][Tp] fp32 partials, or argmax partials [tiles][T]
 int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi) {
   const bool swap = use_swap(T, epi);
-  if (epi == EPI_ARGMAX) return ((N + BM - 1) / BM) * T * 8;
+  const int64_t tiles = (N + BM - 1) / BM;
+  const int64_t argmax = epi == EPI_ARGMAX ? align256(tiles * T * 8) : 0;
+  if (swap && streamk_enabled()) {
+    const int64_t bn = swap_bn(T);
+    return SK_COUNTER_BYTES + argmax + 2 * sk_grid(N, K) * BM * bn * 4;
+  }
+  if (epi == EPI_ARGMAX) return tiles * T * 8;
   const int splits = gemm_num_splits(N, K, swap);
   if (splits <= 1) return 0;
   const int64_t bn = swap_bn(T);
@@ -856,7 +1022,7 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
                 const __nv_bfloat16* bias, __nv_bfloat16* C, int64_t ldc,
                 const __nv_bfloat16* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,
                 int epi, void* ws, int64_t ws_bytes, int64_t* argmax_out, cudaStream_t st,
-                const FusedEpi* fuse, bool* fused) {
+                const FusedEpi* fuse, bool* fused, bool w_packed) {
   if (fused) *fused = false;
   if (T <= 0) return PL_OK;
   if (K % BK != 0 || N <= 0 || K <= 0)
@@ -876,6 +1042,11 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   GemmArgs a{};
   a.T = static_cast<int>(T);
   a.N = static_cast<int>(N);
+  if (w_packed) {
+    if (N % 256 || ldw != K)
+      return set_error(PL_ERR_CONFIG, "gemm: packed weights need N %% 256 == 0 and ldw == K");
+    a.wp = reinterpret_cast<const uint8_t*>(W);
+  }
   a.num_kb = static_cast<int>(K / BK);
   a.epi = epi;
   a.C = C;
@@ -883,20 +1054,22 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   a.bias = bias;
   a.residual = residual;
   a.ldr = ldr;
-  a.splits = (epi == EPI_ARGMAX) ? 1 : gemm_num_splits(N, K, swap);
+  const bool sk = swap && streamk_enabled();
+  a.splits = (epi == EPI_ARGMAX || sk) ? 1 : gemm_num_splits(N, K, swap);
   a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
   const int bn = swap ? swap_bn(T) : 256;
   a.tiles_m = static_cast<int>(swap ? (N + BM - 1) / BM : (T + BM - 1) / BM);
   const int tiles_n = static_cast<int>(swap ? (T + bn - 1) / bn : (N + bn - 1) / bn);
   a.num_items = a.tiles_m * tiles_n * a.splits;
   a.Tp = tiles_n * bn;
-  // the fused epilogues only apply on the split-K path (their reduction is the epilogue)
-  const int fkind = (fuse && a.splits > 1 && swap) ? fuse->kind : FUSE_NONE;
+  // split-K: the fused epilogues are the partial reduction kernels; stream-K: the GEMM
+  // writes final values and the fusion's second half runs as its own small kernel
+  const int fkind = (fuse && swap && (a.splits > 1 || sk)) ? fuse->kind : FUSE_NONE;
   if (fkind == FUSE_RESIDUAL_NORM && (epi != EPI_RESIDUAL || N > 8192 || N % 4))
     return set_error(PL_ERR_CONFIG, "gemm: residual+norm fusion needs a RESIDUAL GEMM, N <= 8192");
   if (fkind == FUSE_QKV_ROPE && (epi != EPI_STORE && epi != EPI_BIAS))
     return set_error(PL_ERR_CONFIG, "gemm: qkv+rope fusion needs a STORE/BIAS GEMM");
-  a.pmode = fkind == FUSE_RESIDUAL_NORM ? 1 : 0;
+  a.pmode = (fkind == FUSE_RESIDUAL_NORM && !sk) ? 1 : 0;
   // L2 warm-up only for weights that comfortably fit the 126 MB L2 (PL_L2PF overrides)
   static const int l2pf = [] { const char* v = getenv("PL_L2PF"); return v ? atoi(v) : 16; }();
   a.l2_prefetch = (swap && N * K * 2 <= (64ll << 20)) ? l2pf : 0;
@@ -904,15 +1077,31 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   if (need > 0 && (ws_bytes < need || !ws))
     return set_error(PL_ERR_CONFIG, "gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
                      (long long)need);
-  if (epi == EPI_ARGMAX) {
-    a.argmax_ws = reinterpret_cast<float2*>(ws);
-  } else if (a.splits > 1) {
-    a.partial = reinterpret_cast<float*>(ws);
-  }
+  int grid;
   // PL_GEMM_WIDE=1: one CTA per SM with a deep (~196 KB) ring instead of two shallower ones
   static const bool wide = [] { const char* v = getenv("PL_GEMM_WIDE"); return v && v[0] == '1'; }();
-  const int per_sm = (swap && bn <= 128 && !wide) ? 2 : 1;
-  const int grid = std::min(a.num_items, num_sms() * per_sm);
+  if (sk) {
+    if (a.tiles_m * 4 > SK_COUNTER_BYTES) return set_error(PL_ERR_CONFIG, "gemm: N too large");
+    uint8_t* w8 = static_cast<uint8_t*>(ws);
+    const int64_t argmax_bytes = epi == EPI_ARGMAX ? align256(a.tiles_m * T * 8) : 0;
+    a.sk_counters = reinterpret_cast<int*>(w8);
+    if (epi == EPI_ARGMAX) a.argmax_ws = reinterpret_cast<float2*>(w8 + SK_COUNTER_BYTES);
+    a.sk_slots = reinterpret_cast<float*>(w8 + SK_COUNTER_BYTES + argmax_bytes);
+    const int64_t total = static_cast<int64_t>(a.tiles_m) * a.num_kb;
+    grid = static_cast<int>(sk_grid(N, K));
+    a.streamk = 1;
+    a.sk_base = static_cast<int>(total / grid);
+    a.sk_extra = static_cast<int>(total % grid);
+    a.num_items = static_cast<int>(total);
+  } else {
+    if (epi == EPI_ARGMAX) {
+      a.argmax_ws = reinterpret_cast<float2*>(ws);
+    } else if (a.splits > 1) {
+      a.partial = reinterpret_cast<float*>(ws);
+    }
+    const int per_sm = (swap && bn <= 128 && !wide) ? 2 : 1;
+    grid = std::min(a.num_items, num_sms() * per_sm);
+  }
 
   CUtensorMap ma, mb;
   int rc;
@@ -938,6 +1127,16 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     return launch_k("argmax_reduce_kernel", argmax_reduce_kernel, dim3(static_cast<unsigned>(T)),
                     dim3(256), 0, st, a.argmax_ws, tiles, static_cast<int>(T), argmax_out,
                     static_cast<float*>(nullptr));
+  }
+  if (sk && fkind == FUSE_RESIDUAL_NORM) {  // h (= C) is final: the next RMSNorm reads it
+    if (fused) *fused = true;
+    return rmsnorm_launch(C, ldc, nullptr, fuse->norm_w, fuse->eps, T, static_cast<int>(N), fuse->norm_out,
+                          fuse->ld_norm, st);
+  }
+  if (sk && fkind == FUSE_QKV_ROPE) {  // qkv (= C) is final: RoPE + paged KV append
+    if (fused) *fused = true;
+    return rope_kv_launch(C, ldc, fuse->pos, fuse->slot, fuse->cos_sin, fuse->max_pos, fuse->k_cache,
+                          fuse->v_cache, fuse->block_size, T, fuse->Hq, fuse->Hkv, 128, st);
   }
   if (fkind == FUSE_RESIDUAL_NORM) {
     if (fused) *fused = true;
@@ -972,6 +1171,32 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
 }
 
 
+// Weight packing: W [N, K] (row stride ld) -> 16 KB tiles [N/128][K/64], each tile the
+// exact 128-byte-swizzled shared-memory image TMA would produce for a 128 x 64 box, so
+// the GEMM producer streams it with one contiguous bulk copy per k-block.
+__global__ void pack_weight_kernel(const __nv_bfloat16* __restrict__ W, int64_t ld, int64_t N, int64_t K,
+                                   uint8_t* __restrict__ out) {
+  const int64_t nkb = K / BK;
+  const int64_t chunks = N * (K / 8);  // 16-byte chunks
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i / (K / 8), kc = i % (K / 8);
+    const int64_t mt = n / BM, r = n % BM, kb = kc / 8, c = kc % 8;
+    const uint4 v = *reinterpret_cast<const uint4*>(W + n * ld + kc * 8);
+    uint8_t* d = out + (mt * nkb + kb) * A_TILE_BYTES + r * 128 + ((c ^ (r & 7)) << 4);
+    *reinterpret_cast<uint4*>(d) = v;
+  }
+}
+
+int pack_weight_launch(const __nv_bfloat16* W, int64_t ld, int64_t N, int64_t K, void* out, cudaStream_t st) {
+  if (N % 256 || K % BK || ld % 8)
+    return set_error(PL_ERR_CONFIG, "pack_weight: N %% 256, K %% 64 and ld %% 8 must be 0");
+  const int64_t chunks = N * (K / 8);
+  const int blocks = static_cast<int>(std::min<int64_t>((chunks + 255) / 256, 148 * 16));
+  pack_weight_kernel<<<blocks, 256, 0, st>>>(W, ld, N, K, static_cast<uint8_t*>(out));
+  return check_launch("pack_weight_kernel");
+}
+
 // Load every kernel of this file into the context now (lazy module loading would
 // otherwise load it at first launch, which can wait on a spinning NCCL kernel).
 template <typename K>
@@ -999,6 +1224,7 @@ int gemm_preload() {
   if (!rc) rc = preload_one(reduce_residual_norm_kernel<8>, "reduce_residual_norm_kernel");
   if (!rc) rc = preload_one(reduce_qkv_rope_kernel, "reduce_qkv_rope_kernel");
   if (!rc) rc = preload_one(gemm_splitk_reduce_kernel, "gemm_splitk_reduce_kernel");
+  if (!rc) rc = preload_one(pack_weight_kernel, "pack_weight_kernel");
   return rc;
 }
 

@@ -79,7 +79,9 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
                 const __nv_bfloat16* bias, __nv_bfloat16* C, int64_t ldc,
                 const __nv_bfloat16* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,
                 int epi, void* ws, int64_t ws_bytes, int64_t* argmax_out, cudaStream_t st,
-                const FusedEpi* fuse = nullptr, bool* fused = nullptr);
+                const FusedEpi* fuse = nullptr, bool* fused = nullptr, bool w_packed = false);
+// W [N, K] -> pre-swizzled 16 KB tiles (see gemm_tc.cu); out may not alias W
+int pack_weight_launch(const __nv_bfloat16* W, int64_t ld, int64_t N, int64_t K, void* out, cudaStream_t st);
 
 // per-file eager kernel loading (pl_preload_kernels)
 int attention_preload();

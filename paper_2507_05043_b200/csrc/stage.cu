@@ -81,6 +81,52 @@ struct Stage {
   int probe_layer = -1;
   std::vector<ProbeRec> probes;
   size_t probe_used = 0;
+  // weights repacked into pre-swizzled 16 KB tiles (pl_stage_pack_weights)
+  bool pk_qkv = false, pk_o = false, pk_gu = false, pk_down = false, pk_lm = false;
+
+  int pack(cudaStream_t st) {
+    const pl_stage_config& c = cfg;
+    const int64_t d = c.d, qkv_dim = static_cast<int64_t>(c.Hq + 2 * c.Hkv) * c.hd;
+    const int64_t attn_dim = static_cast<int64_t>(c.Hq) * c.hd, ffn = c.ffn;
+    struct Job { bool* flag; int64_t N, K; };
+    const Job jobs[5] = {{&pk_qkv, qkv_dim, d}, {&pk_o, d, attn_dim}, {&pk_gu, 2 * ffn, d}, {&pk_down, d, ffn},
+                         {&pk_lm, c.is_last ? c.vocab : 0, d}};
+    int64_t biggest = 0;
+    for (const Job& j : jobs)
+      if (j.N % 256 == 0 && j.K % 64 == 0 && j.N > 0) biggest = std::max(biggest, j.N * j.K * 2);
+    if (biggest == 0) return PL_OK;
+    void* tmp = nullptr;
+    cudaError_t e = cudaMalloc(&tmp, biggest);
+    if (e != cudaSuccess) return set_cuda_error(e, "pack_weights: temp");
+    int rc = PL_OK;
+    auto pack_one = [&](void* w, int64_t N, int64_t K) {
+      if (rc || !w) return;
+      e = cudaMemcpyAsync(tmp, w, N * K * 2, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) {
+        rc = set_cuda_error(e, "pack_weights: copy");
+        return;
+      }
+      rc = pack_weight_launch(static_cast<const __nv_bfloat16*>(tmp), K, N, K, w, st);
+    };
+    for (const Job& j : jobs) {
+      if (j.N <= 0 || j.N % 256 || j.K % 64 || *j.flag) continue;
+      if (j.flag == &pk_lm) {
+        pack_one(const_cast<void*>(c.lm_head), j.N, j.K);
+      } else {
+        for (auto& lw : layers) {
+          const void* w = j.flag == &pk_qkv ? lw.w_qkv : j.flag == &pk_o ? lw.w_o : j.flag == &pk_gu ? lw.w_gate_up
+                                                                                                 : lw.w_down;
+          pack_one(const_cast<void*>(w), j.N, j.K);
+        }
+      }
+      if (rc) break;
+      *j.flag = true;
+    }
+    e = cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    if (!rc && e != cudaSuccess) rc = set_cuda_error(e, "pack_weights");
+    return rc;
+  }
 
   __nv_bfloat16* buf(int64_t off) const { return reinterpret_cast<__nv_bfloat16*>(ws + off); }
 
@@ -176,7 +222,7 @@ struct Stage {
       if ((rc = gemm_launch(a, d, static_cast<const __nv_bfloat16*>(w.w_qkv), d,
                             static_cast<const __nv_bfloat16*>(w.b_qkv), qkv, qkv_dim, nullptr, 0, T,
                             qkv_dim, d, w.b_qkv ? EPI_BIAS : EPI_STORE, gws, gws_bytes, nullptr, st,
-                            &qf, &roped)))
+                            &qf, &roped, pk_qkv)))
         return rc;
       mark(1);
       if (!roped &&
@@ -212,7 +258,7 @@ struct Stage {
       bool normed = false;
       if ((rc = gemm_launch(o, attn_dim, static_cast<const __nv_bfloat16*>(w.w_o), attn_dim, nullptr,
                             hid, d, hid, d, T, d, attn_dim, EPI_RESIDUAL, gws, gws_bytes, nullptr, st,
-                            &of, &normed)))
+                            &of, &normed, pk_o)))
         return rc;
       mark(3);
       if (!normed &&
@@ -221,14 +267,15 @@ struct Stage {
         return rc;
       mark(4);
       if ((rc = gemm_launch(a, d, static_cast<const __nv_bfloat16*>(w.w_gate_up), d, nullptr, m, ffn,
-                            nullptr, 0, T, 2 * ffn, d, EPI_SWIGLU, gws, gws_bytes, nullptr, st)))
+                            nullptr, 0, T, 2 * ffn, d, EPI_SWIGLU, gws, gws_bytes, nullptr, st, nullptr,
+                            nullptr, pk_gu)))
         return rc;
       mark(5);
       // the next layer's input norm rides on this residual reduction (not across stages)
       FusedEpi df = norm_fuse(l + 1 < c.num_layers ? layers[l + 1].attn_norm : nullptr);
       if ((rc = gemm_launch(m, ffn, static_cast<const __nv_bfloat16*>(w.w_down), ffn, nullptr, hid, d,
                             hid, d, T, d, ffn, EPI_RESIDUAL, gws, gws_bytes, nullptr, st, &df,
-                            &a_ready)))
+                            &a_ready, pk_down)))
         return rc;
       mark(6);
     }
@@ -240,7 +287,8 @@ struct Stage {
                                R, c.d, hn, d, st)))
         return rc;
       if ((rc = gemm_launch(hn, d, static_cast<const __nv_bfloat16*>(c.lm_head), d, nullptr, nullptr, 0,
-                            nullptr, 0, R, c.vocab, d, EPI_ARGMAX, gws, gws_bytes, mb.out_ids, st)))
+                            nullptr, 0, R, c.vocab, d, EPI_ARGMAX, gws, gws_bytes, mb.out_ids, st, nullptr,
+                            nullptr, pk_lm)))
         return rc;
     }
     return PL_OK;
@@ -290,6 +338,11 @@ int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* laye
 int32_t pl_stage_forward(void* handle, const pl_microbatch* mb, void* stream) {
   if (!handle || !mb) return set_error(PL_ERR_CONFIG, "stage_forward: null argument");
   return static_cast<Stage*>(handle)->forward(*mb, static_cast<cudaStream_t>(stream));
+}
+
+int32_t pl_stage_pack_weights(void* handle, void* stream) {
+  if (!handle) return set_error(PL_ERR_CONFIG, "stage_pack_weights: null handle");
+  return static_cast<Stage*>(handle)->pack(static_cast<cudaStream_t>(stream));
 }
 
 int32_t pl_stage_destroy(void* handle) {

@@ -9,7 +9,9 @@ HBM layout per stage (bf16 unless noted):
   weights        per layer w_qkv [(Hq+2Hkv)hd, d], w_o [d, Hq hd],
                  w_gate_up [2ffn, d] (64-row gate|up blocks), w_down [d, ffn],
                  2 norm vectors (+ qkv bias); embed [V, d] on the first stage,
-                 final norm + lm_head [V, d] on the last
+                 final norm + lm_head [V, d] on the last.  After creation the
+                 projection weights and lm_head are repacked in place into
+                 pre-swizzled 16 KB tiles [N/128][K/64] (pl_stage_pack_weights)
   KV cache       per layer k/v [num_blocks, Hkv, 64, hd]  (paged, 64-token blocks)
   hidden[slot]   [max_tokens, d] residual stream per in-flight micro-batch slot
                  (the payload buffer the inter-stage links read and write)
@@ -54,7 +56,8 @@ class StageExecutor:
 
     def __init__(self, spec: DecoderSpec, stage_idx: int, layers: tuple[int, int], is_first: bool,
                  is_last: bool, device: torch.device, *, seed: int = 0, max_tokens: int,
-                 max_reqs: int, max_ctx: int, num_blocks: int, n_slots: int = 1):
+                 max_reqs: int, max_ctx: int, num_blocks: int, n_slots: int = 1,
+                 pack_weights: bool = True):
         self.spec = spec
         self.stage_idx = stage_idx
         self.lo, self.hi = layers
@@ -68,6 +71,11 @@ class StageExecutor:
             self.stream = torch.cuda.Stream(self.device)
             self._alloc(seed)
             self._create()
+            # projection weights -> pre-swizzled 16 KB tiles (one bulk copy per k-block);
+            # afterwards the weight tensors are only meaningful to this stage
+            self.packed = bool(pack_weights)
+            if self.packed:
+                N.call("pl_stage_pack_weights", self.handle, self.stream.cuda_stream)
 
     # ------------------------------------------------------------- setup
     def _alloc(self, seed: int) -> None:

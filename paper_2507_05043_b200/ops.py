@@ -40,7 +40,8 @@ def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
     """Per-device scratch reused across calls (stream-ordered on the current stream)."""
     buf = _WS.get(device)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        # zeroed once: stream-K tile counters must start at 0 (each launch re-zeroes its own)
+        buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
         _WS[device] = buf
     return buf
 

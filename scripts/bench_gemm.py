@@ -45,12 +45,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--T", type=int, nargs="+", default=[8, 16, 32, 64])
     ap.add_argument("--model", default="l3")
+    ap.add_argument("--shapes", nargs="*", default=None,
+                    help="custom N,K pairs (plain store epilogue), e.g. 18944,4096 18944,1024")
     a = ap.parse_args()
     spec = {"l3": LLAMA3_8B, "q2": QWEN2_72B}[a.model]
     dev = torch.device("cuda", 0)
     shapes = {"qkv": (spec.qkv_dim, spec.d, ops.EPI_NONE), "o": (spec.d, spec.attn_dim, ops.EPI_RESIDUAL),
               "gate_up": (2 * spec.ffn, spec.d, ops.EPI_SWIGLU), "down": (spec.d, spec.ffn, ops.EPI_RESIDUAL),
               "lm_head": (spec.vocab, spec.d, ops.EPI_ARGMAX)}
+    if a.shapes:
+        shapes = {f"N{n}K{k}": (int(n), int(k), ops.EPI_NONE) for n, k in (x.split(",") for x in a.shapes)}
     for name, (N, K, epi) in shapes.items():
         wbytes = N * K * 2
         copies = max(1, -(-300_000_000 // wbytes))

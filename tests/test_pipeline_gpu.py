@@ -95,12 +95,46 @@ def test_config1_standard_init_tie_band():
     assert exact / total >= 0.9, f"only {exact}/{total} exact"
 
 
+@pytest.mark.parametrize("spec_name,T", [("tiny", 64), ("l3-2", 64), ("l3-2", 300)])
+def test_packed_weights_bit_identical(spec_name, T):
+    """Pre-swizzled weight tiles (bulk copies) vs row-major weights (TMA boxes): the
+    same tiles reach the tensor cores in the same order, so hidden states and token
+    ids are bit-identical -- decode (SWAP) and prefill (T > 256) orientations."""
+    spec = TINY if spec_name == "tiny" else LLAMA3_8B.with_(num_layers=2)
+    R = 4
+    lens = [T // R] * R
+    lens[-1] += T - sum(lens)
+    outs = []
+    for pack in (False, True):
+        exe = StageExecutor(spec, 0, (0, spec.num_layers), True, True, torch.device("cuda", 0), seed=0,
+                            pack_weights=pack, max_tokens=T, max_reqs=R, max_ctx=512, num_blocks=64,
+                            n_slots=1)
+        cu = np.concatenate([[0], np.cumsum(lens)])
+        pos = np.concatenate([np.arange(n) for n in lens])
+        rows = np.arange(R * exe.max_blocks, dtype=np.int32).reshape(R, -1)
+        req_of = np.repeat(np.arange(R), lens)
+        slots = rows[req_of, pos // 64] * 64 + pos % 64
+        meta = build_meta(T, R, exe.max_blocks, pos, slots, req_of, cu, lens, cu[1:] - 1, rows)
+        ids = np.concatenate([prompt_tokens(0, i, n, spec.vocab) for i, n in enumerate(lens)])
+        exe.meta_dev[: meta.size].copy_(torch.from_numpy(meta))
+        exe.ids_dev[:T].copy_(torch.from_numpy(ids))
+        torch.cuda.synchronize()
+        exe.forward(0, T, R, False, max(lens), max(lens))
+        exe.stream.synchronize()
+        outs.append((exe.hidden[0][:T].clone().cpu(), exe.out_ids[0][:R].clone().cpu()))
+        exe.close()
+        del exe
+    assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
+    assert torch.equal(outs[0][1], outs[1][1])
+
+
 def test_stage_logits_within_tolerance():
     """Whole tiny model as one stage: GPU residual stream + GPU logits vs the oracle."""
     spec = TINY
     lens = [128, 77, 3]
     R, T = len(lens), sum(lens)
     exe = StageExecutor(spec, 0, (0, spec.num_layers), True, True, torch.device("cuda", 0), seed=0,
+                        pack_weights=False,
                         max_tokens=T, max_reqs=R, max_ctx=256, num_blocks=16, n_slots=1)
     cu = np.concatenate([[0], np.cumsum(lens)])
     pos = np.concatenate([np.arange(n) for n in lens])
@@ -140,6 +174,7 @@ def test_decode_logits_within_tolerance(spec):
     R, T = len(lens), sum(lens)
     steps = 5
     exe = StageExecutor(spec, 0, (0, spec.num_layers), True, True, torch.device("cuda", 0), seed=0,
+                        pack_weights=False,
                         max_tokens=T, max_reqs=R, max_ctx=256, num_blocks=3 * 4, n_slots=1)
     mb_ = exe.max_blocks
     rows = np.arange(R * mb_, dtype=np.int32).reshape(R, -1)
