@@ -97,6 +97,17 @@ class ClockSampler:
         return False
 
 
+def ncu_traffic(kernel: str, T: int):
+    """DRAM bytes (read + write) per launch of `kernel` at T tokens from the committed
+    ncu --set full capture summary (profiles/traffic.json), or None."""
+    try:
+        d = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        e = d[kernel]
+        return e["dram_bytes"] if int(e["T"]) == T else None
+    except Exception:
+        return None
+
+
 def dist_setup():
     import torch
     import torch.distributed as dist
@@ -235,7 +246,7 @@ def run_b200(args):
         achieved = alg / avg_s / 1e9
         roof = {"kernel": "gemm_tc_kernel<SWAP> gate_up+SwiGLU (decode, incl. split-K reduce)",
                 "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": None,
+                "frac": round(achieved / hbm, 4), "traffic": ncu_traffic("gate_up", int(round(avg_T))),
                 "algorithmic_bytes_per_launch": int(alg), "avg_launch_us": round(avg_s * 1e6, 2),
                 "avg_T": round(avg_T, 2), "launches_timed": len(gu_ms), "peak_source": peak_src,
                 "other_decode_kernels_avg_us": {
@@ -376,6 +387,13 @@ def main():
     out = run_reference(args) if args.impl == "reference" else run_b200(args)
     if out is not None:
         print(json.dumps(out), flush=True)
+    try:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
 
 
 if __name__ == "__main__":

@@ -967,7 +967,22 @@ int gemm_num_splits(int64_t N, int64_t K, bool swap) {
   if (forced > 0) return static_cast<int>(std::min<int64_t>(forced, K / BK));
   const int64_t tiles = (N + BM - 1) / BM;
   const int64_t kb = K / BK;
+  // PL_SPLIT_RULE=fit: the largest split with tiles*splits <= 148 (every CTA on its own
+  // SM, so the next GEMM's CTAs can become resident beside it); default: the smallest
+  // split with tiles*splits >= 148
+  static const bool fit = [] { const char* v = getenv("PL_SPLIT_RULE"); return v && v[0] == 'f'; }();
   const int64_t sms = 148;
+  if (fit) {
+    int best = 1;
+    for (int s = 1; s <= 16; ++s) {
+      const int64_t per = (kb + s - 1) / s;
+      if (s > 1 && per < 4) break;
+      const int eff = static_cast<int>((kb + per - 1) / per);
+      if (tiles * eff > sms) break;
+      best = eff;
+    }
+    return best;
+  }
   int best = 1;
   for (int s = 1; s <= 16; ++s) {
     const int64_t per = (kb + s - 1) / s;
@@ -1071,8 +1086,13 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     return set_error(PL_ERR_CONFIG, "gemm: qkv+rope fusion needs a STORE/BIAS GEMM");
   a.pmode = (fkind == FUSE_RESIDUAL_NORM && !sk) ? 1 : 0;
   // L2 warm-up only for weights that comfortably fit the 126 MB L2 (PL_L2PF overrides)
-  static const int l2pf = [] { const char* v = getenv("PL_L2PF"); return v ? atoi(v) : 16; }();
-  a.l2_prefetch = (swap && N * K * 2 <= (64ll << 20)) ? l2pf : 0;
+  // measured (scripts/l2pf_sweep.sh): warming L2 beyond the ring only slows the decode chain
+  static const int l2pf = [] { const char* v = getenv("PL_L2PF"); return v ? atoi(v) : 0; }();
+  static const int64_t l2pf_max = [] {
+    const char* v = getenv("PL_L2PF_MAXMB");
+    return (v ? atoll(v) : 64) << 20;
+  }();
+  a.l2_prefetch = (swap && N * K * 2 <= l2pf_max) ? l2pf : 0;
   const int64_t need = gemm_workspace_bytes(T, N, K, epi);
   if (need > 0 && (ws_bytes < need || !ws))
     return set_error(PL_ERR_CONFIG, "gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
@@ -1099,7 +1119,8 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     } else if (a.splits > 1) {
       a.partial = reinterpret_cast<float*>(ws);
     }
-    const int per_sm = (swap && bn <= 128 && !wide) ? 2 : 1;
+    static const int per_sm_env = [] { const char* v = getenv("PL_GRID_PER_SM"); return v ? atoi(v) : 0; }();
+    const int per_sm = per_sm_env > 0 ? per_sm_env : (swap && bn <= 128 && !wide) ? 2 : 1;
     grid = std::min(a.num_items, num_sms() * per_sm);
   }
 

@@ -8,11 +8,13 @@ set -u
 TAG=${1:-r1}
 OUT=gpurun_out
 export PYTHONPATH=$PWD
-python bench.py --steps 1 --warmup 3 > $OUT/prof_${TAG}_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
-# ~67k launches per serving run; setup + profiling + 3 warm-up runs precede the timed one
-ncu --metrics gpu__time_duration.sum --clock-control none -s 235000 -c 2500 --csv \
-    --log-file $OUT/prof_${TAG}_launches.csv python bench.py --steps 1 --warmup 3 \
-    > $OUT/prof_${TAG}_launches_run.log 2>&1
+# launch list of a short serving run (decode 4 tokens) -- the full 256-token bench
+# command is ~270k launches and does not finish under ncu; the decode kernel set and
+# per-step structure are the same.  Skip setup, profiling and the warm-up runs.
+CMD="python bench.py --steps 1 --warmup 3 --decode 4 --no-cpu-baseline"
+$CMD > $OUT/prof_${TAG}_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
+ncu --metrics gpu__time_duration.sum --clock-control none -s 14000 -c 1500 --csv \
+    --log-file $OUT/prof_${TAG}_launches.csv $CMD > $OUT/prof_${TAG}_launches_run.log 2>&1
 python scripts/profile_decode.py --layers 4 --iters 2 --last 0 > $OUT/prof_${TAG}_decode_plain.log 2>&1 || exit 1
 # per 4-layer decode forward: gemm launches qkv,o,gate_up,down per layer; skip the first forwards
 ncu --set full --import-source on --clock-control none -k regex:gemm_tc -s 10 -c 1 \
