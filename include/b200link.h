@@ -169,15 +169,18 @@ typedef struct pl_stage_config {
  *   | block_table[R * max_blocks_per_req]                                    */
 typedef struct pl_microbatch {
   int32_t T, R;
-  int32_t phase;      /* 0 prefill, 1 decode */
+  int32_t phase;      /* 0 prefill, 1 decode, 2 mixed (allow_mixed_phase, engine.py:184-190):
+                         requests [0, n_decode) decode one token each in rows [0, n_decode),
+                         the rest are prompts in rows [n_decode, T)                        */
   int32_t max_seqlen; /* prefill: longest prompt in the micro-batch */
   int32_t max_ctx;    /* decode: longest context in the micro-batch */
   const int32_t* meta;
-  const int64_t* token_ids;  /* first stage, prefill: prompt ids [T]          */
-  const int64_t* last_token; /* first stage, decode: per-slot feedback table  */
+  const int64_t* token_ids;  /* first stage, prefill/mixed: prompt ids [T]    */
+  const int64_t* last_token; /* first stage, decode/mixed: feedback table     */
   void* hidden;              /* bf16 [T, d] residual stream: input (non-first),
                                 output (non-last), updated in place           */
   int64_t* out_ids;          /* last stage: [R] greedy tokens                 */
+  int32_t n_decode;          /* mixed: decode requests leading the batch      */
 } pl_microbatch;
 
 PL_API int64_t pl_stage_workspace_bytes(const pl_stage_config* cfg);

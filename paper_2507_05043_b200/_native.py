@@ -47,6 +47,7 @@ class MicroBatch(C.Structure):
     _fields_ = [
         ("T", i32), ("R", i32), ("phase", i32), ("max_seqlen", i32), ("max_ctx", i32),
         ("meta", vp), ("token_ids", vp), ("last_token", vp), ("hidden", vp), ("out_ids", vp),
+        ("n_decode", i32),
     ]
 
 

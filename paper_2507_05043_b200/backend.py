@@ -109,9 +109,6 @@ class _PinnedRing:
 class GpuBackend(Backend):
     def __init__(self, spec: DecoderSpec, cfg, placement: Placement, *, seed: int = 0,
                  prompts: dict | None = None, comms: dict | None = None, throttle: bool = False):
-        if cfg.allow_mixed_phase:
-            raise pipelink.ConfigError("mixed prefill/decode micro-batches are not supported on the "
-                                       "B200 backend yet (allow_mixed_phase=False)")
         self.spec, self.cfg, self.pl = spec, cfg, placement
         self.seed = seed
         self.user_prompts = prompts
@@ -192,6 +189,9 @@ class GpuBackend(Backend):
 
     # ------------------------------------------------------------ driver hooks
     def start(self, driver, trace) -> None:
+        if self.cfg.allow_mixed_phase:
+            raise pipelink.ConfigError("mixed prefill/decode micro-batches run on the native runtime "
+                                       "only (B200PipelineEngine(native=True))")
         self.driver = driver
         self.prepare(trace)
         reqs = trace.requests
@@ -599,7 +599,7 @@ class GpuBackend(Backend):
         self.decode_start_s = None if np.isnan(ds.value) else ds.value
         self.mb_requests = {int(m): tuple(mb_ids[mb_off[i]:mb_off[i + 1]].tolist())
                             for i, m in enumerate(mbl[:, 0].tolist())}
-        self.mb_log = [("decode" if d else "prefill", int(R), int(w)) for _, d, R, w in mbl.tolist()]
+        self.mb_log = [(("prefill", "decode", "mixed")[d], int(R), int(w)) for _, d, R, w in mbl.tolist()]
         self.busy_real_ns = {}
         for (s, mb), (a, b) in zip(busy.tolist(), busy_s.tolist()):
             self.busy_real_ns.setdefault(s, []).append((mb, round(a * 1e9), round(b * 1e9)))

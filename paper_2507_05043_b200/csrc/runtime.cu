@@ -76,7 +76,8 @@ struct RingEntry {
 };
 
 struct MbRec {
-  int slot, T, R, decode, max_seqlen, max_ctx;
+  int slot, T, R, decode, max_seqlen, max_ctx;  // decode: 0 prefill, 1 decode, 2 mixed
+  int n_decode;
   int entry;
   int64_t meta_len;
 };
@@ -323,16 +324,26 @@ struct Pipeline : sched::Hooks {
   // ------------------------------------------------------------ hooks
   void admit(const sched::MicroBatch& mb, int64_t) override {
     if (err) return;
-    if (mb.phase == sched::MIXED) {
-      fail(set_error(PL_ERR_CONFIG, "mixed micro-batch reached the B200 runtime"));
-      return;
-    }
     if (free_slots.empty()) {
       fail(set_error(PL_ERR_PROTOCOL, "no free micro-batch slot"));
       return;
     }
     const int R = (int)mb.reqs.size();
     const bool decode = mb.phase == sched::DECODE;
+    const bool mixed = mb.phase == sched::MIXED;
+    // mixed batches: admit_and_batch places decoders ahead of prompts (engine.py:184-198)
+    int n_dec = 0;
+    if (mixed) {
+      for (int ri : mb.reqs) {
+        if ((*reqs)[ri].state != sched::DECODING) break;
+        ++n_dec;
+      }
+      for (int i = n_dec; i < R; ++i)
+        if ((*reqs)[mb.reqs[i]].state == sched::DECODING) {
+          fail(set_error(PL_ERR_PROTOCOL, "mixed micro-batch with a decoder after a prompt"));
+          return;
+        }
+    }
     if (R > max_reqs) {
       fail(set_error(PL_ERR_CONFIG, "micro-batch of %d requests exceeds capacity %d", R, max_reqs));
       return;
@@ -356,7 +367,7 @@ struct Pipeline : sched::Hooks {
     if (decode) {
       T = R;
     } else {
-      for (int ri : mb.reqs) T += (*reqs)[ri].input_len;
+      for (int i = 0; i < R; ++i) T += i < n_dec ? 1 : (*reqs)[mb.reqs[i]].input_len;
     }
     if (T > max_tokens) {
       fail(set_error(PL_ERR_CONFIG, "micro-batch of %lld tokens exceeds capacity %d", (long long)T, max_tokens));
@@ -377,6 +388,7 @@ struct Pipeline : sched::Hooks {
     int64_t work = 0;
     cuq[0] = 0;
     int64_t t = 0;
+    int64_t* ids = reinterpret_cast<int64_t*>(en.host + ids_off);
     for (int i = 0; i < R; ++i) {
       const int ri = mb.reqs[i];
       const sched::Request& q = (*reqs)[ri];
@@ -384,18 +396,21 @@ struct Pipeline : sched::Hooks {
       std::memcpy(btm + (int64_t)i * max_blocks, row, sizeof(int32_t) * max_blocks);
       scat[i] = ri;
       scat[R + i] = (int32_t)q.tokens;
-      if (decode) {
+      if (decode || i < n_dec) {
         const int64_t p = q.input_len + q.tokens - 1;
-        pos[i] = (int32_t)p;
-        slot[i] = row[p / block_size] * block_size + (int32_t)(p % block_size);
-        rslot[i] = ri;
-        cuq[i + 1] = i + 1;
+        pos[t] = (int32_t)p;
+        slot[t] = row[p / block_size] * block_size + (int32_t)(p % block_size);
+        rslot[t] = ri;
+        if (mixed) ids[t] = 0;  // the decode row embeds last_token[req] instead
+        ++t;
+        cuq[i + 1] = (int32_t)t;
         ctx[i] = (int32_t)(p + 1);
-        last[i] = i;
+        last[i] = (int32_t)(t - 1);
         max_ctx = std::max<int>(max_ctx, (int)(p + 1));
         work += p + 1;
       } else {
         const int64_t L = q.input_len;
+        std::memcpy(ids + t, prompt_ids.data() + prompt_off[ri], sizeof(int64_t) * L);
         for (int64_t p = 0; p < L; ++p, ++t) {
           pos[t] = (int32_t)p;
           slot[t] = row[p / block_size] * block_size + (int32_t)(p % block_size);
@@ -405,24 +420,16 @@ struct Pipeline : sched::Hooks {
         ctx[i] = (int32_t)L;
         last[i] = (int32_t)(t - 1);
         max_seqlen = std::max<int>(max_seqlen, (int)L);
+        work += L;
       }
     }
-    if (!decode) {
-      max_ctx = max_seqlen;
-      work = T;
-      int64_t* ids = reinterpret_cast<int64_t*>(en.host + ids_off);
-      int64_t o = 0;
-      for (int ri : mb.reqs) {
-        const int64_t n = prompt_off[ri + 1] - prompt_off[ri];
-        std::memcpy(ids + o, prompt_ids.data() + prompt_off[ri], sizeof(int64_t) * n);
-        o += n;
-      }
-    }
+    if (!decode && !mixed) max_ctx = max_seqlen;  // unused by the prefill kernel
     const int slot_k = free_slots.back();
     free_slots.pop_back();
-    MbRec rec{slot_k, (int)T, R, decode ? 1 : 0, max_seqlen, max_ctx, entry, meta_len((int)T, R)};
+    MbRec rec{slot_k, (int)T, R, decode ? 1 : (mixed ? 2 : 0), max_seqlen, max_ctx, n_dec, entry,
+              meta_len((int)T, R)};
     mbs.emplace(mb.id, std::move(rec));
-    mb_log.push_back(MbLog{mb.id, decode ? 1 : 0, R, work});
+    mb_log.push_back(MbLog{mb.id, decode ? 1 : (mixed ? 2 : 0), R, work});
     for (int ri : mb.reqs) mb_req_ids.push_back((*reqs)[ri].id);
     mb_req_off.push_back((int64_t)mb_req_ids.size());
   }
@@ -437,7 +444,7 @@ struct Pipeline : sched::Hooks {
     if (r.n_fwd >= RUN_AHEAD && !cu(cudaEventSynchronize(ahead), "run-ahead")) return;  // run-ahead cap
     if (r.has_send[k]) cudaStreamWaitEvent(r.comp, r.ev_send[k], 0);
     if (s > 0 && r.recv_ev[k]) cudaStreamWaitEvent(r.comp, r.recv_ev[k], 0);
-    if (s == 0 && rec.decode && last_fb) {
+    if (s == 0 && rec.decode != 0 && last_fb) {  // decode rows read the latest token scatter
       cudaStreamWaitEvent(r.comp, last_fb, 0);
       if (!first_decode) {
         first_decode = pool(r.dev).take();
@@ -448,7 +455,7 @@ struct Pipeline : sched::Hooks {
     if (!cu(cudaMemcpyAsync(r.meta_dev, en.host, sizeof(int32_t) * rec.meta_len, cudaMemcpyHostToDevice, r.comp),
             "meta H2D"))
       return;
-    if (s == 0 && !rec.decode &&
+    if (s == 0 && rec.decode != 1 &&
         !cu(cudaMemcpyAsync(r.ids_dev, en.host + ids_off, sizeof(int64_t) * rec.T, cudaMemcpyHostToDevice, r.comp),
             "ids H2D"))
       return;
@@ -458,9 +465,10 @@ struct Pipeline : sched::Hooks {
     cudaEventRecord(a, r.comp);
     pl_microbatch m{};
     m.T = rec.T, m.R = rec.R, m.phase = rec.decode, m.max_seqlen = rec.max_seqlen, m.max_ctx = rec.max_ctx;
+    m.n_decode = rec.n_decode;
     m.meta = r.meta_dev;
-    m.token_ids = (s == 0 && !rec.decode) ? r.ids_dev : nullptr;
-    m.last_token = (s == 0 && rec.decode) ? last_token : nullptr;
+    m.token_ids = (s == 0 && rec.decode != 1) ? r.ids_dev : nullptr;
+    m.last_token = (s == 0 && rec.decode != 0) ? last_token : nullptr;
     m.hidden = r.hidden[k];
     m.out_ids = s == S - 1 ? r.out_ids[k] : nullptr;
     if (!ok(pl_stage_forward(r.stage, &m, r.comp))) return;

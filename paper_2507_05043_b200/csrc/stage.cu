@@ -152,7 +152,14 @@ struct Stage {
       return set_error(PL_ERR_CONFIG, "stage_forward: micro-batch (T=%d, R=%d) exceeds capacity (%d, %d)",
                        T, R, c.max_tokens, c.max_reqs);
     const bool decode = mb.phase == 1;
+    const bool mixed = mb.phase == 2;
+    if (mb.phase < 0 || mb.phase > 2) return set_error(PL_ERR_CONFIG, "stage_forward: bad phase %d", mb.phase);
     if (decode && T != R) return set_error(PL_ERR_CONFIG, "stage_forward: decode needs T == R");
+    // decode requests lead the batch: rows [0, Rd); prompts fill rows [Rd, T)
+    const int Rd = decode ? R : (mixed ? mb.n_decode : 0);
+    const int Rp = R - Rd;
+    if (mixed && (Rd <= 0 || Rp <= 0 || T - Rd < Rp))
+      return set_error(PL_ERR_CONFIG, "stage_forward: mixed batch needs decode and prompt requests");
     if (!mb.meta || !mb.hidden) return set_error(PL_ERR_CONFIG, "stage_forward: missing buffers");
     const int32_t* pos = mb.meta;
     const int32_t* slot = pos + T;
@@ -177,16 +184,18 @@ struct Stage {
     int rc;
 
     if (c.is_first) {
-      if (decode) {
+      if (Rd > 0) {
         if (!mb.last_token) return set_error(PL_ERR_CONFIG, "stage_forward: decode needs last_token");
         rc = embed_launch(nullptr, req_slot, mb.last_token, static_cast<const __nv_bfloat16*>(c.embed),
-                          c.vocab, T, c.d, hid, st);
-      } else {
-        if (!mb.token_ids) return set_error(PL_ERR_CONFIG, "stage_forward: prefill needs token_ids");
-        rc = embed_launch(mb.token_ids, nullptr, nullptr, static_cast<const __nv_bfloat16*>(c.embed),
-                          c.vocab, T, c.d, hid, st);
+                          c.vocab, Rd, c.d, hid, st);
+        if (rc) return rc;
       }
-      if (rc) return rc;
+      if (Rp > 0) {
+        if (!mb.token_ids) return set_error(PL_ERR_CONFIG, "stage_forward: prefill needs token_ids");
+        rc = embed_launch(mb.token_ids + Rd, nullptr, nullptr, static_cast<const __nv_bfloat16*>(c.embed),
+                          c.vocab, T - Rd, c.d, hid + static_cast<int64_t>(Rd) * c.d, st);
+        if (rc) return rc;
+      }
     }
 
     // Decode-path fusions (split-K reductions double as epilogues): QKV reduce + RoPE +
@@ -231,17 +240,19 @@ struct Stage {
                                static_cast<__nv_bfloat16*>(w.v_cache), c.block_size, T, c.Hq, c.Hkv,
                                c.hd, st)))
         return rc;
-      if (decode) {
+      if (Rd > 0) {  // one query row per decode request over its paged context
         rc = attn_decode_launch(qkv, qkv_dim, static_cast<const __nv_bfloat16*>(w.k_cache),
                                 static_cast<const __nv_bfloat16*>(w.v_cache), c.num_blocks,
                                 c.block_size, bt,
-                                c.max_blocks_per_req, ctx, R, mb.max_ctx, c.Hq, c.Hkv, c.hd, scale, o,
+                                c.max_blocks_per_req, ctx, Rd, mb.max_ctx, c.Hq, c.Hkv, c.hd, scale, o,
                                 attn_dim, ws + L.attn_ws, L.total - L.attn_ws, st);
-      } else {
-        rc = attn_prefill_launch(qkv, qkv_dim, cu, R, mb.max_seqlen, c.Hq, c.Hkv, c.hd, scale, o,
-                                 attn_dim, st);
+        if (rc) return rc;
       }
-      if (rc) return rc;
+      if (Rp > 0) {  // causal attention over the prompt rows (cu_seqlens are absolute rows)
+        rc = attn_prefill_launch(qkv, qkv_dim, cu + Rd, Rp, mb.max_seqlen, c.Hq, c.Hkv, c.hd, scale, o,
+                                 attn_dim, st);
+        if (rc) return rc;
+      }
       mark(2);
       auto norm_fuse = [&](const void* norm_w) {
         FusedEpi f;

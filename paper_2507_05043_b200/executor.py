@@ -166,16 +166,19 @@ class StageExecutor:
 
     # ----------------------------------------------------------- forward
     def forward(self, slot: int, T: int, R: int, decode: bool, max_seqlen: int, max_ctx: int,
-                last_token: torch.Tensor | None = None) -> None:
+                last_token: torch.Tensor | None = None, n_decode: int = 0) -> None:
         """Launch the stage forward for the micro-batch whose metadata sits in meta_dev
         (and prompt ids in ids_dev) on self.stream; hidden[slot] in, hidden[slot] out,
-        out_ids[slot] on the last stage."""
+        out_ids[slot] on the last stage.  n_decode > 0 with decode=False: a mixed batch
+        whose first n_decode requests decode one token each."""
         mb = self._mb
-        mb.T, mb.R, mb.phase = T, R, 1 if decode else 0
+        mixed = (not decode) and n_decode > 0
+        mb.T, mb.R, mb.phase = T, R, 2 if mixed else (1 if decode else 0)
+        mb.n_decode = n_decode if mixed else 0
         mb.max_seqlen, mb.max_ctx = max_seqlen, max_ctx
         mb.meta = self.meta_dev.data_ptr()
         mb.token_ids = self.ids_dev.data_ptr() if (self.is_first and not decode) else None
-        mb.last_token = last_token.data_ptr() if (self.is_first and decode) else None
+        mb.last_token = last_token.data_ptr() if (self.is_first and (decode or mixed)) else None
         mb.hidden = self.hidden[slot].data_ptr()
         mb.out_ids = self.out_ids[slot].data_ptr() if self.is_last else None
         rc = self._forward(self.handle, C.byref(mb), self._stream_ptr)

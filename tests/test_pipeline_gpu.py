@@ -227,6 +227,32 @@ def test_stage_counts_on_one_gpu(S, native):
         assert np.array_equal(res.b200.tokens[r.id], want[i].numpy())
 
 
+def test_mixed_prefill_decode_microbatches():
+    """allow_mixed_phase=True (engine.py:184-198): decoders and late-arriving prompts share
+    micro-batches; schedule == pipelink's, tokens == the oracle's."""
+    spec = TINY.with_(peaked=True)
+    cluster = deploy.b200_cluster(2)
+    plan = deploy.plan(cluster, spec, 2)
+    ctrl = pipelink.ControllerConfig(max_batched_tokens=512, max_batch_size=8)
+    cfg = deploy.engine_config(plan, spec, ctrl, chunk_size=4096, allow_mixed_phase=True)
+    trace = pipelink.Trace(requests=[pipelink.Request(i, 0.0001 * i, 40 + 9 * i, 7) for i in range(8)])
+    profiles = synth_profiles(plan)
+    eng = B200PipelineEngine(cfg, cluster, profiles, decoder=spec, seed=0)
+    res = eng.run(trace)
+    ref = pipelink.PipelineEngine(cfg, cluster, profiles).run(trace)
+    a, b = result_key(ref), result_key(res)
+    for k in a:
+        assert a[k] == b[k], f"schedule mismatch in {k}"
+    phases = {mb[0] for mb in eng.gpu.mb_log}
+    assert "mixed" in phases, f"trace produced no mixed micro-batch: {phases}"
+    model = OD.OracleModel(OD.OracleSpec.from_spec(spec), seed=0, max_pos=256)
+    for r in trace.requests:
+        want, _ = model.greedy([torch.from_numpy(prompt_tokens(0, r.id, r.input_len, spec.vocab))],
+                               r.output_len)
+        assert np.array_equal(res.b200.tokens[r.id], want[0].numpy()), f"request {r.id}"
+    eng.close()
+
+
 def test_prefill_chunking_on_and_off_same_tokens():
     """Chunk boundaries change only the transport, never the tokens (config 4 invariant)."""
     spec = TINY.with_(peaked=True)
