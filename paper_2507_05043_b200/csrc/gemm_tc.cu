@@ -92,24 +92,45 @@ PL_DEV int sk_slot(const GemmArgs& a, int c, int tile) {
   return (sk_start(a, c) < tile * a.num_kb) ? 2 * c + 1 : 2 * c;
 }
 
-// Walks this CTA's pieces in order (identical in the producer, MMA and epilogue roles).
+// Walks this CTA's pieces (identical in the producer, MMA and epilogue roles).
+// Stream-K order: the piece in the CTA's LAST tile first, then the rest in k order.
+// A shared tile's head is the last piece of one CTA and its tail the first piece of
+// the next, so both finish early in their CTAs and the fix-up overlaps the mainloop
+// of the CTA's remaining (full) tiles instead of trailing the kernel.
 struct PieceWalk {
-  int it, end;  // stream-K iteration cursor / item cursor
+  int it, end;        // cursor / end of the in-order part
+  int last0, last1;   // the hoisted last-tile piece [last0, last1), empty when done
   PL_DEV void init(const GemmArgs& a) {
     if (a.streamk) {
-      it = sk_start(a, blockIdx.x);
-      end = it + a.sk_base + (static_cast<int>(blockIdx.x) < a.sk_extra ? 1 : 0);
+      const int s0 = sk_start(a, blockIdx.x);
+      const int e0 = s0 + a.sk_base + (static_cast<int>(blockIdx.x) < a.sk_extra ? 1 : 0);
+      const int lt = max(s0, ((e0 - 1) / a.num_kb) * a.num_kb);  // start of the last tile's piece
+      if (lt > s0) {
+        last0 = lt, last1 = e0;
+        it = s0, end = lt;
+      } else {
+        last0 = last1 = 0;
+        it = s0, end = e0;
+      }
     } else {
       it = blockIdx.x;
       end = a.num_items;
+      last0 = last1 = 0;
     }
   }
   PL_DEV bool next(const GemmArgs& a, Piece& p) {
-    if (it >= end) return false;
     if (a.streamk) {
-      const int tile = it / a.num_kb;
-      const int k0 = it % a.num_kb;
-      const int k1 = min(a.num_kb, k0 + (end - it));
+      int k_it, k_end;
+      if (last1 > last0) {
+        k_it = last0, k_end = last1;
+        last0 = last1 = 0;
+      } else {
+        if (it >= end) return false;
+        k_it = it, k_end = end;
+      }
+      const int tile = k_it / a.num_kb;
+      const int k0 = k_it % a.num_kb;
+      const int k1 = min(a.num_kb, k0 + (k_end - k_it));
       p.m_tile = tile;
       p.n_tile = 0;
       p.split = 0;
@@ -119,17 +140,18 @@ struct PieceWalk {
       p.c_last = sk_cta_of(a, tile * a.num_kb + a.num_kb - 1);
       p.partial = p.c_first != p.c_last;
       p.slot = sk_slot(a, blockIdx.x, tile);
-      it += k1 - k0;
-    } else {
-      p.split = it % a.splits;
-      const int tile = it / a.splits;
-      p.m_tile = tile % a.tiles_m;
-      p.n_tile = tile / a.tiles_m;
-      p.kb0 = p.split * a.kb_per_split;
-      p.nkb = min(a.num_kb, p.kb0 + a.kb_per_split) - p.kb0;
-      p.partial = 0;
-      it += gridDim.x;
+      if (k_it == it) it += k1 - k0;
+      return true;
     }
+    if (it >= end) return false;
+    p.split = it % a.splits;
+    const int tile = it / a.splits;
+    p.m_tile = tile % a.tiles_m;
+    p.n_tile = tile / a.tiles_m;
+    p.kb0 = p.split * a.kb_per_split;
+    p.nkb = min(a.num_kb, p.kb0 + a.kb_per_split) - p.kb0;
+    p.partial = 0;
+    it += gridDim.x;
     return true;
   }
 };
@@ -478,16 +500,28 @@ __global__ void __launch_bounds__(192, CTAS)
             auto fetch_slots = [&](int c0, float (&v)[16]) {
 #pragma unroll
               for (int c = 0; c < 16; ++c) v[c] = 0.f;
-              for (int cc = pc.c_first; cc <= pc.c_last; ++cc) {  // k order
-                const float4* p = reinterpret_cast<const float4*>(
-                    args.sk_slots + (int64_t)sk_slot(args, cc, tile) * (BM * BN) + row * BN + c0);
+              const int npc = pc.c_last - pc.c_first + 1;
+              for (int b0 = 0; b0 < npc; b0 += 4) {  // four pieces' loads in flight, summed in k order
+                float4 x[4][4];
 #pragma unroll
-                for (int c = 0; c < 16; c += 4) {
-                  const float4 x = __ldcg(p + c / 4);
-                  v[c] += x.x;
-                  v[c + 1] += x.y;
-                  v[c + 2] += x.z;
-                  v[c + 3] += x.w;
+                for (int u = 0; u < 4; ++u) {
+                  const bool ok = b0 + u < npc;
+                  const float4* p = reinterpret_cast<const float4*>(
+                      args.sk_slots + (int64_t)sk_slot(args, pc.c_first + (ok ? b0 + u : 0), tile) * (BM * BN) +
+                      row * BN + c0);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) x[u][q] = ok ? __ldcg(p + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  if (b0 + u >= npc) break;
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    v[4 * q] += x[u][q].x;
+                    v[4 * q + 1] += x[u][q].y;
+                    v[4 * q + 2] += x[u][q].z;
+                    v[4 * q + 3] += x[u][q].w;
+                  }
                 }
               }
             };
@@ -1008,7 +1042,7 @@ bool streamk_enabled() {
 // every token's summation order -- depend on (N, K) only, never on T.
 int64_t sk_grid(int64_t N, int64_t K) {
   const int64_t total = ((N + BM - 1) / BM) * (K / BK);
-  return std::min<int64_t>(2 * num_sms(), total);
+  return std::min<int64_t>(num_sms(), total);  // one CTA per SM with the deep (~200 KB) ring
 }
 
 // Tile counters sit at the same offset for every stream-K GEMM sharing a workspace
@@ -1129,11 +1163,12 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   if (swap) {
     if ((rc = make_map(&ma, W, N, K, ldw, BM))) return rc;
     if ((rc = make_map(&mb, X, T, K, ldx, bn))) return rc;
+    const bool w1 = wide || sk;  // stream-K: one CTA per SM with the deep ring
     switch (bn) {
-      case 16: rc = wide ? launch_tc<16, true, 1>(ma, mb, a, grid, st) : launch_tc<16, true>(ma, mb, a, grid, st); break;
-      case 32: rc = wide ? launch_tc<32, true, 1>(ma, mb, a, grid, st) : launch_tc<32, true>(ma, mb, a, grid, st); break;
-      case 64: rc = wide ? launch_tc<64, true, 1>(ma, mb, a, grid, st) : launch_tc<64, true>(ma, mb, a, grid, st); break;
-      case 128: rc = wide ? launch_tc<128, true, 1>(ma, mb, a, grid, st) : launch_tc<128, true>(ma, mb, a, grid, st); break;
+      case 16: rc = w1 ? launch_tc<16, true, 1>(ma, mb, a, grid, st) : launch_tc<16, true>(ma, mb, a, grid, st); break;
+      case 32: rc = w1 ? launch_tc<32, true, 1>(ma, mb, a, grid, st) : launch_tc<32, true>(ma, mb, a, grid, st); break;
+      case 64: rc = w1 ? launch_tc<64, true, 1>(ma, mb, a, grid, st) : launch_tc<64, true>(ma, mb, a, grid, st); break;
+      case 128: rc = w1 ? launch_tc<128, true, 1>(ma, mb, a, grid, st) : launch_tc<128, true>(ma, mb, a, grid, st); break;
       default: rc = launch_tc<256, true>(ma, mb, a, grid, st); break;
     }
   } else {
