@@ -1,0 +1,120 @@
+// Per-SM HBM streaming ceiling by load mechanism (experiment, not product code).
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/stream_probe scripts/stream_probe.cu
+//   /tmp/stream_probe
+//
+// Each CTA streams `per_cta` contiguous bytes into shared memory and discards them.
+// Grids of 74 and 148 CTAs (1 per SM), modes:
+//   0: one thread issues 16 KB cp.async.bulk copies into a ring (TMA bulk engine)
+//   1: 256 threads issue cp.async 16 B copies (LDGSTS)
+//   2: 256 threads issue ld.global.nc.v4 (registers, summed)
+//   3: bulk copies + LDGSTS together (half the bytes each)
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define DEV __device__ __forceinline__
+
+DEV uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+DEV void mbar_init(uint64_t* b, uint32_t n) { asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(b)), "r"(n)); }
+DEV void mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+DEV bool mbar_try(uint64_t* b, uint32_t ph) {
+  uint32_t ok;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(ok) : "r"(su32(b)), "r"(ph) : "memory");
+  return ok;
+}
+DEV void mbar_wait(uint64_t* b, uint32_t ph) { while (!mbar_try(b, ph)) {} }
+DEV void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(b)) : "memory");
+}
+
+constexpr int STAGE = 16384, NST = 12;
+
+__global__ void __launch_bounds__(256, 1) probe(const uint8_t* __restrict__ src, int64_t per_cta, int mode,
+                                                  float* sink) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + NST * STAGE);
+  const uint8_t* base = src + blockIdx.x * per_cta;
+  const int64_t nblk = per_cta / STAGE;
+  if (mode == 0 || mode == 3) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < NST; ++s) mbar_init(&full[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t half = mode == 3 ? STAGE / 2 : STAGE;
+    if (mode == 3 && threadIdx.x >= 32) goto ldgsts;  // warps 1-7 stream the other half
+    if (threadIdx.x == 0) {
+      for (int64_t i = 0; i < nblk; ++i) {
+        const int s = i % NST;
+        if (i >= NST) mbar_wait(&full[s], ((i / NST) - 1) & 1);
+        mbar_expect(&full[s], half);
+        bulk(sm + s * STAGE, base + i * STAGE, half, &full[s]);
+      }
+      for (int64_t i = nblk - NST > 0 ? nblk - NST : 0; i < nblk; ++i) mbar_wait(&full[i % NST], (i / NST) & 1);
+    }
+    return;
+  }
+ldgsts:
+  if (mode == 1 || mode == 3) {
+    const int off = mode == 3 ? STAGE / 2 : 0;
+    const int chunk = STAGE - off;  // bytes per block by LDGSTS
+    const int t0 = mode == 3 ? threadIdx.x - 32 : threadIdx.x;
+    const int nt = mode == 3 ? 224 : 256;
+    for (int64_t i = 0; i < nblk; ++i) {
+      const int s = i % NST;
+      for (int c = t0 * 16; c < chunk; c += nt * 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(sm + s * STAGE + off + c)),
+                     "l"(base + i * STAGE + off + c) : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 8;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    return;
+  }
+  // mode 2: plain vector loads
+  float acc = 0.f;
+  const uint4* p = reinterpret_cast<const uint4*>(base);
+  const int64_t n = per_cta / 16;
+#pragma unroll 8
+  for (int64_t i = threadIdx.x; i < n; i += 256) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p + i));
+    acc += __uint_as_float(v.x ^ v.y ^ v.z ^ v.w);
+  }
+  if (acc == 1.2345f) sink[0] = acc;
+}
+
+int main() {
+  const int64_t per_cta = 16ll << 20;  // 16 MB per CTA
+  const int64_t total = per_cta * 148;
+  uint8_t* buf;
+  float* sink;
+  cudaMalloc(&buf, total);
+  cudaMalloc(&sink, 4);
+  cudaMemset(buf, 1, total);
+  const int smem = NST * STAGE + 1024;
+  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const char* names[4] = {"bulk(TMA)", "cp.async", "ld.global.v4", "bulk+cp.async"};
+  for (int mode = 0; mode < 4; ++mode)
+    for (int grid : {37, 74, 148}) {
+      probe<<<grid, 256, smem>>>(buf, per_cta, mode, sink);
+      cudaEventRecord(a);
+      for (int r = 0; r < 3; ++r) probe<<<grid, 256, smem>>>(buf, per_cta, mode, sink);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      const double bytes = 3.0 * grid * per_cta;
+      printf("%-14s grid %3d: %7.1f GB/s total, %6.1f GB/s per SM  (%s)\n", names[mode], grid,
+             bytes / (ms * 1e-3) / 1e9, bytes / (ms * 1e-3) / 1e9 / grid, cudaGetErrorString(cudaGetLastError()));
+    }
+  return 0;
+}
