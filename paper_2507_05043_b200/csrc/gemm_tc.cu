@@ -165,11 +165,28 @@ struct PieceWalk {
 // deep and every other byte of shared memory holds weights in flight -- the
 // kernel is latency-bound on HBM, so weight bytes in flight set its speed.
 // The producer issues B block k only (AS - BS) blocks behind A block k.
+// Ring split (SWAP): the producer issues B block k (L2 hit, latency ~Ll) only
+// (AS - BS) blocks behind A block k (HBM, ~Ld ~ 2 Ll), so each ring bounds the
+// k-block rate: rate <= min(AS / Ld, BS / Ll).  Pick the split maximizing
+// min(AS, 2 BS) within the budget (measured: a 3-deep B ring capped one CTA at
+// ~48 GB/s however deep the A ring was).
+constexpr int ring_bs(int budget, int a_bytes, int b_bytes) {
+  int best_bs = 2, best = 0;
+  for (int bs = 2; bs <= 16; ++bs) {
+    const int as = (budget - bs * b_bytes) / a_bytes;
+    if (as < 2) break;
+    const int v = as < 2 * bs ? as : 2 * bs;
+    if (v > best || (v == best && as > (budget - best_bs * b_bytes) / a_bytes)) best = v, best_bs = bs;
+  }
+  return best_bs;
+}
+
 template <int BN, bool SWAP, int CTAS>
 struct GemmSmem {
   static constexpr int B_TILE_BYTES = BN * BK * 2;
   static constexpr int BUDGET = CTAS == 2 ? 104 * 1024 : 200 * 1024;
-  static constexpr int BS = SWAP ? 3 : BUDGET / (A_TILE_BYTES + B_TILE_BYTES);
+  static constexpr int BS = SWAP ? ring_bs(BUDGET, A_TILE_BYTES, B_TILE_BYTES)
+                                 : BUDGET / (A_TILE_BYTES + B_TILE_BYTES);
   static constexpr int AS = SWAP ? (BUDGET - BS * B_TILE_BYTES) / A_TILE_BYTES : BS;
   static constexpr int LAG = AS - BS;  // A (weights, SWAP) run this many k-blocks ahead of B
   static constexpr int B_OFFSET = AS * A_TILE_BYTES;
