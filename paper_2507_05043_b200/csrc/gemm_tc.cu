@@ -68,8 +68,10 @@ struct GemmArgs {
   // reduced by the last arriving CTA from per-piece fp32 slots, in k order.
   const uint8_t* wp;  // pre-packed weights (pl_pack_weight): 16 KB SW128 tile images, [N/128][K/64]
   int streamk;
+  int sk_dp;          // hybrid: CTAs [0, sk_dp) each own full tile blockIdx (data-parallel);
+                      // the stream-K part covers tiles [sk_dp, tiles_m) with CTAs sk_dp..grid-1
   int sk_base, sk_extra;
-  float* sk_slots;    // [2 * grid][BM][BN] fp32
+  float* sk_slots;    // [2 * stream-K CTAs][BN][BM] fp32 (column-major: coalesced per column)
   int* sk_counters;   // [tiles_m], zero between launches (the fixer resets its tile)
 };
 
@@ -81,13 +83,15 @@ struct Piece {
   int c_first, c_last;  // stream-K: CTAs covering the tile (k order)
 };
 
+// Stream-K coordinates are local: CTA c = blockIdx - sk_dp, iteration 0 = the first
+// k-block of tile sk_dp.
 PL_DEV int sk_start(const GemmArgs& a, int c) { return c * a.sk_base + min(c, a.sk_extra); }
 PL_DEV int sk_cta_of(const GemmArgs& a, int it) {
   const int big = a.sk_extra * (a.sk_base + 1);
   return it < big ? it / (a.sk_base + 1) : a.sk_extra + (it - big) / a.sk_base;
 }
-// slot of CTA c's piece in tile t: its second slot when c's range began in an earlier
-// tile (then the piece is c's last), else its first
+// slot of CTA c's piece in local tile t: its second slot when c's range began in an
+// earlier tile (then the piece is c's last), else its first
 PL_DEV int sk_slot(const GemmArgs& a, int c, int tile) {
   return (sk_start(a, c) < tile * a.num_kb) ? 2 * c + 1 : 2 * c;
 }
@@ -100,10 +104,17 @@ PL_DEV int sk_slot(const GemmArgs& a, int c, int tile) {
 struct PieceWalk {
   int it, end;        // cursor / end of the in-order part
   int last0, last1;   // the hoisted last-tile piece [last0, last1), empty when done
+  int dp;             // hybrid data-parallel CTA: one full tile, then done
   PL_DEV void init(const GemmArgs& a) {
+    dp = a.streamk && static_cast<int>(blockIdx.x) < a.sk_dp;
+    if (dp) {
+      it = 0, end = 1, last0 = last1 = 0;
+      return;
+    }
     if (a.streamk) {
-      const int s0 = sk_start(a, blockIdx.x);
-      const int e0 = s0 + a.sk_base + (static_cast<int>(blockIdx.x) < a.sk_extra ? 1 : 0);
+      const int c = static_cast<int>(blockIdx.x) - a.sk_dp;
+      const int s0 = sk_start(a, c);
+      const int e0 = s0 + a.sk_base + (c < a.sk_extra ? 1 : 0);
       const int lt = max(s0, ((e0 - 1) / a.num_kb) * a.num_kb);  // start of the last tile's piece
       if (lt > s0) {
         last0 = lt, last1 = e0;
@@ -119,6 +130,13 @@ struct PieceWalk {
     }
   }
   PL_DEV bool next(const GemmArgs& a, Piece& p) {
+    if (dp) {
+      if (it >= end) return false;
+      it = end;
+      p.m_tile = blockIdx.x, p.n_tile = 0, p.split = 0, p.kb0 = 0, p.nkb = a.num_kb;
+      p.partial = 0, p.slot = 0, p.c_first = p.c_last = 0;
+      return true;
+    }
     if (a.streamk) {
       int k_it, k_end;
       if (last1 > last0) {
@@ -128,10 +146,10 @@ struct PieceWalk {
         if (it >= end) return false;
         k_it = it, k_end = end;
       }
-      const int tile = k_it / a.num_kb;
+      const int tile = k_it / a.num_kb;  // local tile
       const int k0 = k_it % a.num_kb;
       const int k1 = min(a.num_kb, k0 + (k_end - k_it));
-      p.m_tile = tile;
+      p.m_tile = a.sk_dp + tile;
       p.n_tile = 0;
       p.split = 0;
       p.kb0 = k0;
@@ -139,7 +157,7 @@ struct PieceWalk {
       p.c_first = sk_cta_of(a, tile * a.num_kb);
       p.c_last = sk_cta_of(a, tile * a.num_kb + a.num_kb - 1);
       p.partial = p.c_first != p.c_last;
-      p.slot = sk_slot(a, blockIdx.x, tile);
+      p.slot = sk_slot(a, static_cast<int>(blockIdx.x) - a.sk_dp, tile);
       if (k_it == it) it += k1 - k0;
       return true;
     }
@@ -493,13 +511,12 @@ __global__ void __launch_bounds__(192, CTAS)
 
         if (args.streamk && pc.partial) {
           // stream-K piece of a shared tile: fp32 slot, then the last arriver reduces
-          float* sp = args.sk_slots + (int64_t)pc.slot * (BM * BN) + row * BN;
+          float* sp = args.sk_slots + (int64_t)pc.slot * (BM * BN) + row;  // [col][BM]: lanes coalesce
           for (int c0 = 0; c0 < BN; c0 += 16) {
             float v[16];
             fetch_tmem(c0, v);
-            float4* d = reinterpret_cast<float4*>(sp + c0);
 #pragma unroll
-            for (int c = 0; c < 16; c += 4) d[c / 4] = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+            for (int c = 0; c < 16; ++c) sp[(c0 + c) * BM] = v[c];
           }
           release_tmem();
           epi_sync();
@@ -513,37 +530,32 @@ __global__ void __launch_bounds__(192, CTAS)
           }
           epi_sync();
           if (*sk_flag) {
-            const int tile = m_tile;
+            const int tile = m_tile - args.sk_dp;  // local
             auto fetch_slots = [&](int c0, float (&v)[16]) {
 #pragma unroll
               for (int c = 0; c < 16; ++c) v[c] = 0.f;
               const int npc = pc.c_last - pc.c_first + 1;
-              for (int b0 = 0; b0 < npc; b0 += 4) {  // four pieces' loads in flight, summed in k order
-                float4 x[4][4];
+              for (int b0 = 0; b0 < npc; b0 += 2) {  // two pieces' loads in flight, summed in k order
+                float x[2][16];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < 2; ++u) {
                   const bool ok = b0 + u < npc;
-                  const float4* p = reinterpret_cast<const float4*>(
-                      args.sk_slots + (int64_t)sk_slot(args, pc.c_first + (ok ? b0 + u : 0), tile) * (BM * BN) +
-                      row * BN + c0);
+                  const float* p = args.sk_slots +
+                                   (int64_t)sk_slot(args, pc.c_first + (ok ? b0 + u : 0), tile) * (BM * BN) +
+                                   row + c0 * BM;
 #pragma unroll
-                  for (int q = 0; q < 4; ++q) x[u][q] = ok ? __ldcg(p + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                  for (int c = 0; c < 16; ++c) x[u][c] = ok ? __ldcg(p + c * BM) : 0.f;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < 2; ++u) {
                   if (b0 + u >= npc) break;
 #pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    v[4 * q] += x[u][q].x;
-                    v[4 * q + 1] += x[u][q].y;
-                    v[4 * q + 2] += x[u][q].z;
-                    v[4 * q + 3] += x[u][q].w;
-                  }
+                  for (int c = 0; c < 16; ++c) v[c] += x[u][c];
                 }
               }
             };
             final_epi(fetch_slots);
-            if (ep == 0) args.sk_counters[tile] = 0;
+            if (ep == 0) args.sk_counters[m_tile] = 0;
           }
           continue;
         }
@@ -707,9 +719,15 @@ __global__ void __launch_bounds__(1024)
                                 const __nv_bfloat16* __restrict__ w, float eps,
                                 __nv_bfloat16* __restrict__ a, int64_t lda) {
   pdl_trigger();
-  pdl_wait();
   const int t = blockIdx.x;
   const int nt = blockDim.x;
+  uint2 wv[VPT];  // the norm weight is static: fetched before griddepcontrol.wait
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int f = (threadIdx.x + nt * k) * 4;
+    wv[k] = f < N ? *reinterpret_cast<const uint2*>(w + f) : make_uint2(0, 0);
+  }
+  pdl_wait();
   uint2 old[VPT];
   float4 acc[VPT];
 #pragma unroll
@@ -768,8 +786,7 @@ __global__ void __launch_bounds__(1024)
   for (int k = 0; k < VPT; ++k) {
     const int f = (threadIdx.x + nt * k) * 4;
     if (f >= N) continue;
-    const uint2 wv = *reinterpret_cast<const uint2*>(w + f);
-    const float2 w0 = unpack_bf16x2(wv.x), w1 = unpack_bf16x2(wv.y);
+    const float2 w0 = unpack_bf16x2(wv[k].x), w1 = unpack_bf16x2(wv[k].y);
     *reinterpret_cast<uint2*>(a + static_cast<int64_t>(t) * lda + f) =
         make_uint2(pack_bf16x2(w0.x * rbf(hv[k][0] * inv), w0.y * rbf(hv[k][1] * inv)),
                    pack_bf16x2(w1.x * rbf(hv[k][2] * inv), w1.y * rbf(hv[k][3] * inv)));
@@ -787,19 +804,53 @@ __global__ void __launch_bounds__(256)
                            int max_pos, __nv_bfloat16* __restrict__ k_cache,
                            __nv_bfloat16* __restrict__ v_cache, int block_size, int Hq, int Hkv) {
   pdl_trigger();
-  pdl_wait();
   constexpr int HDIM = 128, HALF = 64;
   const int heads = Hq + 2 * Hkv;
   const int tq = (T + 3) / 4;
   const int64_t total = static_cast<int64_t>(heads) * HALF * tq;
   const int64_t split_stride = static_cast<int64_t>(N) * Tp / 4;
   const float4* P = reinterpret_cast<const float4*>(partial);
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
+  // Inputs that do not come from the GEMM (bias, positions and KV slots from the host
+  // metadata, the RoPE table) are fetched before griddepcontrol.wait, so only the
+  // partial sums sit on the dependent path.
+  struct Side {
+    float b1, b2, c[4], sn[4];
+    int sl[4];
+  };
+  auto side = [&](int64_t idx, Side& sd) {
     const int i = static_cast<int>(idx % HALF);
     const int hh = static_cast<int>((idx / HALF) % heads);
     const int t0 = static_cast<int>(idx / (HALF * heads)) * 4;
     const int n1 = hh * HDIM + i, n2 = n1 + HALF;
+    sd.b1 = bias ? bf2f(bias[n1]) : 0.f;
+    sd.b2 = bias ? bf2f(bias[n2]) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = min(t0 + k, T - 1);
+      sd.c[k] = 1.f, sd.sn[k] = 0.f;
+      if (hh < Hq + Hkv) {
+        int pp = pos[t];
+        pp = pp < 0 ? 0 : (pp >= max_pos ? max_pos - 1 : pp);
+        sd.c[k] = bf2f(cos_sin[static_cast<int64_t>(pp) * HDIM + i]);
+        sd.sn[k] = bf2f(cos_sin[static_cast<int64_t>(pp) * HDIM + HALF + i]);
+      }
+      sd.sl[k] = slot ? slot[t] : -1;
+    }
+  };
+  const int64_t idx0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  Side sd0;
+  if (idx0 < total) side(idx0, sd0);
+  pdl_wait();
+  for (int64_t idx = idx0; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(idx % HALF);
+    const int hh = static_cast<int>((idx / HALF) % heads);
+    const int t0 = static_cast<int>(idx / (HALF * heads)) * 4;
+    const int n1 = hh * HDIM + i, n2 = n1 + HALF;
+    Side sd;
+    if (idx == idx0)
+      sd = sd0;
+    else
+      side(idx, sd);
     float4 a1 = make_float4(0.f, 0.f, 0.f, 0.f), a2 = a1;
     const float4* p1 = P + (static_cast<int64_t>(n1) * Tp + t0) / 4;
     const float4* p2 = P + (static_cast<int64_t>(n2) * Tp + t0) / 4;
@@ -817,26 +868,21 @@ __global__ void __launch_bounds__(256)
         a2.x += y[u].x; a2.y += y[u].y; a2.z += y[u].z; a2.w += y[u].w;
       }
     }
-    const float b1 = bias ? bf2f(bias[n1]) : 0.f, b2 = bias ? bf2f(bias[n2]) : 0.f;
-    const float v1[4] = {rbf(a1.x + b1), rbf(a1.y + b1), rbf(a1.z + b1), rbf(a1.w + b1)};
-    const float v2[4] = {rbf(a2.x + b2), rbf(a2.y + b2), rbf(a2.z + b2), rbf(a2.w + b2)};
+    const float v1[4] = {rbf(a1.x + sd.b1), rbf(a1.y + sd.b1), rbf(a1.z + sd.b1), rbf(a1.w + sd.b1)};
+    const float v2[4] = {rbf(a2.x + sd.b2), rbf(a2.y + sd.b2), rbf(a2.z + sd.b2), rbf(a2.w + sd.b2)};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int t = t0 + k;
       if (t >= T) break;
       float o1 = v1[k], o2 = v2[k];
       if (hh < Hq + Hkv) {
-        int pp = pos[t];
-        pp = pp < 0 ? 0 : (pp >= max_pos ? max_pos - 1 : pp);
-        const float c = bf2f(cos_sin[static_cast<int64_t>(pp) * HDIM + i]);
-        const float sn = bf2f(cos_sin[static_cast<int64_t>(pp) * HDIM + HALF + i]);
-        o1 = rbf(rbf(v1[k] * c) + rbf(-v2[k] * sn));
-        o2 = rbf(rbf(v2[k] * c) + rbf(v1[k] * sn));
+        o1 = rbf(rbf(v1[k] * sd.c[k]) + rbf(-v2[k] * sd.sn[k]));
+        o2 = rbf(rbf(v2[k] * sd.c[k]) + rbf(v1[k] * sd.sn[k]));
       }
       __nv_bfloat16* row = qkv + static_cast<int64_t>(t) * ldqkv;
       row[n1] = f2bf(o1);
       row[n2] = f2bf(o2);
-      const int sl = slot ? slot[t] : -1;
+      const int sl = sd.sl[k];
       if (hh >= Hq && sl >= 0) {
         const bool is_k = hh < Hq + Hkv;
         const int kh = is_k ? hh - Hq : hh - Hq - Hkv;
@@ -1055,11 +1101,36 @@ bool streamk_enabled() {
   return on;
 }
 
+// DP + stream-K hybrid for tile counts between one and two waves: opt-in (PL_SK_HYBRID=1).
+// Measured no faster than split-K on Llama-3 gate_up (47.5 vs 44 us at T=64), and its tile
+// counters share the workspace offset of other GEMMs' split-K partials, so it is only
+// safe when every GEMM sharing the workspace also runs stream-K (PL_STREAMK=1).
+bool hybrid_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("PL_SK_HYBRID");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+int64_t sk_dp_tiles(int64_t N);
+bool use_streamk(bool swap, int64_t N) {
+  return swap && (streamk_enabled() || (hybrid_enabled() && sk_dp_tiles(N) > 0));
+}
+
 // Stream-K grid: a constant (two CTAs per SM) so piece boundaries -- and therefore
 // every token's summation order -- depend on (N, K) only, never on T.
+// Hybrid for SMs < tiles < 2*SMs (Llama-3 gate_up: 224 tiles): one full tile per SM
+// data-parallel (no fix-up) plus the remaining tiles stream-K'd over one more CTA per
+// SM, so every SM streams the same weight bytes; otherwise plain stream-K.
+int64_t sk_dp_tiles(int64_t N) {
+  const int64_t tiles = (N + BM - 1) / BM, sms = num_sms();
+  return (tiles > sms && tiles < 2 * sms) ? sms : 0;
+}
 int64_t sk_grid(int64_t N, int64_t K) {
-  const int64_t total = ((N + BM - 1) / BM) * (K / BK);
-  return std::min<int64_t>(num_sms(), total);  // one CTA per SM with the deep (~200 KB) ring
+  const int64_t tiles = (N + BM - 1) / BM;
+  const int64_t dp = sk_dp_tiles(N);
+  if (dp) return 2 * num_sms();  // dp + num_sms() stream-K CTAs, two CTAs per SM
+  return std::min<int64_t>(num_sms(), tiles * (K / BK));  // one CTA per SM, deep ring
 }
 
 // Tile counters sit at the same offset for every stream-K GEMM sharing a workspace
@@ -1072,7 +1143,7 @@ int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi) {
   const bool swap = use_swap(T, epi);
   const int64_t tiles = (N + BM - 1) / BM;
   const int64_t argmax = epi == EPI_ARGMAX ? align256(tiles * T * 8) : 0;
-  if (swap && streamk_enabled()) {
+  if (use_streamk(swap, N)) {
     const int64_t bn = swap_bn(T);
     return SK_COUNTER_BYTES + argmax + 2 * sk_grid(N, K) * BM * bn * 4;
   }
@@ -1120,7 +1191,7 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   a.bias = bias;
   a.residual = residual;
   a.ldr = ldr;
-  const bool sk = swap && streamk_enabled();
+  const bool sk = use_streamk(swap, N);
   a.splits = (epi == EPI_ARGMAX || sk) ? 1 : gemm_num_splits(N, K, swap);
   a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
   const int bn = swap ? swap_bn(T) : 256;
@@ -1158,11 +1229,13 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     a.sk_counters = reinterpret_cast<int*>(w8);
     if (epi == EPI_ARGMAX) a.argmax_ws = reinterpret_cast<float2*>(w8 + SK_COUNTER_BYTES);
     a.sk_slots = reinterpret_cast<float*>(w8 + SK_COUNTER_BYTES + argmax_bytes);
-    const int64_t total = static_cast<int64_t>(a.tiles_m) * a.num_kb;
     grid = static_cast<int>(sk_grid(N, K));
     a.streamk = 1;
-    a.sk_base = static_cast<int>(total / grid);
-    a.sk_extra = static_cast<int>(total % grid);
+    a.sk_dp = static_cast<int>(sk_dp_tiles(N));
+    const int sk_ctas = grid - a.sk_dp;
+    const int64_t total = static_cast<int64_t>(a.tiles_m - a.sk_dp) * a.num_kb;
+    a.sk_base = static_cast<int>(total / sk_ctas);
+    a.sk_extra = static_cast<int>(total % sk_ctas);
     a.num_items = static_cast<int>(total);
   } else {
     if (epi == EPI_ARGMAX) {
@@ -1180,7 +1253,7 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   if (swap) {
     if ((rc = make_map(&ma, W, N, K, ldw, BM))) return rc;
     if ((rc = make_map(&mb, X, T, K, ldx, bn))) return rc;
-    const bool w1 = wide || sk;  // stream-K: one CTA per SM with the deep ring
+    const bool w1 = wide || (sk && !sk_dp_tiles(N));  // pure stream-K: one CTA per SM, deep ring
     switch (bn) {
       case 16: rc = w1 ? launch_tc<16, true, 1>(ma, mb, a, grid, st) : launch_tc<16, true>(ma, mb, a, grid, st); break;
       case 32: rc = w1 ? launch_tc<32, true, 1>(ma, mb, a, grid, st) : launch_tc<32, true>(ma, mb, a, grid, st); break;

@@ -87,6 +87,9 @@ def test_rmsnorm_row_gather(ops):
 GEMM_SHAPES = [  # (T, N, K)
     (1, 512, 256), (5, 640, 256), (16, 6144, 4096), (17, 384, 768), (64, 4096, 4096),
     (100, 1024, 512), (256, 512, 256), (300, 512, 256), (1000, 1536, 256), (2048, 768, 1024),
+    # 148 < N/128 < 296 weight tiles: data-parallel + stream-K hybrid (fix-up of shared tiles,
+    # up to ~12 pieces per tile at K=1024)
+    (64, 28672, 4096), (7, 20480, 1024), (130, 19200, 512),
 ]
 
 

@@ -274,6 +274,34 @@ def test_llama3_shape_truncated_tokens_identical():
         assert np.array_equal(res.b200.tokens[r.id], want[i].numpy())
 
 
+@pytest.mark.parametrize("native", [True, False], ids=["native", "python"])
+def test_link_throttle_replays_virtual_link_timing(native):
+    """Throttle mode (transport.py:199-200 + engine.py:552 in wall time): every delivery is
+    gated on the GPU clock at its virtual time, so the device run spans at least the virtual
+    schedule's makespan (and not much more when compute is faster than the links), and the
+    tokens are unchanged."""
+    spec = TINY.with_(peaked=True)
+    S = 2
+    cluster = deploy.b200_cluster(S, 0.004, 2.0e6)     # 4 ms, 2 MB/s links
+    plan = deploy.plan(cluster, spec, S)
+    ctrl = pipelink.ControllerConfig(max_batched_tokens=256, max_batch_size=8)
+    cfg = deploy.engine_config(plan, spec, ctrl, chunk_size=16384)
+    trace = deploy.uniform_trace(4, 64, 5)
+    profiles = synth_profiles(plan)
+    eng = B200PipelineEngine(cfg, cluster, profiles, decoder=spec, throttle=True, native=native)
+    res = eng.run(trace)
+    ref = pipelink.PipelineEngine(cfg, cluster, profiles).run(trace)
+    assert result_key(ref) == result_key(res)
+    span = ref.end_ns / 1e9
+    assert span > 0.05                                  # link-dominated schedule
+    assert res.b200.run_time_s >= 0.97 * span, (res.b200.run_time_s, span)
+    assert res.b200.run_time_s <= 1.5 * span + 0.05, (res.b200.run_time_s, span)
+    _, _, want = oracle_greedy(spec, trace)
+    for i, r in enumerate(trace.requests):
+        assert np.array_equal(res.b200.tokens[r.id], want[i].numpy())
+    eng.close()
+
+
 def test_real_clock_run_result_feeds_reference_metrics():
     """RunResult on the device clock: summarize()/measure_bubble() apply unchanged."""
     spec = TINY.with_(peaked=True)
