@@ -1147,12 +1147,14 @@ int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi) {
     const int64_t bn = swap_bn(T);
     return SK_COUNTER_BYTES + argmax + 2 * sk_grid(N, K) * BM * bn * 4;
   }
-  if (epi == EPI_ARGMAX) return tiles * T * 8;
+  // split-K partials / argmax partials sit after the (untouched) stream-K counter region,
+  // so GEMMs of either kind can share one workspace
+  if (epi == EPI_ARGMAX) return SK_COUNTER_BYTES + tiles * T * 8;
   const int splits = gemm_num_splits(N, K, swap);
   if (splits <= 1) return 0;
   const int64_t bn = swap_bn(T);
   const int64_t tiles_n = (T + bn - 1) / bn;
-  return static_cast<int64_t>(splits) * N * (tiles_n * bn) * 4;
+  return SK_COUNTER_BYTES + static_cast<int64_t>(splits) * N * (tiles_n * bn) * 4;
 }
 
 int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int64_t ldw,
@@ -1239,9 +1241,9 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     a.num_items = static_cast<int>(total);
   } else {
     if (epi == EPI_ARGMAX) {
-      a.argmax_ws = reinterpret_cast<float2*>(ws);
+      a.argmax_ws = reinterpret_cast<float2*>(static_cast<uint8_t*>(ws) + SK_COUNTER_BYTES);
     } else if (a.splits > 1) {
-      a.partial = reinterpret_cast<float*>(ws);
+      a.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + SK_COUNTER_BYTES);
     }
     static const int per_sm_env = [] { const char* v = getenv("PL_GRID_PER_SM"); return v ? atoi(v) : 0; }();
     const int per_sm = per_sm_env > 0 ? per_sm_env : (swap && bn <= 128 && !wide) ? 2 : 1;

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
 def test_pure_host_queries():
     lib = N.lib()
     # argmax partials = tiles * T * 8; split-K partials = splits * N * Tp * 4
-    assert lib.pl_gemm_workspace_bytes(16, 128256, 4096, N.EPI_ARGMAX) == 1002 * 16 * 8
+    assert lib.pl_gemm_workspace_bytes(16, 128256, 4096, N.EPI_ARGMAX) == 65536 + 1002 * 16 * 8
     assert lib.pl_gemm_workspace_bytes(300, 4096, 4096, N.EPI_NONE) == 0   # prefill: no split-K
     # decode splits: ceil(pages / 16) per request -- context-length driven only
     assert lib.pl_attn_decode_workspace_bytes(16, 32, 1024, 128) == 0
