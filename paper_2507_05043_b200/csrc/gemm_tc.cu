@@ -318,40 +318,65 @@ __global__ void __launch_bounds__(192, CTAS)
           pb ^= 1;
         }
       };
+      // Two independent streams, one thread each, so neither waits behind the other's
+      // ring: lane 0 streams the weights (never produced by the previous kernel, so no
+      // PDL wait -- they flow while the predecessor drains), lane 1 the activations
+      // (after griddepcontrol.wait).  A single issuing thread coupled the rings: an
+      // activation load could only go out once a weight slot freed, which left the MMA
+      // waiting on L2 latency every few k-blocks.
+      PieceWalk walk;
+      walk.init(args);
+      Piece pc;
       bool first = true;
+      while (walk.next(args, pc)) {
+        const int m_tile = pc.m_tile, n_tile = pc.n_tile, kb0 = pc.kb0, nkb = pc.nkb;
+        if (SWAP && first && args.l2_prefetch) {
+          const int pf_end = min(nkb, AS + args.l2_prefetch);
+          for (int j = AS; j < pf_end; ++j) {
+            if (args.wp)
+              bulk_prefetch_l2(args.wp + ((int64_t)m_tile * args.num_kb + kb0 + j) * A_TILE_BYTES, A_TILE_BYTES);
+            else
+              tma_prefetch_l2_2d(&tmA, (kb0 + j) * BK, m_tile * BM);
+          }
+        }
+        first = false;
+        for (int i = 0; i < nkb; ++i) {
+          if (SWAP) issue_a(kb0 + i, m_tile);
+          else issue_b(kb0 + i, n_tile);
+        }
+      }
+    } else if (lane == 1) {
+      const uint64_t pol_x = policy_evict_last();
+      const uint64_t polA = pol_x, polB = pol_x;
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      pdl_wait();  // activations come from the previous kernel
       PieceWalk walk;
       walk.init(args);
       Piece pc;
       while (walk.next(args, pc)) {
         const int m_tile = pc.m_tile, n_tile = pc.n_tile, kb0 = pc.kb0, nkb = pc.nkb;
-        int pre = 0;  // weight blocks issued ahead of the PDL wait
-        if (first) {
-          // Weights never depend on the previous kernel: fill the weight ring before
-          // waiting on it (PDL), and warm L2 with the weight blocks beyond the ring.
-          first = false;
-          pre = min(nkb, SWAP ? AS : BS);
-          for (int j = 0; j < pre; ++j) {
-            if (SWAP) issue_a(kb0 + j, m_tile);
-            else issue_b(kb0 + j, n_tile);
-          }
+        for (int i = 0; i < nkb; ++i) {
+          const int kb = kb0 + i;
           if (SWAP) {
-            const int pf_end = min(nkb, pre + args.l2_prefetch);
-            for (int j = pre; j < pf_end; ++j) {
-              if (args.wp)
-                bulk_prefetch_l2(args.wp + ((int64_t)m_tile * args.num_kb + kb0 + j) * A_TILE_BYTES, A_TILE_BYTES);
-              else
-                tma_prefetch_l2_2d(&tmA, (kb0 + j) * BK, m_tile * BM);
+            mbar_wait(&emptyB[sb], pb ^ 1);
+            mbar_arrive_expect_tx(&fullB[sb], L::B_TILE_BYTES);
+            tma_load_2d(smem + L::B_OFFSET + sb * L::B_TILE_BYTES, &tmB, &fullB[sb], kb * BK, n_tile * BN, polB);
+            if (++sb == BS) {
+              sb = 0;
+              pb ^= 1;
+            }
+          } else {
+            mbar_wait(&emptyA[sa], pa ^ 1);
+            mbar_arrive_expect_tx(&fullA[sa], A_TILE_BYTES);
+            tma_load_2d(smem + sa * A_TILE_BYTES, &tmA, &fullA[sa], kb * BK, m_tile * BM, polA);
+            if (++sa == AS) {
+              sa = 0;
+              pa ^= 1;
             }
           }
-          pdl_wait();
-        }
-        for (int i = 0; i < nkb + L::LAG; ++i) {
-          if (i < nkb && !(SWAP && i < pre)) issue_a(kb0 + i, m_tile);
-          const int j = i - L::LAG;
-          if (j >= 0 && j < nkb && !(!SWAP && j < pre)) issue_b(kb0 + j, n_tile);
         }
       }
-      if (first) pdl_wait();
     }
     __syncwarp();
   } else if (warp == 1) {
