@@ -1,4 +1,4 @@
-"""Live two-stage pipeline over NVLink with real B200 compute.
+"""Live pipeline over NVLink with real B200 compute (one stage per rank, S >= 2).
 
 Twin of the reference's ``run_socket_demo`` (pipelink/demo.py:52-196): the head
 loop runs the unchanged ``choose_n`` + ``admit_and_batch`` on every step and
@@ -7,7 +7,8 @@ the micro-batch composition is timing dependent exactly as in the reference
 demo; what must match the virtual run is the token
 accounting -- and here also the generated ids.  Differences from the socket
 demo: each stage is a real decoder stage on its own GPU (one process per GPU,
-``torch.distributed`` world of 2), the links are ``DeviceLinkSender`` /
+``torch.distributed`` world of S; the socket demo has exactly two stages), the
+links are ``DeviceLinkSender`` /
 ``DeviceLinkReceiver`` over NCCL, and the forward payload carries the
 micro-batch metadata ahead of the bf16 residual stream (the socket demo
 prefixes a 4-byte request count, demo.py:161-163).
@@ -55,33 +56,40 @@ class _Requests:
         self._requests = {r.id: r for r in reqs}
 
 
-def _comm_pair():
+def _hop_comms(S: int) -> dict:
+    """One 2-rank communicator per hop: forward hops s -> s+1 and the return hop
+    S-1 -> 0 (the sender is comm-rank 0).  Returns {hop: handle} for this rank's hops;
+    hop S-1 is the return hop."""
     import torch.distributed as dist
 
-    comms = []
-    for src in (0, 1):  # forward link (0 -> 1), return link (1 -> 0)
+    me = dist.get_rank()
+    hops = [(s, s + 1) for s in range(S - 1)] + [(S - 1, 0)]
+    comms = {}
+    for hop, (src, dst) in enumerate(hops):
         obj = [None]
-        if dist.get_rank() == src:
+        if me == src:
             buf = (C.c_uint8 * 128)()
             N.call("pl_nccl_unique_id", buf, 128)
             obj = [bytes(buf)]
         dist.broadcast_object_list(obj, src=src)
-        uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
-        h = C.c_void_p()
-        N.call("pl_comm_init_rank", uid, 2, 0 if dist.get_rank() == src else 1, C.byref(h))
-        comms.append(h)
-    # Establish both P2P connections now, from one thread, in the same order on both
-    # ranks: NCCL connects lazily on first use, and a connect issued while the other
+        if me in (src, dst):
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+            h = C.c_void_p()
+            N.call("pl_comm_init_rank", uid, 2, 0 if me == src else 1, C.byref(h))
+            comms[hop] = h
+    # Establish every P2P connection now, from one thread, in the same order on all
+    # ranks: NCCL connects lazily on first use, and a connect issued while another
     # link's receive kernel spins on the same GPU can wait on that kernel forever.
     dev = torch.device("cuda", torch.cuda.current_device())
     buf = torch.zeros(8, dtype=torch.int64, device=dev)
     st = torch.cuda.Stream(dev)
-    for src, h in zip((0, 1), comms):
-        if dist.get_rank() == src:
-            N.call("pl_p2p_send", h, buf.data_ptr(), 64, 1, st.cuda_stream)
-        else:
-            N.call("pl_p2p_recv", h, buf.data_ptr(), 64, 0, st.cuda_stream)
+    for hop, (src, dst) in enumerate(hops):
+        if me == src:
+            N.call("pl_p2p_send", comms[hop], buf.data_ptr(), 64, 1, st.cuda_stream)
+        elif me == dst:
+            N.call("pl_p2p_recv", comms[hop], buf.data_ptr(), 64, 0, st.cuda_stream)
         st.synchronize()
+        dist.barrier()
     return comms
 
 
@@ -89,26 +97,31 @@ def run_device_demo(cfg, cluster, stage_profiles, trace, *, decoder, seed: int =
                     timeout_s: float = 120.0) -> LiveResult | None:
     import torch.distributed as dist
 
-    if len(cfg.partition.stages) != 2 or not dist.is_initialized() or dist.get_world_size() != 2:
-        raise pipelink.ConfigError("the live demo runs exactly two stages on a world of 2 ranks")
+    S = len(cfg.partition.stages)
+    if S < 2 or not dist.is_initialized() or dist.get_world_size() != S:
+        raise pipelink.ConfigError("the live demo runs one stage per rank (world size == stages >= 2)")
     rank = dist.get_rank()
     names = cfg.partition.node_names()
-    link_profiles = [cluster.link(names[0], names[1]), cluster.link(names[1], names[0])]
+    link_profiles = [cluster.link(a, b) for a, b in list(zip(names, names[1:])) + [(names[-1], names[0])]]
     policy = (pipelink.LinkPolicy.DECODE_PRIORITY
               if cfg.scheduling_policy.value == "decode_priority" else pipelink.LinkPolicy.FCFS)
     bytes_per_token = cfg.model.hidden_dim * cfg.model.dtype_bytes
-    placement = Placement(2, 2, rank)
+    placement = Placement(S, S, rank)
     be = GpuBackend(decoder, cfg, placement, seed=seed)
     requests = {r.id: r.fresh_copy() for r in trace.requests}
     view = _Requests(requests.values())
     be.start(view, trace)
     exe = be.exe[rank]
     dev = exe.device
-    comm_fwd, comm_ret = _comm_pair()
-    if rank == 1:
-        _tail(be, exe, comm_fwd, comm_ret, cfg, policy, timeout_s)
+    comms = _hop_comms(S)
+    comm_ret = comms[S - 1]
+    if rank == S - 1:
+        _tail(be, exe, comms[S - 2], comm_ret, cfg, policy, timeout_s)
         return None
-    return _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profiles,
+    if rank > 0:
+        _middle(exe, comms[rank - 1], comms[rank], cfg, policy, timeout_s)
+        return None
+    return _head(be, exe, comms[0], comm_ret, cfg, policy, requests, trace, stage_profiles,
                  link_profiles, bytes_per_token, timeout_s, dev)
 
 
@@ -143,6 +156,38 @@ def _tail(be, exe, comm_fwd, comm_ret, cfg, policy, timeout_s):
     ret.join(timeout=timeout_s)
     if recv.failed:
         raise pipelink.ProtocolError(f"tail receiver failed: {recv.error!r}")
+
+
+def _middle(exe, comm_in, comm_out, cfg, policy, timeout_s):
+    """A stage between head and tail: receive [header | metadata | residual stream],
+    run the stage forward in place, pass the same framing on to the next rank."""
+    nxt = DeviceLinkSender(comm_out, 1, cfg.chunk_size, policy, "mid-sender", exe.device)
+    nxt.start()
+    stream = exe.stream
+
+    def on_payload(p):
+        hdr = p.body[: HDR * 4].view(torch.int32).cpu().numpy()
+        T, R, phase, max_seqlen, max_ctx, slot, meta_len = (int(x) for x in hdr[:7])
+        off = HDR * 4 + meta_len * 4
+        with torch.cuda.stream(stream):
+            stream.wait_stream(torch.cuda.current_stream())
+            exe.meta_dev[:meta_len].view(torch.uint8).copy_(p.body[HDR * 4: off])
+            exe.hidden[slot][:T].view(torch.uint8).reshape(-1).copy_(p.body[off:])
+        exe.forward(slot, T, R, phase == 1, max_seqlen, max_ctx)
+        with torch.cuda.stream(stream):
+            p.body[off:].copy_(exe.hidden[slot][:T].view(torch.uint8).reshape(-1))  # reuse the frame
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        out = pipelink.Payload(id=p.payload_id, phase_class=p.phase_class, size_bytes=p.body.numel(),
+                               micro_batch_id=p.payload_id, enqueue_time=0)
+        nxt.send(out, p.body, ready=ev)
+
+    recv = DeviceLinkReceiver(comm_in, 0, on_payload, "mid-recv", exe.device)
+    recv.run()  # inline: this thread is the stage
+    nxt.close()
+    nxt.join(timeout=timeout_s)
+    if recv.failed:
+        raise pipelink.ProtocolError(f"stage receiver failed: {recv.error!r}")
 
 
 def _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profiles, link_profiles,

@@ -1,6 +1,6 @@
-"""Live 2-stage NVLink pipeline (run_device_demo) vs the virtual engine and the CPU oracle.
+"""Live S-stage NVLink pipeline (run_device_demo) vs the virtual engine and the CPU oracle.
 
-    torchrun --nproc-per-node 2 scripts/check_live.py
+    torchrun --nproc-per-node S scripts/check_live.py      (S = 2 or 4 stages, one per rank)
 
 Criterion-11 analog (test_acceptance.py:367-381): per-request token counts of the
 live run equal the virtual run's; additionally the generated ids equal the CPU
@@ -29,9 +29,10 @@ def main():
     from paper_2507_05043_b200.spec import prompt_tokens
     import pipelink as PL
 
+    S = dist.get_world_size()  # one stage per rank
     spec = TINY.with_(peaked=True)
-    cluster = deploy.b200_cluster(2)
-    plan = deploy.plan(cluster, spec, 2)
+    cluster = deploy.b200_cluster(S)
+    plan = deploy.plan(cluster, spec, S)
     cfg = deploy.engine_config(plan, spec, PL.ControllerConfig(max_batched_tokens=256, max_batch_size=8),
                                chunk_size=4096)
     trace = PL.Trace(requests=[PL.Request(i, 0.0, 40 + 7 * i, 6 + (i % 5)) for i in range(20)])
@@ -49,7 +50,7 @@ def main():
             want, _ = model.greedy([torch.from_numpy(prompt_tokens(0, r.id, r.input_len, spec.vocab))],
                                    r.output_len)
             bad += not np.array_equal(res.tokens[r.id], want[0].numpy())
-        print(f"live 2-stage NVLink run: {res.microbatches} micro-batches in {res.wall_s:.2f} s; "
+        print(f"live {S}-stage NVLink run: {res.microbatches} micro-batches in {res.wall_s:.2f} s; "
               f"token counts {'==' if counts_ok else '!='} virtual; "
               f"{len(trace.requests) - bad}/{len(trace.requests)} requests identical to the oracle", flush=True)
         ok = counts_ok and bad == 0

@@ -54,3 +54,8 @@ def test_two_ranks_four_stages_llama3_width():
 def test_live_nvlink_pipeline_token_parity():
     out = torchrun("check_live.py")
     assert "token counts == virtual" in out and "20/20 requests identical" in out
+
+
+def test_live_nvlink_pipeline_four_stages():
+    out = torchrun("check_live.py", nproc=4)
+    assert "live 4-stage" in out and "token counts == virtual" in out and "20/20 requests identical" in out
