@@ -114,7 +114,7 @@ def run_device_demo(cfg, cluster, stage_profiles, trace, *, decoder, seed: int =
     exe = be.exe[rank]
     dev = exe.device
     comms = _hop_comms(S)
-    comm_ret = comms[S - 1]
+    comm_ret = comms.get(S - 1)  # the return hop: tail and head only
     if rank == S - 1:
         _tail(be, exe, comms[S - 2], comm_ret, cfg, policy, timeout_s)
         return None
