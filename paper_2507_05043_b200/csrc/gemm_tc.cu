@@ -67,6 +67,7 @@ struct GemmArgs {
   // [c*base + min(c, extra), +base + (c < extra)); tiles shared by several CTAs are
   // reduced by the last arriving CTA from per-piece fp32 slots, in k order.
   const uint8_t* wp;  // pre-packed weights (pl_pack_weight): 16 KB SW128 tile images, [N/128][K/64]
+  int swiglu_il;      // packed gate_up: rows alternate gate_j, up_j inside each 128-row tile
   int streamk;
   int sk_dp;          // hybrid: CTAs [0, sk_dp) each own full tile blockIdx (data-parallel);
                       // the stream-K part covers tiles [sk_dp, tiles_m) with CTAs sk_dp..grid-1
@@ -455,7 +456,21 @@ __global__ void __launch_bounds__(192, CTAS)
         const int t_base = n_tile * BN;
         // the tile's final epilogue, accumulator values from `fetch(c0, v[16])`
         auto final_epi = [&](auto fetch) {
-          if (epi == EPI_SWIGLU) {
+          if (epi == EPI_SWIGLU && args.swiglu_il) {
+            // interleaved rows: lane pairs (gate_j, up_j) meet by one shuffle, no smem
+            const int j = m_tile * 64 + (row >> 1);
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float v[16];
+              fetch(c0, v);
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const float other = __shfl_xor_sync(0xffffffffu, v[c], 1);
+                const int t = t_base + c0 + c;
+                if (!(row & 1) && t < args.T)
+                  args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(rbf(v[c]))) * rbf(other));
+              }
+            }
+          } else if (epi == EPI_SWIGLU) {
             // rows [0,64) gate, [64,128) up of the same 64 output features
             const int j = m_tile * 64 + (row & 63);
             for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -616,7 +631,26 @@ __global__ void __launch_bounds__(192, CTAS)
         // lane <-> token t, column <-> feature n   (splits == 1 on this path)
         const int t = m_tile * BM + row;
         const bool tv = t < args.T;
-        if (epi == EPI_SWIGLU) {
+        if (epi == EPI_SWIGLU && args.swiglu_il) {
+          // interleaved columns (gate_j, up_j): 16 accumulator columns -> 8 outputs
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tcol + c0, r);
+            tmem_ld_wait();
+            const int j0 = (n_tile * BN + c0) / 2;
+            if (tv && n_tile * BN + c0 < args.N) {
+              uint32_t packed[4];
+#pragma unroll
+              for (int c = 0; c < 16; c += 4) {
+                const float g0 = rbf(__uint_as_float(r[c])), u0 = rbf(__uint_as_float(r[c + 1]));
+                const float g1 = rbf(__uint_as_float(r[c + 2])), u1 = rbf(__uint_as_float(r[c + 3]));
+                packed[c / 4] = pack_bf16x2(rbf(silu_f(g0)) * u0, rbf(silu_f(g1)) * u1);
+              }
+              *reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + j0) =
+                  make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            }
+          }
+        } else if (epi == EPI_SWIGLU) {
           for (int p = 0; p < BN / 128; ++p) {
             for (int c0 = 0; c0 < 64; c0 += 16) {
               uint32_t g[16], u[16];
@@ -688,7 +722,7 @@ __global__ void __launch_bounds__(256)
     gemm_splitk_reduce_kernel(const float* __restrict__ partial, int splits, int T, int Tp, int N,
                               int epi, __nv_bfloat16* __restrict__ C, int64_t ldc,
                               const __nv_bfloat16* __restrict__ bias,
-                              const __nv_bfloat16* __restrict__ residual, int64_t ldr) {
+                              const __nv_bfloat16* __restrict__ residual, int64_t ldr, int swiglu_il) {
   pdl_trigger();
   pdl_wait();
   const int n_out = (epi == EPI_SWIGLU) ? N / 2 : N;
@@ -700,7 +734,8 @@ __global__ void __launch_bounds__(256)
        i += (int64_t)gridDim.x * blockDim.x) {
     const int j = static_cast<int>(i % n_out);   // consecutive threads -> consecutive features
     const int t0 = static_cast<int>(i / n_out) * 4;
-    const int n = (epi == EPI_SWIGLU) ? (j / 64) * 128 + (j % 64) : j;
+    const int n = (epi == EPI_SWIGLU) ? (j / 64) * 128 + (swiglu_il ? 2 * (j % 64) : j % 64) : j;
+    const int64_t up_off = (swiglu_il ? 1 : 64) * static_cast<int64_t>(Tp) / 4;  // up row, in float4
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), up = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4* p = P + (static_cast<int64_t>(n) * Tp + t0) / 4;
 #pragma unroll 4
@@ -708,7 +743,7 @@ __global__ void __launch_bounds__(256)
       const float4 x = p[s * split_stride];
       acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
       if (epi == EPI_SWIGLU) {
-        const float4 u = p[s * split_stride + 64 * Tp / 4];
+        const float4 u = p[s * split_stride + up_off];
         up.x += u.x; up.y += u.y; up.z += u.z; up.w += u.w;
       }
     }
@@ -1210,6 +1245,7 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     if (N % 256 || ldw != K)
       return set_error(PL_ERR_CONFIG, "gemm: packed weights need N %% 256 == 0 and ldw == K");
     a.wp = reinterpret_cast<const uint8_t*>(W);
+    a.swiglu_il = epi == EPI_SWIGLU;  // pack_weight interleaves gate/up rows
   }
   a.num_kb = static_cast<int>(K / BK);
   a.epi = epi;
@@ -1338,7 +1374,7 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     const int64_t total = n_out * ((T + 3) / 4);
     const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
     return launch_k("gemm_splitk_reduce_kernel", gemm_splitk_reduce_kernel, dim3(blocks), dim3(256), 0,
-                    st, a.partial, a.splits, a.T, a.Tp, a.N, epi, C, ldc, bias, residual, ldr);
+                    st, a.partial, a.splits, a.T, a.Tp, a.N, epi, C, ldc, bias, residual, ldr, a.swiglu_il);
   }
   return PL_OK;
 }
@@ -1348,25 +1384,28 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
 // exact 128-byte-swizzled shared-memory image TMA would produce for a 128 x 64 box, so
 // the GEMM producer streams it with one contiguous bulk copy per k-block.
 __global__ void pack_weight_kernel(const __nv_bfloat16* __restrict__ W, int64_t ld, int64_t N, int64_t K,
-                                   uint8_t* __restrict__ out) {
+                                   uint8_t* __restrict__ out, int interleave) {
   const int64_t nkb = K / BK;
   const int64_t chunks = N * (K / 8);  // 16-byte chunks
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = i / (K / 8), kc = i % (K / 8);
-    const int64_t mt = n / BM, r = n % BM, kb = kc / 8, c = kc % 8;
+    const int64_t mt = n / BM, kb = kc / 8, c = kc % 8;
+    int64_t r = n % BM;
+    if (interleave) r = r < 64 ? 2 * r : 2 * (r - 64) + 1;  // [gate 64 | up 64] -> gate_j, up_j pairs
     const uint4 v = *reinterpret_cast<const uint4*>(W + n * ld + kc * 8);
     uint8_t* d = out + (mt * nkb + kb) * A_TILE_BYTES + r * 128 + ((c ^ (r & 7)) << 4);
     *reinterpret_cast<uint4*>(d) = v;
   }
 }
 
-int pack_weight_launch(const __nv_bfloat16* W, int64_t ld, int64_t N, int64_t K, void* out, cudaStream_t st) {
+int pack_weight_launch(const __nv_bfloat16* W, int64_t ld, int64_t N, int64_t K, void* out, cudaStream_t st,
+                       bool interleave_swiglu) {
   if (N % 256 || K % BK || ld % 8)
     return set_error(PL_ERR_CONFIG, "pack_weight: N %% 256, K %% 64 and ld %% 8 must be 0");
   const int64_t chunks = N * (K / 8);
   const int blocks = static_cast<int>(std::min<int64_t>((chunks + 255) / 256, 148 * 16));
-  pack_weight_kernel<<<blocks, 256, 0, st>>>(W, ld, N, K, static_cast<uint8_t*>(out));
+  pack_weight_kernel<<<blocks, 256, 0, st>>>(W, ld, N, K, static_cast<uint8_t*>(out), interleave_swiglu ? 1 : 0);
   return check_launch("pack_weight_kernel");
 }
 

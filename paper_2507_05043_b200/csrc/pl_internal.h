@@ -81,7 +81,10 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
                 int epi, void* ws, int64_t ws_bytes, int64_t* argmax_out, cudaStream_t st,
                 const FusedEpi* fuse = nullptr, bool* fused = nullptr, bool w_packed = false);
 // W [N, K] -> pre-swizzled 16 KB tiles (see gemm_tc.cu); out may not alias W
-int pack_weight_launch(const __nv_bfloat16* W, int64_t ld, int64_t N, int64_t K, void* out, cudaStream_t st);
+// interleave_swiglu: [gate 64 | up 64] row blocks become (gate_j, up_j) row pairs (the
+// packed SwiGLU epilogue pairs them with one shuffle)
+int pack_weight_launch(const __nv_bfloat16* W, int64_t ld, int64_t N, int64_t K, void* out, cudaStream_t st,
+                       bool interleave_swiglu = false);
 
 // per-file eager kernel loading (pl_preload_kernels)
 int attention_preload();

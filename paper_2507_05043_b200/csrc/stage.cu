@@ -99,24 +99,24 @@ struct Stage {
     cudaError_t e = cudaMalloc(&tmp, biggest);
     if (e != cudaSuccess) return set_cuda_error(e, "pack_weights: temp");
     int rc = PL_OK;
-    auto pack_one = [&](void* w, int64_t N, int64_t K) {
+    auto pack_one = [&](void* w, int64_t N, int64_t K, bool swiglu) {
       if (rc || !w) return;
       e = cudaMemcpyAsync(tmp, w, N * K * 2, cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) {
         rc = set_cuda_error(e, "pack_weights: copy");
         return;
       }
-      rc = pack_weight_launch(static_cast<const __nv_bfloat16*>(tmp), K, N, K, w, st);
+      rc = pack_weight_launch(static_cast<const __nv_bfloat16*>(tmp), K, N, K, w, st, swiglu);
     };
     for (const Job& j : jobs) {
       if (j.N <= 0 || j.N % 256 || j.K % 64 || *j.flag) continue;
       if (j.flag == &pk_lm) {
-        pack_one(const_cast<void*>(c.lm_head), j.N, j.K);
+        pack_one(const_cast<void*>(c.lm_head), j.N, j.K, false);
       } else {
         for (auto& lw : layers) {
           const void* w = j.flag == &pk_qkv ? lw.w_qkv : j.flag == &pk_o ? lw.w_o : j.flag == &pk_gu ? lw.w_gate_up
                                                                                                  : lw.w_down;
-          pack_one(const_cast<void*>(w), j.N, j.K);
+          pack_one(const_cast<void*>(w), j.N, j.K, j.flag == &pk_gu);
         }
       }
       if (rc) break;
