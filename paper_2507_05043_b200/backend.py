@@ -59,6 +59,7 @@ class _MbRec:
     ids: np.ndarray | None
     scatter: np.ndarray  # int32 [req_slot R | out_pos R]
     rids: tuple = ()
+    n_decode: int = 0    # mixed batch: leading decode requests (rows [0, n_decode))
 
 
 class Placement:
@@ -189,9 +190,6 @@ class GpuBackend(Backend):
 
     # ------------------------------------------------------------ driver hooks
     def start(self, driver, trace) -> None:
-        if self.cfg.allow_mixed_phase:
-            raise pipelink.ConfigError("mixed prefill/decode micro-batches run on the native runtime "
-                                       "only (B200PipelineEngine(native=True))")
         self.driver = driver
         self.prepare(trace)
         reqs = trace.requests
@@ -234,8 +232,6 @@ class GpuBackend(Backend):
         slot = self.free_slots.pop()
         R = len(mb.request_ids)
         decode = mb.phase is BatchPhase.DECODE
-        if mb.phase is BatchPhase.MIXED:
-            raise pipelink.ConfigError("mixed micro-batch reached the B200 backend")
         reqs = [self.driver._requests[rid] for rid in mb.request_ids]
         rows = np.empty((R, self.max_blocks), dtype=np.int32)
         for i, r in enumerate(reqs):
@@ -261,6 +257,30 @@ class GpuBackend(Backend):
             rec = _MbRec(slot, T, R, True, 1, int(ctx.max()), meta, None,
                          np.concatenate([ridx, out_pos]).astype(np.int32), mb.request_ids)
             self.mb_log.append(("decode", R, int(ctx.sum())))
+        elif mb.phase is BatchPhase.MIXED:
+            # admit_and_batch places decoders ahead of prompts (engine.py:184-198)
+            nd = 0
+            while nd < R and reqs[nd].state is RequestState.DECODING:
+                nd += 1
+            if nd == 0 or any(r.state is RequestState.DECODING for r in reqs[nd:]):
+                raise pipelink.ProtocolError("mixed micro-batch must lead with its decoders")
+            dpos = np.array([r.input_len + r.tokens_emitted - 1 for r in reqs[:nd]], dtype=np.int64)
+            plens = np.array([r.input_len for r in reqs[nd:]], dtype=np.int64)
+            lens = np.concatenate([np.ones(nd, dtype=np.int64), plens])
+            T = int(lens.sum())
+            cu = np.zeros(R + 1, dtype=np.int64)
+            np.cumsum(lens, out=cu[1:])
+            ppos = np.arange(int(plens.sum()), dtype=np.int64) - np.repeat(cu[nd:-1] - nd, plens)
+            pos = np.concatenate([dpos, ppos])
+            req_of = np.repeat(np.arange(R), lens)
+            slots = rows[req_of, pos // BLOCK_SIZE].astype(np.int64) * BLOCK_SIZE + pos % BLOCK_SIZE
+            ctx = np.concatenate([dpos + 1, plens])
+            meta = build_meta(T, R, self.max_blocks, pos, slots, np.repeat(ridx, lens), cu, ctx,
+                              cu[1:] - 1, rows)
+            ids = np.concatenate([np.zeros(nd, dtype=np.int64)] + [self.prompts[r.id] for r in reqs[nd:]])
+            rec = _MbRec(slot, T, R, False, int(plens.max()), int((dpos + 1).max()), meta, ids,
+                         np.concatenate([ridx, out_pos]).astype(np.int32), mb.request_ids, n_decode=nd)
+            self.mb_log.append(("mixed", R, T))
         else:
             lens = np.array([r.input_len for r in reqs], dtype=np.int64)
             T = int(lens.sum())
@@ -292,7 +312,7 @@ class GpuBackend(Backend):
             st.wait_event(self.ev_send[s][k])
         if s > 0 and self.ev_recv[s][k] is not None:
             st.wait_event(self.ev_recv[s][k])
-        if s == 0 and rec.decode and self.fb_events:
+        if s == 0 and (rec.decode or rec.n_decode) and self.fb_events:
             st.wait_event(self.fb_events[-1][0])
             if self.first_decode_ev is None:
                 self.first_decode_ev = torch.cuda.Event(enable_timing=True)
@@ -311,7 +331,7 @@ class GpuBackend(Backend):
         t_start = torch.cuda.Event(enable_timing=True)
         t_start.record(st)
         exe.forward(k, rec.T, rec.R, rec.decode, rec.max_seqlen, rec.max_ctx,
-                    last_token=self.last_token if (s == 0) else None)
+                    last_token=self.last_token if (s == 0) else None, n_decode=rec.n_decode)
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(st)
         self.busy_events.append((s, mb.id, t_start, ev))  # ev also marks the payload's enqueue

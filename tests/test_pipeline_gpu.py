@@ -227,7 +227,8 @@ def test_stage_counts_on_one_gpu(S, native):
         assert np.array_equal(res.b200.tokens[r.id], want[i].numpy())
 
 
-def test_mixed_prefill_decode_microbatches():
+@pytest.mark.parametrize("native", [True, False], ids=["native", "python"])
+def test_mixed_prefill_decode_microbatches(native):
     """allow_mixed_phase=True (engine.py:184-198): decoders and late-arriving prompts share
     micro-batches; schedule == pipelink's, tokens == the oracle's."""
     spec = TINY.with_(peaked=True)
@@ -237,7 +238,7 @@ def test_mixed_prefill_decode_microbatches():
     cfg = deploy.engine_config(plan, spec, ctrl, chunk_size=4096, allow_mixed_phase=True)
     trace = pipelink.Trace(requests=[pipelink.Request(i, 0.0001 * i, 40 + 9 * i, 7) for i in range(8)])
     profiles = synth_profiles(plan)
-    eng = B200PipelineEngine(cfg, cluster, profiles, decoder=spec, seed=0)
+    eng = B200PipelineEngine(cfg, cluster, profiles, decoder=spec, seed=0, native=native)
     res = eng.run(trace)
     ref = pipelink.PipelineEngine(cfg, cluster, profiles).run(trace)
     a, b = result_key(ref), result_key(res)
