@@ -1278,10 +1278,6 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     return (v ? atoll(v) : 64) << 20;
   }();
   a.l2_prefetch = (swap && N * K * 2 <= l2pf_max) ? l2pf : 0;
-  // experiment: warm L2 with the whole K-range only for GEMMs whose K is the widest
-  // (down-proj: launched while gate_up's single-tile SMs sit idle)
-  static const int l2pf_wide = [] { const char* v = getenv("PL_L2PF_WIDEK"); return v ? atoi(v) : 0; }();
-  if (swap && l2pf_wide && K >= 4 * N / 2) a.l2_prefetch = l2pf_wide;
   const int64_t need = gemm_workspace_bytes(T, N, K, epi);
   if (need > 0 && (ws_bytes < need || !ws))
     return set_error(PL_ERR_CONFIG, "gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,

@@ -36,7 +36,7 @@ def _meta_for(exe: StageExecutor, T: int, decode: bool, ctx: int):
                           pos + 1, np.arange(R), rows)
         del nb
         return meta, R, 1, ctx
-    L = min(T, 512)
+    L = min(T, 512, exe.max_blocks * BLOCK_SIZE)  # prompts must fit the stage's block tables
     R = max(1, T // L)
     lens = np.full(R, T // R, dtype=np.int64)
     lens[-1] += T - lens.sum()
@@ -82,7 +82,8 @@ def profile_stage(exe: StageExecutor, decode_points=DECODE_POINTS, prefill_point
         if T <= min(exe.max_reqs, exe.max_tokens):
             entries[(Phase.DECODE, T)] = round(time_forward(exe, T, True, ctx), 7)
     for T in prefill_points:
-        if T <= exe.max_tokens:
+        L = min(T, 512, exe.max_blocks * BLOCK_SIZE)
+        if T <= exe.max_tokens and max(1, T // L) <= exe.max_reqs:
             entries[(Phase.PREFILL, T)] = round(time_forward(exe, T, False, ctx), 7)
     # the reference requires >= 2 monotone points per phase (profiles.py:38-64)
     for ph in (Phase.DECODE, Phase.PREFILL):
