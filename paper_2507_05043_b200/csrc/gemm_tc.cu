@@ -189,12 +189,15 @@ struct PieceWalk {
 // k-block rate: rate <= min(AS / Ld, BS / Ll).  Pick the split maximizing
 // min(AS, 2 BS) within the budget (measured: a 3-deep B ring capped one CTA at
 // ~48 GB/s however deep the A ring was).
+#ifndef PL_RING_RATIO
+#define PL_RING_RATIO 1
+#endif
 constexpr int ring_bs(int budget, int a_bytes, int b_bytes) {
   int best_bs = 2, best = 0;
   for (int bs = 2; bs <= 16; ++bs) {
     const int as = (budget - bs * b_bytes) / a_bytes;
     if (as < 2) break;
-    const int v = as < 2 * bs ? as : 2 * bs;
+    const int v = as < PL_RING_RATIO * bs ? as : PL_RING_RATIO * bs;
     if (v > best || (v == best && as > (budget - best_bs * b_bytes) / a_bytes)) best = v, best_bs = bs;
   }
   return best_bs;
@@ -204,17 +207,19 @@ template <int BN, bool SWAP, int CTAS>
 struct GemmSmem {
   static constexpr int B_TILE_BYTES = BN * BK * 2;
   static constexpr int BUDGET = CTAS == 2 ? 104 * 1024 : 200 * 1024;
-  static constexpr int BS = SWAP ? ring_bs(BUDGET, A_TILE_BYTES, B_TILE_BYTES)
-                                 : BUDGET / (A_TILE_BYTES + B_TILE_BYTES);
-  static constexpr int AS = SWAP ? (BUDGET - BS * B_TILE_BYTES) / A_TILE_BYTES : BS;
-  static constexpr int LAG = AS - BS;  // A (weights, SWAP) run this many k-blocks ahead of B
+  static constexpr int BS0 = SWAP ? ring_bs(BUDGET, A_TILE_BYTES, B_TILE_BYTES)
+                                  : BUDGET / (A_TILE_BYTES + B_TILE_BYTES);
+  static constexpr int AS = SWAP ? (BUDGET - BS0 * B_TILE_BYTES) / A_TILE_BYTES : BS0;
+  // left-over budget deepens the activation ring (its L2 latency caps the k-block rate too)
+  static constexpr int BS_FILL = SWAP ? (BUDGET - AS * A_TILE_BYTES) / B_TILE_BYTES : BS0;
+  static constexpr int BS = BS_FILL > 16 ? 16 : BS_FILL;
   static constexpr int B_OFFSET = AS * A_TILE_BYTES;
   static constexpr int BAR_OFFSET = B_OFFSET + BS * B_TILE_BYTES;
   // fullA[AS], emptyA[AS], fullB[BS], emptyB[BS], tmem_full[2], tmem_empty[2], tmem slot + flag
   static constexpr int SCRATCH_OFFSET = BAR_OFFSET + 8 * (2 * AS + 2 * BS + 4) + 16;
   static constexpr int SCRATCH_BYTES = 64 * 16 * 4;  // swiglu exchange / argmax partials
   static constexpr int TOTAL = SCRATCH_OFFSET + SCRATCH_BYTES + 1024;  // + alignment slack
-  static_assert(AS >= 2 && BS >= 2 && LAG >= 0, "ring too shallow");
+  static_assert(AS >= 2 && BS >= 2, "ring too shallow");
 };
 
 PL_DEV float silu_f(float x) { return x / (1.0f + expf(-x)); }

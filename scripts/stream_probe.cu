@@ -11,6 +11,7 @@
 //   3: bulk copies + LDGSTS together (half the bytes each)
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define DEV __device__ __forceinline__
@@ -32,9 +33,12 @@ DEV void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
                ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(b)) : "memory");
 }
 
-constexpr int STAGE = 16384, NST = 12;
+#ifndef NSTAGES
+#define NSTAGES 12
+#endif
+constexpr int STAGE = 16384, NST = NSTAGES;
 
-__global__ void __launch_bounds__(256, 1) probe(const uint8_t* __restrict__ src, int64_t per_cta, int mode,
+__global__ void __launch_bounds__(256) probe(const uint8_t* __restrict__ src, int64_t per_cta, int mode,
                                                   float* sink) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + NST * STAGE);
@@ -89,9 +93,10 @@ ldgsts:
   if (acc == 1.2345f) sink[0] = acc;
 }
 
-int main() {
-  const int64_t per_cta = 16ll << 20;  // 16 MB per CTA
-  const int64_t total = per_cta * 148;
+int main(int argc, char** argv) {
+  // usage: stream_probe [per_cta_KB [grid ...]]
+  const int64_t per_cta = (argc > 1 ? atoll(argv[1]) : 16384) << 10;
+  const int64_t total = per_cta * 296;
   uint8_t* buf;
   float* sink;
   cudaMalloc(&buf, total);
@@ -103,8 +108,14 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const char* names[4] = {"bulk(TMA)", "cp.async", "ld.global.v4", "bulk+cp.async"};
+  int grids[8] = {37, 74, 148}, ng = 3;
+  if (argc > 2) {
+    ng = 0;
+    for (int i = 2; i < argc && ng < 8; ++i) grids[ng++] = atoi(argv[i]);
+  }
   for (int mode = 0; mode < 4; ++mode)
-    for (int grid : {37, 74, 148}) {
+    for (int gi = 0; gi < ng; ++gi) {
+      const int grid = grids[gi];
       probe<<<grid, 256, smem>>>(buf, per_cta, mode, sink);
       cudaEventRecord(a);
       for (int r = 0; r < 3; ++r) probe<<<grid, 256, smem>>>(buf, per_cta, mode, sink);
@@ -113,8 +124,9 @@ int main() {
       float ms;
       cudaEventElapsedTime(&ms, a, b);
       const double bytes = 3.0 * grid * per_cta;
-      printf("%-14s grid %3d: %7.1f GB/s total, %6.1f GB/s per SM  (%s)\n", names[mode], grid,
-             bytes / (ms * 1e-3) / 1e9, bytes / (ms * 1e-3) / 1e9 / grid, cudaGetErrorString(cudaGetLastError()));
+      printf("%-14s grid %3d x %6lld KB: %7.2f us/launch, %7.1f GB/s total  (%s)\n", names[mode], grid,
+             (long long)(per_cta >> 10), ms * 1e3 / 3, bytes / (ms * 1e-3) / 1e9,
+             cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
 }
