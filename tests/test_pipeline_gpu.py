@@ -275,6 +275,34 @@ def test_llama3_shape_truncated_tokens_identical():
         assert np.array_equal(res.b200.tokens[r.id], want[i].numpy())
 
 
+def test_qwen2_shape_truncated_tokens_identical():
+    """Qwen2-72B widths (d=8192, GQA 64/8 -> group 8, qkv bias, ffn 29568, V=152064),
+    2 layers, 2 stages: bias epilogues and the G=8 attention path end to end."""
+    from paper_2507_05043_b200 import QWEN2_72B
+
+    spec = QWEN2_72B.with_(num_layers=2, peaked=True)
+    cfg, cluster, plan, trace = config1(spec, S=2, n_req=3, in_len=80, out_len=5, mbt=512)
+    res = run_gpu(spec, cfg, cluster, plan, trace)
+    _, _, want = oracle_greedy(spec, trace)
+    for i, r in enumerate(trace.requests):
+        assert np.array_equal(res.b200.tokens[r.id], want[i].numpy()), f"request {r.id}"
+
+
+def test_long_context_split_decode_attention_tokens_identical():
+    """Prompts of 1100-1300 tokens: decode contexts exceed 1024, so each (request, kv head)
+    splits into two items merged by the last arriver -- end to end through the pipeline."""
+    spec = TINY.with_(peaked=True)
+    cluster = deploy.b200_cluster(2)
+    plan = deploy.plan(cluster, spec, 2)
+    ctrl = pipelink.ControllerConfig(max_batched_tokens=4096, max_batch_size=4)
+    cfg = deploy.engine_config(plan, spec, ctrl)
+    trace = pipelink.Trace(requests=[pipelink.Request(i, 0.0, 1100 + 70 * i, 6) for i in range(4)])
+    res = run_gpu(spec, cfg, cluster, plan, trace)
+    _, _, want = oracle_greedy(spec, trace)
+    for i, r in enumerate(trace.requests):
+        assert np.array_equal(res.b200.tokens[r.id], want[i].numpy()), f"request {r.id}"
+
+
 @pytest.mark.parametrize("native", [True, False], ids=["native", "python"])
 def test_link_throttle_replays_virtual_link_timing(native):
     """Throttle mode (transport.py:199-200 + engine.py:552 in wall time): every delivery is
