@@ -13,6 +13,14 @@ reference (engine.py:264-294, 509-600), plus the decoder shape the reference
 cannot know (its ModelSpec has no heads/FFN/vocab).  Under ``torchrun`` each
 rank constructs the engine identically and owns ``S / world_size`` contiguous
 stages; hops between ranks are NCCL P2P.
+
+By default (``native=True``) ``run`` hands the whole event loop to the C++
+scheduler (csrc/sched.cu), whose hooks issue every per-micro-batch GPU action
+in C++ (csrc/runtime.cu); ``native=False`` runs the Python twin
+(driver.PipelineDriver + backend.GpuBackend).  Both give the identical
+schedule and tokens.  Extra keywords: ``throttle=True`` replays the virtual
+link timing on the GPU clock; ``prompts={rid: ids}`` overrides the synthetic
+prompts; ``devices=[...]`` spreads stages over local GPUs without torchrun.
 """
 
 from __future__ import annotations
