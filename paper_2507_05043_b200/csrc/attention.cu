@@ -47,11 +47,17 @@ PL_DEV void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, u
 // 64 x 128 bf16 tile, rows of 256 B = 16 chunks of 16 B, chunk c of row r at c ^ (r & 7).
 PL_DEV uint32_t swz(int row, int chunk) { return row * 256 + ((chunk ^ (row & 7)) << 4); }
 
-PL_DEV void load_tile_64x128(uint8_t* smem, const __nv_bfloat16* base, int64_t ld, int rows_valid) {
-  // 64 rows x 16 chunks = 1024 chunks, 8 per thread
+// One CTA = 128 query rows = the G query heads of one kv head x (128 / G) positions,
+// so each K/V tile staged in shared memory serves all G heads of the group (GQA):
+// 8 warps of 16 rows, FA2-style online softmax on m16n8k16 tensor cores, K/V
+// double-buffered by cp.async.
+constexpr int PF_ROWS = 128, PF_THREADS = 256;
+
+PL_DEV void load_kv_tile(uint8_t* smem, const __nv_bfloat16* base, int64_t ld, int rows_valid) {
+  // 64 rows x 16 chunks = 1024 chunks, 4 per thread
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int c = threadIdx.x + i * 128;
+  for (int i = 0; i < 4; ++i) {
+    const int c = threadIdx.x + i * PF_THREADS;
     const int row = c >> 4, ch = c & 15;
     const bool ok = row < rows_valid;
     const __nv_bfloat16* src = base + (ok ? static_cast<int64_t>(row) * ld : 0) + ch * 8;
@@ -59,38 +65,50 @@ PL_DEV void load_tile_64x128(uint8_t* smem, const __nv_bfloat16* base, int64_t l
   }
 }
 
-__global__ void __launch_bounds__(128, 2)
+__global__ void __launch_bounds__(PF_THREADS, 2)
     attn_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldqkv,
                         const int32_t* __restrict__ cu_seqlens, int Hq, int Hkv, float scale_log2,
                         __nv_bfloat16* __restrict__ out, int64_t ldo) {
   extern __shared__ uint8_t smem_raw[];
   pdl_trigger();
   pdl_wait();
-  uint8_t* sQ = smem_raw;                 // 16 KB
-  uint8_t* sK = smem_raw + 16384;         // 2 x 16 KB
-  uint8_t* sV = smem_raw + 16384 * 3;     // 2 x 16 KB
+  uint8_t* sQ = smem_raw;                 // 128 rows x 256 B = 32 KB
+  uint8_t* sK = smem_raw + 32768;         // 2 x 16 KB
+  uint8_t* sV = smem_raw + 32768 * 2;     // 2 x 16 KB
 
-  const int r = blockIdx.z, h = blockIdx.y;
+  const int r = blockIdx.z, kh = blockIdx.y;
+  const int G = Hq / Hkv;
+  const int QT = PF_ROWS / G;             // positions per head in this CTA
   const int seq0 = cu_seqlens[r];
   const int L = cu_seqlens[r + 1] - seq0;
-  const int q0 = blockIdx.x * 64;
+  const int q0 = blockIdx.x * QT;
   if (q0 >= L) return;
-  const int kh = h / (Hq / Hkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  const __nv_bfloat16* qbase = qkv + static_cast<int64_t>(seq0 + q0) * ldqkv + h * HD;
   const __nv_bfloat16* kbase = qkv + static_cast<int64_t>(seq0) * ldqkv + (Hq + kh) * HD;
   const __nv_bfloat16* vbase = qkv + static_cast<int64_t>(seq0) * ldqkv + (Hq + Hkv + kh) * HD;
 
-  const int q_hi = min(q0 + 64, L);          // exclusive
+  const int q_hi = min(q0 + QT, L);          // exclusive
   const int n_kv_tiles = (q_hi + 63) / 64;   // causal: keys < q_hi
 
-  load_tile_64x128(sQ, qbase, ldqkv, q_hi - q0);
-  load_tile_64x128(sK, kbase, ldqkv, min(64, L));
-  load_tile_64x128(sV, vbase, ldqkv, min(64, L));
+  // Q: row rho = head (kh G + rho / QT) at position q0 + rho % QT
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = threadIdx.x + i * PF_THREADS;
+    const int row = c >> 4, ch = c & 15;
+    const int pos = q0 + row % QT;
+    const bool ok = pos < L;
+    const __nv_bfloat16* src =
+        qkv + static_cast<int64_t>(seq0 + (ok ? pos : 0)) * ldqkv + (kh * G + row / QT) * HD + ch * 8;
+    cp_async16_zfill(sQ + swz(row, ch), src, ok);
+  }
+  load_kv_tile(sK, kbase, ldqkv, min(64, L));
+  load_kv_tile(sV, vbase, ldqkv, min(64, L));
   cp_async_commit();
 
-  // Q fragments for this warp's 16 rows: 8 k-steps x 4 regs
+  // this warp's 16 rows: one head, 16 consecutive positions
+  const int head_g = (warp * 16) / QT;
+  const int pos0 = q0 + (warp * 16) % QT;
   uint32_t qf[8][4];
   float o[16][4];
 #pragma unroll
@@ -105,10 +123,10 @@ __global__ void __launch_bounds__(128, 2)
     const int buf = j & 1;
     if (j + 1 < n_kv_tiles) {
       const int kv0 = (j + 1) * 64;
-      load_tile_64x128(sK + (buf ^ 1) * 16384, kbase + static_cast<int64_t>(kv0) * ldqkv, ldqkv,
-                       min(64, L - kv0));
-      load_tile_64x128(sV + (buf ^ 1) * 16384, vbase + static_cast<int64_t>(kv0) * ldqkv, ldqkv,
-                       min(64, L - kv0));
+      load_kv_tile(sK + (buf ^ 1) * 16384, kbase + static_cast<int64_t>(kv0) * ldqkv, ldqkv,
+                   min(64, L - kv0));
+      load_kv_tile(sV + (buf ^ 1) * 16384, vbase + static_cast<int64_t>(kv0) * ldqkv, ldqkv,
+                   min(64, L - kv0));
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -123,89 +141,91 @@ __global__ void __launch_bounds__(128, 2)
         ldmatrix_x4(qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], sQa + swz(row, ch));
       }
     }
-    // S = Q K^T  (16 rows x 64 keys per warp)
-    float s[8][4];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
-    const uint32_t kt = sKa + buf * 16384;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-      for (int nt = 0; nt < 8; nt += 2) {
-        uint32_t b0, b1, b2, b3;
-        const int row = nt * 8 + (mi >> 1) * 8 + ri;
-        const int ch = ks * 2 + (mi & 1);
-        ldmatrix_x4(b0, b1, b2, b3, kt + swz(row, ch));
-        mma_bf16_16816(s[nt], qf[ks], b0, b1);
-        mma_bf16_16816(s[nt + 1], qf[ks], b2, b3);
-      }
-    }
-    // causal + length mask, online softmax (base 2)
     const int kv0 = j * 64;
-    const int qrow0 = q0 + warp * 16 + (lane >> 2);
-    float mx[2] = {-INFINITY, -INFINITY};
+    if (kv0 <= pos0 + 15) {  // tiles wholly above this warp's rows contribute nothing
+      // S = Q K^T  (16 rows x 64 keys per warp)
+      float s[8][4];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
+      for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+      const uint32_t kt = sKa + buf * 16384;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int qi = qrow0 + (e >> 1) * 8;
-        const int kj = kv0 + nt * 8 + (lane & 3) * 2 + (e & 1);
-        float v = s[nt][e] * scale_log2;
-        if (kj > qi || kj >= L) v = -INFINITY;
-        s[nt][e] = v;
-        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+        for (int nt = 0; nt < 8; nt += 2) {
+          uint32_t b0, b1, b2, b3;
+          const int row = nt * 8 + (mi >> 1) * 8 + ri;
+          const int ch = ks * 2 + (mi & 1);
+          ldmatrix_x4(b0, b1, b2, b3, kt + swz(row, ch));
+          mma_bf16_16816(s[nt], qf[ks], b0, b1);
+          mma_bf16_16816(s[nt + 1], qf[ks], b2, b3);
+        }
       }
-    }
-    float corr[2];
+      // causal + length mask, online softmax (base 2)
+      const int qrow0 = pos0 + (lane >> 2);
+      float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 1));
-      mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 2));
-      const float m_new = fmaxf(m_r[hr], mx[hr]);
-      corr[hr] = (m_new == -INFINITY) ? 1.f : exp2f(m_r[hr] - m_new);
-      m_r[hr] = m_new;
-    }
-    float rs[2] = {0.f, 0.f};
+      for (int nt = 0; nt < 8; ++nt) {
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int hr = e >> 1;
-        const float p = (m_r[hr] == -INFINITY) ? 0.f : exp2f(s[nt][e] - m_r[hr]);
-        s[nt][e] = p;
-        rs[hr] += p;
+        for (int e = 0; e < 4; ++e) {
+          const int qi = qrow0 + (e >> 1) * 8;
+          const int kj = kv0 + nt * 8 + (lane & 3) * 2 + (e & 1);
+          float v = s[nt][e] * scale_log2;
+          if (kj > qi || kj >= L) v = -INFINITY;
+          s[nt][e] = v;
+          mx[e >> 1] = fmaxf(mx[e >> 1], v);
+        }
       }
-    }
+      float corr[2];
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 1);
-      rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 2);
-      l_r[hr] = l_r[hr] * corr[hr] + rs[hr];
-    }
+      for (int hr = 0; hr < 2; ++hr) {
+        mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 1));
+        mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 2));
+        const float m_new = fmaxf(m_r[hr], mx[hr]);
+        corr[hr] = (m_new == -INFINITY) ? 1.f : exp2f(m_r[hr] - m_new);
+        m_r[hr] = m_new;
+      }
+      float rs[2] = {0.f, 0.f};
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      o[nt][0] *= corr[0];
-      o[nt][1] *= corr[0];
-      o[nt][2] *= corr[1];
-      o[nt][3] *= corr[1];
-    }
-    // O += P V
-    const uint32_t vt = sVa + buf * 16384;
+      for (int nt = 0; nt < 8; ++nt) {
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {  // 16 keys per k-step
-      uint32_t a[4];
-      a[0] = pack_bf16x2(s[2 * ks][0], s[2 * ks][1]);
-      a[1] = pack_bf16x2(s[2 * ks][2], s[2 * ks][3]);
-      a[2] = pack_bf16x2(s[2 * ks + 1][0], s[2 * ks + 1][1]);
-      a[3] = pack_bf16x2(s[2 * ks + 1][2], s[2 * ks + 1][3]);
+        for (int e = 0; e < 4; ++e) {
+          const int hr = e >> 1;
+          const float p = (m_r[hr] == -INFINITY) ? 0.f : exp2f(s[nt][e] - m_r[hr]);
+          s[nt][e] = p;
+          rs[hr] += p;
+        }
+      }
 #pragma unroll
-      for (int nt = 0; nt < 16; nt += 2) {
-        uint32_t b0, b1, b2, b3;
-        const int row = ks * 16 + (mi & 1) * 8 + ri;
-        const int ch = nt + (mi >> 1);
-        ldmatrix_x4_trans(b0, b1, b2, b3, vt + swz(row, ch));
-        mma_bf16_16816(o[nt], a, b0, b1);
-        mma_bf16_16816(o[nt + 1], a, b2, b3);
+      for (int hr = 0; hr < 2; ++hr) {
+        rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 1);
+        rs[hr] += __shfl_xor_sync(0xffffffffu, rs[hr], 2);
+        l_r[hr] = l_r[hr] * corr[hr] + rs[hr];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+        o[nt][0] *= corr[0];
+        o[nt][1] *= corr[0];
+        o[nt][2] *= corr[1];
+        o[nt][3] *= corr[1];
+      }
+      // O += P V
+      const uint32_t vt = sVa + buf * 16384;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {  // 16 keys per k-step
+        uint32_t a[4];
+        a[0] = pack_bf16x2(s[2 * ks][0], s[2 * ks][1]);
+        a[1] = pack_bf16x2(s[2 * ks][2], s[2 * ks][3]);
+        a[2] = pack_bf16x2(s[2 * ks + 1][0], s[2 * ks + 1][1]);
+        a[3] = pack_bf16x2(s[2 * ks + 1][2], s[2 * ks + 1][3]);
+#pragma unroll
+        for (int nt = 0; nt < 16; nt += 2) {
+          uint32_t b0, b1, b2, b3;
+          const int row = ks * 16 + (mi & 1) * 8 + ri;
+          const int ch = nt + (mi >> 1);
+          ldmatrix_x4_trans(b0, b1, b2, b3, vt + swz(row, ch));
+          mma_bf16_16816(o[nt], a, b0, b1);
+          mma_bf16_16816(o[nt + 1], a, b2, b3);
+        }
       }
     }
     __syncthreads();
@@ -214,10 +234,10 @@ __global__ void __launch_bounds__(128, 2)
   // normalize and store
 #pragma unroll
   for (int hr = 0; hr < 2; ++hr) {
-    const int qi = q0 + warp * 16 + (lane >> 2) + hr * 8;
+    const int qi = pos0 + (lane >> 2) + hr * 8;
     if (qi >= L) continue;
     const float inv = l_r[hr] > 0.f ? 1.f / l_r[hr] : 0.f;
-    __nv_bfloat16* orow = out + static_cast<int64_t>(seq0 + qi) * ldo + h * HD;
+    __nv_bfloat16* orow = out + static_cast<int64_t>(seq0 + qi) * ldo + (kh * G + head_g) * HD;
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) {
       const int col = nt * 8 + (lane & 3) * 2;
@@ -233,8 +253,11 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
   if (R <= 0 || max_seqlen <= 0) return PL_OK;
   if (hd != HD) return set_error(PL_ERR_CONFIG, "attention: head_dim must be 128 (got %d)", hd);
   if (Hkv <= 0 || Hq % Hkv) return set_error(PL_ERR_CONFIG, "attention: Hq must be a multiple of Hkv");
+  const int G = Hq / Hkv;
+  if (G > 8 || PF_ROWS % (16 * G))
+    return set_error(PL_ERR_CONFIG, "attention prefill: GQA group %d unsupported (1, 2, 4, 8)", G);
   if (ldqkv % 8 || ldo % 8) return set_error(PL_ERR_CONFIG, "attention: leading dims % 8");
-  constexpr int smem = 16384 * 5;
+  constexpr int smem = 32768 * 3;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_prefill_kernel,
@@ -242,8 +265,9 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
     if (e != cudaSuccess) return set_cuda_error(e, "attn_prefill smem attribute");
     attr = true;
   }
-  dim3 grid((max_seqlen + 63) / 64, Hq, R);
-  return launch_k("attn_prefill_kernel", attn_prefill_kernel, grid, dim3(128), smem, st, qkv, ldqkv,
+  const int QT = PF_ROWS / G;
+  dim3 grid((max_seqlen + QT - 1) / QT, Hkv, R);
+  return launch_k("attn_prefill_kernel", attn_prefill_kernel, grid, dim3(PF_THREADS), smem, st, qkv, ldqkv,
                   cu_seqlens, Hq, Hkv, scale * LOG2E, out, ldo);
 }
 
