@@ -249,6 +249,87 @@ PL_DEV void store_out(const GemmArgs& a, int epi, int t, int n, float acc) {
     a.C[(int64_t)t * a.ldc + n] = f2bf(acc);
 }
 
+// !SWAP (prefill) epilogue: TMEM lane <-> token t, accumulator column c <-> feature
+// n_tile * BN + c (split-K is never used on this path).
+template <int BN>
+PL_DEV void token_rows_epilogue(const GemmArgs& args, uint32_t tcol, int t, int n_tile) {
+  const int epi = args.epi;
+  const bool tv = t < args.T;
+  if (epi == EPI_SWIGLU && args.swiglu_il) {
+    // interleaved columns (gate_j, up_j): 16 accumulator columns -> 8 outputs
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld16(tcol + c0, r);
+      tmem_ld_wait();
+      const int j0 = (n_tile * BN + c0) / 2;
+      if (tv && n_tile * BN + c0 < args.N) {
+        uint32_t packed[4];
+#pragma unroll
+        for (int c = 0; c < 16; c += 4) {
+          const float g0 = rbf(__uint_as_float(r[c])), u0 = rbf(__uint_as_float(r[c + 1]));
+          const float g1 = rbf(__uint_as_float(r[c + 2])), u1 = rbf(__uint_as_float(r[c + 3]));
+          packed[c / 4] = pack_bf16x2(rbf(silu_f(g0)) * u0, rbf(silu_f(g1)) * u1);
+        }
+        *reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + j0) =
+            make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      }
+    }
+  } else if (epi == EPI_SWIGLU) {
+    for (int p = 0; p < BN / 128; ++p) {
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        uint32_t g[16], u[16];
+        tmem_ld16(tcol + p * 128 + c0, g);
+        tmem_ld16(tcol + p * 128 + 64 + c0, u);
+        tmem_ld_wait();
+        const int j0 = (n_tile * BN) / 2 + p * 64 + c0;
+        if (tv && (n_tile * BN + p * 128) < args.N) {
+          uint32_t packed[8];
+#pragma unroll
+          for (int c = 0; c < 16; c += 2) {
+            const float g0 = rbf(__uint_as_float(g[c])), g1 = rbf(__uint_as_float(g[c + 1]));
+            const float u0 = rbf(__uint_as_float(u[c])), u1 = rbf(__uint_as_float(u[c + 1]));
+            packed[c / 2] = pack_bf16x2(rbf(silu_f(g0)) * u0, rbf(silu_f(g1)) * u1);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + j0);
+          dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+        }
+      }
+    }
+  } else {
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld16(tcol + c0, r);
+      tmem_ld_wait();
+      const int n0 = n_tile * BN + c0;
+      if (!tv || n0 >= args.N) continue;
+      float v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(r[c]);
+      if (epi == EPI_BIAS) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] += bf2f(args.bias[n0 + c]);
+      } else if (epi == EPI_RESIDUAL) {
+        const uint4* rp = reinterpret_cast<const uint4*>(args.residual + (int64_t)t * args.ldr + n0);
+        const uint4 r0 = rp[0], r1 = rp[1];
+        const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) {
+          const float2 rv = unpack_bf16x2(rr[c / 2]);
+          v[c] = rbf(v[c]) + rv.x;
+          v[c + 1] = rbf(v[c + 1]) + rv.y;
+        }
+      }
+      uint32_t packed[8];
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) packed[c / 2] = pack_bf16x2(v[c], v[c + 1]);
+      uint4* dst = reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + n0);
+      dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+    }
+  }
+}
+
 template <int BN, bool SWAP, int CTAS>
 __global__ void __launch_bounds__(192, CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -648,81 +729,7 @@ __global__ void __launch_bounds__(192, CTAS)
         }
       } else {
         // lane <-> token t, column <-> feature n   (splits == 1 on this path)
-        const int t = m_tile * BM + row;
-        const bool tv = t < args.T;
-        if (epi == EPI_SWIGLU && args.swiglu_il) {
-          // interleaved columns (gate_j, up_j): 16 accumulator columns -> 8 outputs
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t r[16];
-            tmem_ld16(tcol + c0, r);
-            tmem_ld_wait();
-            const int j0 = (n_tile * BN + c0) / 2;
-            if (tv && n_tile * BN + c0 < args.N) {
-              uint32_t packed[4];
-#pragma unroll
-              for (int c = 0; c < 16; c += 4) {
-                const float g0 = rbf(__uint_as_float(r[c])), u0 = rbf(__uint_as_float(r[c + 1]));
-                const float g1 = rbf(__uint_as_float(r[c + 2])), u1 = rbf(__uint_as_float(r[c + 3]));
-                packed[c / 4] = pack_bf16x2(rbf(silu_f(g0)) * u0, rbf(silu_f(g1)) * u1);
-              }
-              *reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + j0) =
-                  make_uint4(packed[0], packed[1], packed[2], packed[3]);
-            }
-          }
-        } else if (epi == EPI_SWIGLU) {
-          for (int p = 0; p < BN / 128; ++p) {
-            for (int c0 = 0; c0 < 64; c0 += 16) {
-              uint32_t g[16], u[16];
-              tmem_ld16(tcol + p * 128 + c0, g);
-              tmem_ld16(tcol + p * 128 + 64 + c0, u);
-              tmem_ld_wait();
-              const int j0 = (n_tile * BN) / 2 + p * 64 + c0;
-              if (tv && (n_tile * BN + p * 128) < args.N) {
-                uint32_t packed[8];
-#pragma unroll
-                for (int c = 0; c < 16; c += 2) {
-                  const float g0 = rbf(__uint_as_float(g[c])), g1 = rbf(__uint_as_float(g[c + 1]));
-                  const float u0 = rbf(__uint_as_float(u[c])), u1 = rbf(__uint_as_float(u[c + 1]));
-                  packed[c / 2] = pack_bf16x2(rbf(silu_f(g0)) * u0, rbf(silu_f(g1)) * u1);
-                }
-                uint4* dst = reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + j0);
-                dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-                dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-              }
-            }
-          }
-        } else {
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t r[16];
-            tmem_ld16(tcol + c0, r);
-            tmem_ld_wait();
-            const int n0 = n_tile * BN + c0;
-            if (!tv || n0 >= args.N) continue;
-            float v[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(r[c]);
-            if (epi == EPI_BIAS) {
-#pragma unroll
-              for (int c = 0; c < 16; ++c) v[c] += bf2f(args.bias[n0 + c]);
-            } else if (epi == EPI_RESIDUAL) {
-              const uint4* rp = reinterpret_cast<const uint4*>(args.residual + (int64_t)t * args.ldr + n0);
-              const uint4 r0 = rp[0], r1 = rp[1];
-              const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-              for (int c = 0; c < 16; c += 2) {
-                const float2 rv = unpack_bf16x2(rr[c / 2]);
-                v[c] = rbf(v[c]) + rv.x;
-                v[c + 1] = rbf(v[c + 1]) + rv.y;
-              }
-            }
-            uint32_t packed[8];
-#pragma unroll
-            for (int c = 0; c < 16; c += 2) packed[c / 2] = pack_bf16x2(v[c], v[c + 1]);
-            uint4* dst = reinterpret_cast<uint4*>(args.C + (int64_t)t * args.ldc + n0);
-            dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-            dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-          }
-        }
+        token_rows_epilogue<BN>(args, tcol, m_tile * BM + row, n_tile);
       }
       release_tmem();
 
@@ -732,6 +739,185 @@ __global__ void __launch_bounds__(192, CTAS)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+// ---------------------------------------------------------------- CTA pair (prefill)
+// !SWAP GEMMs on a 2-CTA cluster (one TPC): the pair computes one 256-token x
+// 256-feature tile with tcgen05.mma.cta_group::2 (M = 256).  CTA r stages token rows
+// [128 r, +128) of the A tile and feature rows [128 r, +128) of the B tile; the
+// leader (r = 0) issues the MMA, which reads both CTAs' shared memory, and each CTA's
+// TMEM receives its own 128 token rows x all 256 features.  Per SM and MMA the
+// operand reads drop from 4 KB A + 8 KB B (single CTA, M = 128, N = 256) to 4 + 4 KB,
+// and a ring stage is 32 KB instead of 48 KB, so the ring is deeper.
+//
+// Barriers: every TMA of the pair completes on the LEADER's full barrier (the leader
+// arms it with both halves' bytes); the leader's commits multicast to the empty / TMEM
+// barriers at the same offset in both CTAs; both epilogues release a TMEM buffer on
+// the leader's tempty barrier (8 warp arrivals).  Work items: pair p walks tiles
+// p, p + #pairs, ... (grouped raster in 256-row bands).
+template <int S>
+struct PairSmem {
+  static constexpr int B_OFFSET = S * A_TILE_BYTES;
+  static constexpr int BAR_OFFSET = 2 * S * A_TILE_BYTES;
+  // fullA, emptyA, fullB, emptyB [S], tfull[2], tempty[2], tmem slot
+  static constexpr int TOTAL = BAR_OFFSET + 8 * (4 * S + 4) + 16 + 1024;
+};
+
+PL_DEV bool pair_next(const GemmArgs& a, int& it, int& m_tile, int& n_tile) {
+  if (it >= a.num_items) return false;
+  const int tiles_n = a.num_items / a.tiles_m;
+  if (a.raster_m > 0) {
+    const int band = it / (a.raster_m * tiles_n);
+    const int gm = min(a.raster_m, a.tiles_m - band * a.raster_m);
+    const int idx = it - band * a.raster_m * tiles_n;
+    m_tile = band * a.raster_m + idx % gm;
+    n_tile = idx / gm;
+  } else {
+    m_tile = it % a.tiles_m;
+    n_tile = it / a.tiles_m;
+  }
+  it += gridDim.x >> 1;
+  return true;
+}
+
+template <int S>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmArgs args) {
+  using L = PairSmem<S>;
+  constexpr int BN = 256;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + L::BAR_OFFSET);
+  uint64_t* emptyA = fullA + S;
+  uint64_t* fullB = emptyA + S;
+  uint64_t* emptyB = fullB + S;
+  uint64_t* tfull = emptyB + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();  // barriers initialised in both CTAs before any cross-CTA signal
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  if (warp >= 2) pdl_wait();
+
+  if (warp == 0) {
+    // ------------------------------------------------------- TMA producers (both CTAs)
+    if (lane == 0 || lane == 1) {
+      const bool weights = lane == 0;  // lane 0: B (weights, no PDL wait); lane 1: A (activations)
+      if (!weights) pdl_wait();
+      const uint64_t pol = weights ? policy_evict_first() : policy_evict_last();
+      uint64_t* full = weights ? fullB : fullA;
+      uint64_t* empty = weights ? emptyB : emptyA;
+      uint8_t* ring = smem + (weights ? L::B_OFFSET : 0);
+      int s = 0;
+      uint32_t ph = 0;
+      int it = blockIdx.x >> 1, m_tile, n_tile;
+      while (pair_next(args, it, m_tile, n_tile)) {
+        for (int kb = 0; kb < args.num_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * A_TILE_BYTES);  // both CTAs' halves
+          const uint32_t bar = mapa_shared(&full[s], 0);
+          if (!weights)
+            tma_load_2d_pair(ring + s * A_TILE_BYTES, &tmA, bar, kb * BK, m_tile * 256 + rank * BM, pol);
+          else if (args.wp)  // packed 16 KB tile (feature tile 2 n + r, k-block kb) as a linear 3-D box
+            tma_load_3d_pair(ring + s * A_TILE_BYTES, &tmB, bar, 0, 0,
+                             (n_tile * 2 + static_cast<int>(rank)) * args.num_kb + kb, pol);
+          else
+            tma_load_2d_pair(ring + s * A_TILE_BYTES, &tmB, bar, kb * BK, n_tile * BN + rank * BM, pol);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer (leader only)
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aphase = 0;
+      int it = blockIdx.x >> 1, m_tile, n_tile;
+      while (pair_next(args, it, m_tile, n_tile)) {
+        mbar_wait_cluster(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < args.num_kb; ++kb) {
+          mbar_wait(&fullA[s], ph);
+          mbar_wait(&fullB[s], ph);
+          tc_fence_after();
+          const uint64_t da = umma_desc_sw128(smem_u32(smem + s * A_TILE_BYTES));
+          const uint64_t db = umma_desc_sw128(smem_u32(smem + L::B_OFFSET + s * A_TILE_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) umma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_pair(&emptyA[s]);
+          umma_commit_pair(&emptyB[s]);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------- epilogue (warps 2..5, both CTAs)
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    int acc = 0;
+    uint32_t aphase = 0;
+    int it = blockIdx.x >> 1, m_tile, n_tile;
+    while (pair_next(args, it, m_tile, n_tile)) {
+      mbar_wait_cluster(&tfull[acc], aphase);
+      tc_fence_after();
+      token_rows_epilogue<BN>(args, tmem + lane_base + acc * BN, m_tile * 256 + static_cast<int>(rank) * BM + row,
+                              n_tile);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(mapa_shared(&tempty[acc], 0));
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();  // neither CTA leaves while the pair's MMAs / signals may touch it
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem);
 }
 
 // Split-K reduction + epilogue.  partial: [splits][N][Tp] fp32 (token-contiguous),
@@ -1089,6 +1275,54 @@ int make_map(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int6
   return PL_OK;
 }
 
+// Packed weights (pack_weight_kernel) as a 3-D tensor [tiles][128 rows][64 bf16] with no
+// swizzle: one box {64, 128, 1} is a tile's 16 KB pre-swizzled image, copied verbatim.
+int make_packed_map(CUtensorMap* out, const void* ptr, int64_t tiles) {
+  MapKey key{ptr, tiles, 0, 0, -1};
+  {
+    std::lock_guard<std::mutex> g(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return PL_OK;
+    }
+  }
+  auto fn = get_encode_fn();
+  if (!fn) return set_error(PL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(BK), static_cast<cuuint64_t>(BM), static_cast<cuuint64_t>(tiles)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(BK * 2), static_cast<cuuint64_t>(A_TILE_BYTES)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(BM), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(PL_ERR_CONFIG, "cuTensorMapEncodeTiled (packed) failed (%d) tiles=%lld", (int)r,
+                     (long long)tiles);
+  std::lock_guard<std::mutex> g(g_map_mu);
+  if (g_maps.size() > 8192) g_maps.clear();
+  g_maps.emplace(key, *out);
+  return PL_OK;
+}
+
+template <int S>
+int launch_pair_s(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         PairSmem<S>::TOTAL);
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm pair smem attribute");
+    attr_set = true;
+  }
+  return launch_k("gemm_pair_kernel", gemm_pair_kernel<S>, dim3(grid), dim3(192), PairSmem<S>::TOTAL, st, ma, mb,
+                  a);
+}
+// ring depth: PL_PAIR_STAGES=6 (default 7 = 224 KB of 32 KB stages)
+int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid, cudaStream_t st) {
+  static const int stages = [] { const char* v = getenv("PL_PAIR_STAGES"); return v ? atoi(v) : 7; }();
+  return stages == 6 ? launch_pair_s<6>(ma, mb, a, grid, st) : launch_pair_s<7>(ma, mb, a, grid, st);
+}
+
 template <int BN, bool SWAP, int CTAS = (BN <= 128 ? 2 : 1)>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid,
               cudaStream_t st) {
@@ -1191,6 +1425,14 @@ bool hybrid_enabled() {
   }();
   return on;
 }
+// Prefill (!SWAP) GEMMs on CTA pairs (cta_group::2, 256 x 256 tiles).  PL_GEMM_PAIR=0 /
+// 1 forces it off / on; default on for >= 512 tokens.
+bool use_pair(bool swap, int64_t T) {
+  static const int env = [] { const char* v = getenv("PL_GEMM_PAIR"); return v ? atoi(v) : -1; }();
+  if (swap || env == 0) return false;
+  return env == 1 || T >= 512;
+}
+
 int64_t sk_dp_tiles(int64_t N);
 bool use_streamk(bool swap, int64_t N) {
   return swap && (streamk_enabled() || (hybrid_enabled() && sk_dp_tiles(N) > 0));
@@ -1345,6 +1587,17 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
       case 128: rc = w1 ? launch_tc<128, true, 1>(ma, mb, a, grid, st) : launch_tc<128, true>(ma, mb, a, grid, st); break;
       default: rc = launch_tc<256, true>(ma, mb, a, grid, st); break;
     }
+  } else if (use_pair(swap, T)) {
+    // 256-token row tiles, one CTA pair per TPC
+    a.tiles_m = static_cast<int>((T + 2 * BM - 1) / (2 * BM));
+    a.num_items = a.tiles_m * tiles_n;
+    a.raster_m = (tiles_n > 1 && a.tiles_m > raster / 2) ? raster / 2 : 0;
+    grid = 2 * std::min(a.num_items, num_sms() / 2);
+    if ((rc = make_map(&ma, X, T, K, ldx, BM))) return rc;
+    if (w_packed) rc = make_packed_map(&mb, W, (N / BM) * a.num_kb);
+    else rc = make_map(&mb, W, N, K, ldw, BM);
+    if (rc) return rc;
+    rc = launch_pair(ma, mb, a, grid, st);
   } else {
     if ((rc = make_map(&ma, X, T, K, ldx, BM))) return rc;
     if ((rc = make_map(&mb, W, N, K, ldw, 256))) return rc;
@@ -1450,6 +1703,8 @@ int gemm_preload() {
   if (!rc) rc = preload_one(gemm_tc_kernel<128, true, 1>, "gemm_tc_kernel");
   if (!rc) rc = preload_one(gemm_tc_kernel<256, true, 1>, "gemm_tc_kernel");
   if (!rc) rc = preload_one(gemm_tc_kernel<256, false, 1>, "gemm_tc_kernel");
+  if (!rc) rc = preload_one(gemm_pair_kernel<6>, "gemm_pair_kernel");
+  if (!rc) rc = preload_one(gemm_pair_kernel<7>, "gemm_pair_kernel");
   if (!rc) rc = preload_one(argmax_reduce_kernel, "argmax_reduce_kernel");
   if (!rc) rc = preload_one(reduce_residual_norm_kernel<1>, "reduce_residual_norm_kernel");
   if (!rc) rc = preload_one(reduce_residual_norm_kernel<2>, "reduce_residual_norm_kernel");

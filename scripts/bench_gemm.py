@@ -60,6 +60,8 @@ def main():
         copies = max(1, -(-300_000_000 // wbytes))
         ws = [torch.randn(N, K, device=dev).to(torch.bfloat16) * 0.02 for _ in range(copies)]
         for T in a.T:
+            if epi == ops.EPI_ARGMAX and T > 256:
+                continue
             x = torch.randn(T, K, device=dev).to(torch.bfloat16)
             res = torch.randn(T, N, device=dev).to(torch.bfloat16) if epi == ops.EPI_RESIDUAL else None
             out = torch.empty(T, N // 2 if epi == ops.EPI_SWIGLU else N, device=dev, dtype=torch.bfloat16)

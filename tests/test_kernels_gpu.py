@@ -223,3 +223,55 @@ def test_attn_decode_paged(ops, ctx, Hq, Hkv):
         refs.append(OD.attention_ref(q[r].reshape(1, Hq, hd), k, v, None))
     # P is rounded to bf16 for the tensor-core P.V (as in the prefill kernel)
     close_bf16(out, torch.cat(refs), rel=2.0 ** -6, atol=4e-3)
+
+
+_PAIR_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+from paper_2507_05043_b200 import ops
+d = torch.device("cuda:0")
+outs = []
+for (T, Nw, K, epi) in {cases!r}:
+    g = torch.Generator().manual_seed(T + Nw + K + epi)
+    x = torch.randn(T, K, generator=g).to(torch.bfloat16).to(d)
+    w = (torch.randn(Nw, K, generator=g) * 0.05).to(torch.bfloat16).to(d)
+    b = torch.randn(Nw, generator=g).to(torch.bfloat16).to(d)
+    h = torch.randn(T, Nw, generator=g).to(torch.bfloat16).to(d)
+    if epi == ops.EPI_RESIDUAL:
+        ops.gemm(x, w, epi, residual=h, out=h)
+        outs.append(h.cpu())
+    else:
+        outs.append(ops.gemm(x, w, epi, bias=b if epi == ops.EPI_BIAS else None).cpu())
+torch.cuda.synchronize()
+torch.save(outs, sys.argv[1])
+"""
+
+
+def test_gemm_pair_bit_identical(tmp_path):
+    """Prefill GEMMs on CTA pairs (tcgen05.mma.cta_group::2, 256 x 256 tiles) vs the
+    single-CTA kernel (M = 128): same k order per output element -> bit-identical,
+    for every prefill epilogue and ragged T (packed weights through the pair kernel's
+    3-D TMA box: test_pipeline_gpu.py::test_packed_weights_bit_identical at T = 600)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    from paper_2507_05043_b200 import ops as O
+
+    root = str(Path(__file__).resolve().parent.parent)
+    cases = [(300, 512, 256, O.EPI_NONE), (1000, 1536, 256, O.EPI_NONE), (700, 512, 256, O.EPI_BIAS),
+             (513, 256, 768, O.EPI_RESIDUAL), (777, 1536, 512, O.EPI_SWIGLU), (2048, 6144, 4096, O.EPI_NONE),
+             (4096, 4096, 4096, O.EPI_RESIDUAL), (5000, 2048, 1024, O.EPI_SWIGLU)]
+    script = tmp_path / "pair.py"
+    script.write_text(_PAIR_SCRIPT.format(root=root, cases=cases))
+    res = []
+    for pair in ("0", "1"):
+        out = tmp_path / f"o{pair}.pt"
+        env = dict(os.environ, PL_GEMM_PAIR=pair)
+        p = subprocess.run([sys.executable, str(script), str(out)], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+        res.append(torch.load(out))
+    for c, a, b in zip(cases, *res):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16)), f"case {c}: pair != single-CTA"

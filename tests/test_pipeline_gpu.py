@@ -95,11 +95,12 @@ def test_config1_standard_init_tie_band():
     assert exact / total >= 0.9, f"only {exact}/{total} exact"
 
 
-@pytest.mark.parametrize("spec_name,T", [("tiny", 64), ("l3-2", 64), ("l3-2", 300)])
+@pytest.mark.parametrize("spec_name,T", [("tiny", 64), ("l3-2", 64), ("l3-2", 300), ("l3-2", 600)])
 def test_packed_weights_bit_identical(spec_name, T):
     """Pre-swizzled weight tiles (bulk copies) vs row-major weights (TMA boxes): the
     same tiles reach the tensor cores in the same order, so hidden states and token
-    ids are bit-identical -- decode (SWAP) and prefill (T > 256) orientations."""
+    ids are bit-identical -- decode (SWAP) and prefill (T > 256) orientations, the latter
+    on CTA pairs at T >= 512 (packed tiles as a 3-D TMA box)."""
     spec = TINY if spec_name == "tiny" else LLAMA3_8B.with_(num_layers=2)
     R = 4
     lens = [T // R] * R
