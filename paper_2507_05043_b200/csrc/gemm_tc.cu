@@ -75,6 +75,20 @@ struct GemmArgs {
   int sk_base, sk_extra;
   float* sk_slots;    // [2 * stream-K CTAs][BN][BM] fp32 (column-major: coalesced per column)
   int* sk_counters;   // [tiles_m], zero between launches (the fixer resets its tile)
+  // cluster split-K (decode / SWAP): the `splits` CTAs of one weight tile form a cluster,
+  // each parks its fp32 partial in its own (idle) ring memory and the cluster reduces
+  // over distributed shared memory -- no partial round trip through HBM/L2, no reduce
+  // kernel.  rope: the reduction also applies RoPE + the paged K/V append
+  // (reduce_qkv_rope_kernel's math; a 128-feature tile is one head).
+  int csk;
+  int rope;
+  const int32_t* pos;
+  const int32_t* slot;
+  const __nv_bfloat16* cos_sin;
+  int max_pos;
+  __nv_bfloat16* k_cache;
+  __nv_bfloat16* v_cache;
+  int block_size, Hq, Hkv;
 };
 
 // One unit of work: k-blocks [kb0, kb0 + nkb) of output tile (m_tile, n_tile).
@@ -247,6 +261,72 @@ PL_DEV void store_out(const GemmArgs& a, int epi, int t, int n, float acc) {
     a.C[(int64_t)t * a.ldc + n] = f2bf(acc + bf2f(a.bias[n]));
   else
     a.C[(int64_t)t * a.ldc + n] = f2bf(acc);
+}
+
+// Cluster split-K reduction (SWAP, one weight tile per cluster, cluster rank = split):
+// CTA r finalises token columns [r * per, +per) of the tile, summing the splits' parked
+// partials over DSMEM in split order (the order of gemm_splitk_reduce_kernel /
+// reduce_qkv_rope_kernel, so results are bit-identical to the two-kernel path).
+PL_DEV void csk_reduce(const GemmArgs& args, const uint8_t* smem, int ep, int BN) {
+  const int s = args.splits;
+  const int rank = static_cast<int>(cluster_ctarank());
+  const int m_tile = static_cast<int>(blockIdx.x) / s;
+  const int ncols = min(args.T, BN);
+  const int per = (ncols + s - 1) / s;
+  const int c_begin = rank * per, c_end = min(ncols, c_begin + per);
+  uint32_t base[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) base[j] = j < s ? mapa_shared(smem, j) : 0u;
+  auto sum_at = [&](int c, int r) {  // split-ordered sum of element (feature row r, token c)
+    const uint32_t off = static_cast<uint32_t>((c * BM + r) * 4);
+    float x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = j < s ? ld_dsmem_f32(base[j] + off) : 0.f;
+    float v = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < s) v += x[j];
+    return v;
+  };
+  if (!args.rope) {
+    const int n = m_tile * BM + ep;
+    if (n >= args.N) return;
+    for (int c = c_begin; c < c_end; ++c) store_out(args, args.epi, c, n, sum_at(c, ep));
+    return;
+  }
+  constexpr int HDIM = 128, HALF = 64;
+  const int hh = m_tile;  // a 128-feature tile is one q / k / v head
+  const int i = ep & (HALF - 1);
+  const int n1 = hh * HDIM + i, n2 = n1 + HALF;
+  const float b1 = args.bias ? bf2f(args.bias[n1]) : 0.f;
+  const float b2 = args.bias ? bf2f(args.bias[n2]) : 0.f;
+  const bool roped = hh < args.Hq + args.Hkv;
+  for (int c = c_begin + (ep >> 6); c < c_end; c += 2) {
+    const int t = c;
+    const float v1 = rbf(sum_at(c, i) + b1), v2 = rbf(sum_at(c, i + HALF) + b2);
+    float o1 = v1, o2 = v2;
+    if (roped) {
+      int pp = args.pos[t];
+      pp = pp < 0 ? 0 : (pp >= args.max_pos ? args.max_pos - 1 : pp);
+      const float cs = bf2f(args.cos_sin[static_cast<int64_t>(pp) * HDIM + i]);
+      const float sn = bf2f(args.cos_sin[static_cast<int64_t>(pp) * HDIM + HALF + i]);
+      o1 = rbf(rbf(v1 * cs) + rbf(-v2 * sn));
+      o2 = rbf(rbf(v2 * cs) + rbf(v1 * sn));
+    }
+    __nv_bfloat16* row = args.C + static_cast<int64_t>(t) * args.ldc;
+    row[n1] = f2bf(o1);
+    row[n2] = f2bf(o2);
+    const int sl = args.slot ? args.slot[t] : -1;
+    if (hh >= args.Hq && sl >= 0) {
+      const bool is_k = roped;
+      const int kh = is_k ? hh - args.Hq : hh - args.Hq - args.Hkv;
+      __nv_bfloat16* cache = is_k ? args.k_cache : args.v_cache;
+      __nv_bfloat16* dst = cache + ((static_cast<int64_t>(sl / args.block_size) * args.Hkv + kh) * args.block_size +
+                                    sl % args.block_size) * HDIM;
+      dst[i] = f2bf(o1);
+      dst[i + HALF] = f2bf(o2);
+    }
+  }
 }
 
 // !SWAP (prefill) epilogue: TMEM lane <-> token t, accumulator column c <-> feature
@@ -699,7 +779,17 @@ __global__ void __launch_bounds__(192, CTAS)
           }
           continue;
         }
-        if (args.splits > 1 && args.pmode == 1) {
+        if (args.csk) {
+          // cluster split-K: park this split's tile in the ring (all its loads were
+          // consumed by now), column-major [token][feature] so the reducers' lanes coalesce
+          float* red = reinterpret_cast<float*>(smem);
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16];
+            fetch_tmem(c0, v);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) red[(c0 + c) * BM + row] = v[c];
+          }
+        } else if (args.splits > 1 && args.pmode == 1) {
           // feature-contiguous partials [split][T][N] (per-token fused reductions)
           for (int c0 = 0; c0 < BN; c0 += 16) {
             float v[16];
@@ -736,6 +826,11 @@ __global__ void __launch_bounds__(192, CTAS)
     }
   }
 
+  if (SWAP && args.csk) {
+    cluster_sync();  // every split's partial tile is parked in its CTA's shared memory
+    if (warp >= 2) csk_reduce(args, smem, threadIdx.x - 64, BN);
+    cluster_sync();  // the peers are done reading this CTA's shared memory
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
@@ -1035,8 +1130,9 @@ __global__ void __launch_bounds__(1024)
     hv[k][1] = rbf(rbf(acc[k].y) + o0.y);
     hv[k][2] = rbf(rbf(acc[k].z) + o1.x);
     hv[k][3] = rbf(rbf(acc[k].w) + o1.y);
-    *reinterpret_cast<uint2*>(h + static_cast<int64_t>(t) * ldh + f) =
-        make_uint2(pack_bf16x2(hv[k][0], hv[k][1]), pack_bf16x2(hv[k][2], hv[k][3]));
+    if (splits > 0)  // splits == 0: h is already final (cluster split-K), only normalise it
+      *reinterpret_cast<uint2*>(h + static_cast<int64_t>(t) * ldh + f) =
+          make_uint2(pack_bf16x2(hv[k][0], hv[k][1]), pack_bf16x2(hv[k][2], hv[k][3]));
     ss += hv[k][0] * hv[k][0] + hv[k][1] * hv[k][1] + hv[k][2] * hv[k][2] + hv[k][3] * hv[k][3];
   }
   __shared__ float red[32];
@@ -1325,7 +1421,7 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a,
 
 template <int BN, bool SWAP, int CTAS = (BN <= 128 ? 2 : 1)>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid,
-              cudaStream_t st) {
+              cudaStream_t st, int cluster = 0) {
   constexpr int smem = GemmSmem<BN, SWAP, CTAS>::TOTAL;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1334,8 +1430,8 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, i
     if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
     attr_set = true;
   }
-  return launch_k("gemm_tc_kernel", gemm_tc_kernel<BN, SWAP, CTAS>, dim3(grid), dim3(192), smem, st, ma, mb,
-                  a);
+  return launch_kc("gemm_tc_kernel", gemm_tc_kernel<BN, SWAP, CTAS>, dim3(grid), dim3(192), smem, st, cluster,
+                   ma, mb, a);
 }
 
 int num_sms() {
@@ -1545,7 +1641,7 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   if (need > 0 && (ws_bytes < need || !ws))
     return set_error(PL_ERR_CONFIG, "gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
                      (long long)need);
-  int grid;
+  int grid, cluster = 0;
   // PL_GEMM_WIDE=1: one CTA per SM with a deep (~196 KB) ring instead of two shallower ones
   static const bool wide = [] { const char* v = getenv("PL_GEMM_WIDE"); return v && v[0] == '1'; }();
   if (sk) {
@@ -1572,6 +1668,36 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     static const int per_sm_env = [] { const char* v = getenv("PL_GRID_PER_SM"); return v ? atoi(v) : 0; }();
     const int per_sm = per_sm_env > 0 ? per_sm_env : (swap && bn <= 128 && !wide) ? 2 : 1;
     grid = std::min(a.num_items, num_sms() * per_sm);
+    // cluster split-K (default on; PL_CSK=0 restores partials + reduce kernels): one wave,
+    // one tile per cluster of `splits` CTAs
+    // PL_CSK bit mask of the GEMMs that use it: 1 = QKV (+RoPE/KV append), 2 = residual (+norm),
+    // 4 = the rest (plain / bias / residual without fusion).  Default 5: measured on the
+    // 4-layer L3 decode forward (profiles/r1/cluster_splitk.log) the QKV fusion gains
+    // 4 % at T = 64, while residual+norm loses (its reduce kernel already does the norm
+    // in one pass; in-GEMM reduction + a norm kernel is slower), and at T <= 16 the
+    // partials are small enough that the reduce kernels cost nothing extra.
+    static const int csk_mask = [] { const char* v = getenv("PL_CSK"); return v ? atoi(v) : 5; }();
+    const int csk_kind = fkind == FUSE_QKV_ROPE ? 1 : fkind == FUSE_RESIDUAL_NORM ? 2 : 4;
+    const bool csk_on = (csk_mask & csk_kind) != 0 && (T > 16 || getenv("PL_CSK"));
+    const bool rope_ok = fkind != FUSE_QKV_ROPE ||
+                         (N == static_cast<int64_t>(fuse->Hq + 2 * fuse->Hkv) * 128 && fuse->block_size > 0);
+    if (csk_on && swap && a.splits > 1 && a.splits <= 8 && tiles_n == 1 && a.num_items == grid &&
+        (epi == EPI_STORE || epi == EPI_BIAS || epi == EPI_RESIDUAL) && rope_ok) {
+      a.csk = 1;
+      cluster = a.splits;
+      if (fkind == FUSE_QKV_ROPE) {
+        a.rope = 1;
+        a.pos = fuse->pos;
+        a.slot = fuse->slot;
+        a.cos_sin = fuse->cos_sin;
+        a.max_pos = fuse->max_pos;
+        a.k_cache = fuse->k_cache;
+        a.v_cache = fuse->v_cache;
+        a.block_size = fuse->block_size;
+        a.Hq = fuse->Hq;
+        a.Hkv = fuse->Hkv;
+      }
+    }
   }
 
   CUtensorMap ma, mb;
@@ -1581,11 +1707,11 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     if ((rc = make_map(&mb, X, T, K, ldx, bn))) return rc;
     const bool w1 = wide || (sk && !sk_dp_tiles(N));  // pure stream-K: one CTA per SM, deep ring
     switch (bn) {
-      case 16: rc = w1 ? launch_tc<16, true, 1>(ma, mb, a, grid, st) : launch_tc<16, true>(ma, mb, a, grid, st); break;
-      case 32: rc = w1 ? launch_tc<32, true, 1>(ma, mb, a, grid, st) : launch_tc<32, true>(ma, mb, a, grid, st); break;
-      case 64: rc = w1 ? launch_tc<64, true, 1>(ma, mb, a, grid, st) : launch_tc<64, true>(ma, mb, a, grid, st); break;
-      case 128: rc = w1 ? launch_tc<128, true, 1>(ma, mb, a, grid, st) : launch_tc<128, true>(ma, mb, a, grid, st); break;
-      default: rc = launch_tc<256, true>(ma, mb, a, grid, st); break;
+      case 16: rc = w1 ? launch_tc<16, true, 1>(ma, mb, a, grid, st, cluster) : launch_tc<16, true>(ma, mb, a, grid, st, cluster); break;
+      case 32: rc = w1 ? launch_tc<32, true, 1>(ma, mb, a, grid, st, cluster) : launch_tc<32, true>(ma, mb, a, grid, st, cluster); break;
+      case 64: rc = w1 ? launch_tc<64, true, 1>(ma, mb, a, grid, st, cluster) : launch_tc<64, true>(ma, mb, a, grid, st, cluster); break;
+      case 128: rc = w1 ? launch_tc<128, true, 1>(ma, mb, a, grid, st, cluster) : launch_tc<128, true>(ma, mb, a, grid, st, cluster); break;
+      default: rc = launch_tc<256, true>(ma, mb, a, grid, st, cluster); break;
     }
   } else if (use_pair(swap, T)) {
     // 256-token row tiles, one CTA pair per TPC
@@ -1610,6 +1736,23 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     return launch_k("argmax_reduce_kernel", argmax_reduce_kernel, dim3(static_cast<unsigned>(T)),
                     dim3(256), 0, st, a.argmax_ws, tiles, static_cast<int>(T), argmax_out,
                     static_cast<float*>(nullptr));
+  }
+  if (a.csk) {
+    if (a.rope && fused) *fused = true;
+    if (fkind == FUSE_RESIDUAL_NORM) {  // h (= C) is final: the next RMSNorm, with the
+      // residual-norm kernel's own reduction order (splits = 0: h is only read)
+      if (fused) *fused = true;
+      const int64_t vec = N / 4;
+      const int threads = static_cast<int>(std::min<int64_t>(1024, (vec + 31) / 32 * 32));
+      const int vpt = static_cast<int>((vec + threads - 1) / threads);
+      if (vpt > 8) return set_error(PL_ERR_CONFIG, "residual+norm: N=%lld too large", (long long)N);
+      auto k = vpt <= 1 ? reduce_residual_norm_kernel<1> : vpt <= 2 ? reduce_residual_norm_kernel<2>
+             : vpt <= 4 ? reduce_residual_norm_kernel<4> : reduce_residual_norm_kernel<8>;
+      return launch_k("reduce_residual_norm_kernel", k, dim3(static_cast<unsigned>(T)), dim3(threads), 0, st,
+                      static_cast<const float*>(nullptr), 0, a.T, a.N, C, ldc, fuse->norm_w, fuse->eps,
+                      fuse->norm_out, fuse->ld_norm);
+    }
+    return PL_OK;
   }
   if (sk && fkind == FUSE_RESIDUAL_NORM) {  // h (= C) is final: the next RMSNorm reads it
     if (fused) *fused = true;

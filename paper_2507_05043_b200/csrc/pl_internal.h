@@ -32,6 +32,36 @@ bool pdl_enabled();
 
 // Launch with programmatic stream serialization so the kernel may start while its
 // predecessor in the stream drains (see pdl_wait / pdl_trigger in common.cuh).
+// cluster_x > 0: launch as clusters of cluster_x consecutive CTAs.
+template <typename... KArgs, typename... Args>
+int launch_kc(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+              cudaStream_t st, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster_x > 0) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = static_cast<unsigned>(cluster_x);
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) return set_cuda_error(e, what);
+  return check_launch(what);
+}
+
 template <typename... KArgs, typename... Args>
 int launch_k(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
              cudaStream_t st, Args&&... args) {

@@ -275,3 +275,27 @@ def test_gemm_pair_bit_identical(tmp_path):
         res.append(torch.load(out))
     for c, a, b in zip(cases, *res):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16)), f"case {c}: pair != single-CTA"
+
+
+@pytest.mark.parametrize("T,R", [(64, 4), (16, 16), (200, 8)])
+def test_cluster_splitk_bit_identical(tmp_path, T, R):
+    """Cluster split-K (partials reduced over DSMEM inside the GEMM, QKV+RoPE+KV append
+    in the cluster epilogue) vs partials + reduce kernels: a prefill and three decode
+    steps of a 2-layer Llama-3-shape stage are bit-identical (hidden states and ids)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    script = Path(__file__).resolve().parent / "_stage_steps.py"
+    res = []
+    for csk in ("0", "7"):
+        out = tmp_path / f"s{csk}.pt"
+        p = subprocess.run([sys.executable, str(script), str(out), str(T), str(R)],
+                           env=dict(os.environ, PL_CSK=csk), capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+        res.append(torch.load(out))
+    for i, (a, b) in enumerate(zip(*res)):
+        if a.dtype == torch.bfloat16:
+            a, b = a.view(torch.int16), b.view(torch.int16)
+        assert torch.equal(a, b), f"output {i} differs between PL_CSK=0 and 7"
