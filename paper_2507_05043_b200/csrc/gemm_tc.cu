@@ -41,6 +41,8 @@
 namespace pl {
 
 constexpr int BK = 64;          // bf16 elements per 128-byte swizzle row
+constexpr int GEMM_THREADS = 224;  // warp 0 weight producer, 1 MMA, 2-5 epilogue, 6 activation producer
+constexpr int GEMM_ACT_WARP = 6;
 constexpr int BM = 128;         // MMA M (A-operand rows per CTA)
 constexpr int A_TILE_BYTES = BM * BK * 2;
 
@@ -80,6 +82,7 @@ struct GemmArgs {
   // over distributed shared memory -- no partial round trip through HBM/L2, no reduce
   // kernel.  rope: the reduction also applies RoPE + the paged K/V append
   // (reduce_qkv_rope_kernel's math; a 128-feature tile is one head).
+  int act_lane;       // experiments (PL_ACT_LANE=1): activation producer on warp 0 lane 1
   int csk;
   int rope;
   const int32_t* pos;
@@ -411,7 +414,7 @@ PL_DEV void token_rows_epilogue(const GemmArgs& args, uint32_t tcol, int t, int 
 }
 
 template <int BN, bool SWAP, int CTAS>
-__global__ void __launch_bounds__(192, CTAS)
+__global__ void __launch_bounds__(224, CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs args) {
   using L = GemmSmem<BN, SWAP, CTAS>;
@@ -459,9 +462,9 @@ __global__ void __launch_bounds__(192, CTAS)
   // the residual stream): wait for it before any global write
   if (warp >= 2) pdl_wait();
 
-  if (warp == 0) {
-    // ------------------------------------------------------- TMA producer
-    if (lane == 0) {
+  if (warp == 0 || warp == GEMM_ACT_WARP) {
+    // ------------------------------------------------------- TMA producers
+    if (warp == 0 && lane == 0) {
       const uint64_t pol_w = policy_evict_first();   // weights stream through once
       const uint64_t pol_x = policy_evict_last();    // activations are re-read per weight tile
       const uint64_t polA = SWAP ? pol_w : pol_x;
@@ -499,12 +502,14 @@ __global__ void __launch_bounds__(192, CTAS)
           pb ^= 1;
         }
       };
-      // Two independent streams, one thread each, so neither waits behind the other's
-      // ring: lane 0 streams the weights (never produced by the previous kernel, so no
-      // PDL wait -- they flow while the predecessor drains), lane 1 the activations
-      // (after griddepcontrol.wait).  A single issuing thread coupled the rings: an
-      // activation load could only go out once a weight slot freed, which left the MMA
-      // waiting on L2 latency every few k-blocks.
+      // Two independent streams, one thread each IN DIFFERENT WARPS, so neither waits
+      // behind the other's ring: warp 0 streams the weights (never produced by the
+      // previous kernel, so no PDL wait -- they flow while the predecessor drains), warp
+      // GEMM_ACT_WARP the activations (after griddepcontrol.wait).  A single issuing
+      // thread coupled the rings; two lanes of one warp are no better: a lane suspended
+      // in mbarrier.try_wait holds the warp, so the other lane's loads went out one
+      // suspend interval late -- each CTA streamed only ~24 GB/s (measured: the Llama-3
+      // o-proj at split 1 took 44 us for 32 MB), hidden only when every SM is busy.
       PieceWalk walk;
       walk.init(args);
       Piece pc;
@@ -526,7 +531,7 @@ __global__ void __launch_bounds__(192, CTAS)
           else issue_b(kb0 + i, n_tile);
         }
       }
-    } else if (lane == 1) {
+    } else if (args.act_lane ? (warp == 0 && lane == 1) : (warp == GEMM_ACT_WARP && lane == 0)) {
       const uint64_t pol_x = policy_evict_last();
       const uint64_t polA = pol_x, polB = pol_x;
       int sa = 0, sb = 0;
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(192, CTAS)
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp <= 5) {
     // ------------------------------------------------------- epilogue (warps 2..5)
     const int quarter = warp & 3;                 // TMEM lanes [32q, 32q + 32)
     const int row = quarter * 32 + lane;
@@ -828,7 +833,7 @@ __global__ void __launch_bounds__(192, CTAS)
 
   if (SWAP && args.csk) {
     cluster_sync();  // every split's partial tile is parked in its CTA's shared memory
-    if (warp >= 2) csk_reduce(args, smem, threadIdx.x - 64, BN);
+    if (warp >= 2 && warp <= 5) csk_reduce(args, smem, threadIdx.x - 64, BN);
     cluster_sync();  // the peers are done reading this CTA's shared memory
   }
   tc_fence_before();
@@ -876,7 +881,7 @@ PL_DEV bool pair_next(const GemmArgs& a, int& it, int& m_tile, int& n_tile) {
 }
 
 template <int S>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(224, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmArgs args) {
   using L = PairSmem<S>;
@@ -920,10 +925,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   pdl_trigger();
   if (warp >= 2) pdl_wait();
 
-  if (warp == 0) {
+  if (warp == 0 || warp == GEMM_ACT_WARP) {
     // ------------------------------------------------------- TMA producers (both CTAs)
-    if (lane == 0 || lane == 1) {
-      const bool weights = lane == 0;  // lane 0: B (weights, no PDL wait); lane 1: A (activations)
+    if (lane == 0) {
+      const bool weights = warp == 0;  // warp 0: B (weights, no PDL wait); warp 6: A (activations)
       if (!weights) pdl_wait();
       const uint64_t pol = weights ? policy_evict_first() : policy_evict_last();
       uint64_t* full = weights ? fullB : fullA;
@@ -986,7 +991,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp <= 5) {
     // ------------------------------------------------------- epilogue (warps 2..5, both CTAs)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
@@ -1410,7 +1415,7 @@ int launch_pair_s(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& 
     if (e != cudaSuccess) return set_cuda_error(e, "gemm pair smem attribute");
     attr_set = true;
   }
-  return launch_k("gemm_pair_kernel", gemm_pair_kernel<S>, dim3(grid), dim3(192), PairSmem<S>::TOTAL, st, ma, mb,
+  return launch_k("gemm_pair_kernel", gemm_pair_kernel<S>, dim3(grid), dim3(GEMM_THREADS), PairSmem<S>::TOTAL, st, ma, mb,
                   a);
 }
 // ring depth: PL_PAIR_STAGES=6 (default 7 = 224 KB of 32 KB stages)
@@ -1430,7 +1435,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, i
     if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
     attr_set = true;
   }
-  return launch_kc("gemm_tc_kernel", gemm_tc_kernel<BN, SWAP, CTAS>, dim3(grid), dim3(192), smem, st, cluster,
+  return launch_kc("gemm_tc_kernel", gemm_tc_kernel<BN, SWAP, CTAS>, dim3(grid), dim3(GEMM_THREADS), smem, st, cluster,
                    ma, mb, a);
 }
 
@@ -1596,6 +1601,8 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     return set_error(PL_ERR_CONFIG, "gemm: N and leading dims must be multiples of 16/8");
 
   GemmArgs a{};
+  static const int act_lane = [] { const char* v = getenv("PL_ACT_LANE"); return v ? atoi(v) : 0; }();
+  a.act_lane = act_lane;
   a.T = static_cast<int>(T);
   a.N = static_cast<int>(N);
   if (w_packed) {
