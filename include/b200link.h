@@ -97,6 +97,20 @@ PL_API int32_t pl_gemm(const void* X, int64_t ldx, const void* W, int64_t ldw, c
                 int32_t epilogue, void* workspace, int64_t workspace_bytes, int64_t* argmax_out,
                 void* stream);
 
+/* Pre-swizzle W [N, K] (row stride ldw) into the packed layout the decode GEMMs stream
+ * with one 16 KB bulk copy per 128 x 64 tile: [N/128][K/64] tiles, each the 128-byte-
+ * swizzled shared-memory image (what pl_stage_pack_weights does to a stage's
+ * projections).  interleave = 1 for a gate_up weight (SwiGLU epilogue): rows alternate
+ * gate_j / up_j inside each 128-row tile.  out: N*K*2 bytes, not aliasing W;
+ * N % 256 == 0, K % 64 == 0. */
+PL_API int32_t pl_pack_weight(const void* W, int64_t ldw, int64_t N, int64_t K, int32_t interleave, void* out,
+                              void* stream);
+/* pl_gemm with W packed by pl_pack_weight (interleave = 1 iff epilogue == SWIGLU). */
+PL_API int32_t pl_gemm_packed(const void* X, int64_t ldx, const void* W_packed, const void* bias, void* C,
+                              int64_t ldc, const void* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,
+                              int32_t epilogue, void* workspace, int64_t workspace_bytes, int64_t* argmax_out,
+                              void* stream);
+
 /* Neox RoPE on the q and k heads of qkv[T, (Hq+2Hkv)*hd] in place, then k and v
  * written to the paged caches [num_blocks, Hkv, block_size, hd] at slot[t]
  * (slot < 0 skips the write).  cos_sin: bf16 [max_pos, hd] = [cos | sin]. */

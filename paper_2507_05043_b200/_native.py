@@ -84,6 +84,8 @@ _SIGS = {
     "pl_rmsnorm": (i32, [vp, i64, vp, vp, f32, i64, i32, vp, i64, vp]),
     "pl_gemm_workspace_bytes": (i64, [i64, i64, i64, i32]),
     "pl_gemm": (i32, [vp, i64, vp, i64, vp, vp, i64, vp, i64, i64, i64, i64, i32, vp, i64, vp, vp]),
+    "pl_pack_weight": (i32, [vp, i64, i64, i64, i32, vp, vp]),
+    "pl_gemm_packed": (i32, [vp, i64, vp, vp, vp, i64, vp, i64, i64, i64, i64, i32, vp, i64, vp, vp]),
     "pl_rope_kv_write": (i32, [vp, i64, vp, vp, vp, i32, vp, vp, i32, i64, i32, i32, i32, vp]),
     "pl_attn_prefill": (i32, [vp, i64, vp, i32, i32, i32, i32, i32, f32, vp, i64, vp]),
     "pl_attn_decode_workspace_bytes": (i64, [i32, i32, i32, i32]),

@@ -111,6 +111,28 @@ int32_t pl_gemm(const void* X, int64_t ldx, const void* W, int64_t ldw, const vo
                      workspace, workspace_bytes, argmax_out, S(stream));
 }
 
+int32_t pl_pack_weight(const void* W, int64_t ldw, int64_t N, int64_t K, int32_t interleave, void* out,
+                       void* stream) {
+  if (!W || !out) return set_error(PL_ERR_CONFIG, "pack_weight: null argument");
+  return pack_weight_launch(B(W), ldw, N, K, out, S(stream), interleave != 0);
+}
+
+int32_t pl_gemm_packed(const void* X, int64_t ldx, const void* W_packed, const void* bias, void* C,
+                       int64_t ldc, const void* residual, int64_t ldr, int64_t T, int64_t N, int64_t K,
+                       int32_t epilogue, void* workspace, int64_t workspace_bytes, int64_t* argmax_out,
+                       void* stream) {
+  if (!X || !W_packed) return set_error(PL_ERR_CONFIG, "gemm: null operand");
+  if (epilogue < PL_EPI_NONE || epilogue > PL_EPI_ARGMAX)
+    return set_error(PL_ERR_CONFIG, "gemm: unknown epilogue %d", epilogue);
+  if (epilogue == PL_EPI_ARGMAX ? !argmax_out : !C)
+    return set_error(PL_ERR_CONFIG, "gemm: null output");
+  if (epilogue == PL_EPI_BIAS && !bias) return set_error(PL_ERR_CONFIG, "gemm: bias epilogue needs bias");
+  if (epilogue == PL_EPI_RESIDUAL && !residual)
+    return set_error(PL_ERR_CONFIG, "gemm: residual epilogue needs residual");
+  return gemm_launch(B(X), ldx, B(W_packed), K, B(bias), BM_(C), ldc, B(residual), ldr, T, N, K, epilogue,
+                     workspace, workspace_bytes, argmax_out, S(stream), nullptr, nullptr, true);
+}
+
 int32_t pl_rope_kv_write(void* qkv, int64_t ldqkv, const int32_t* pos, const int32_t* slot,
                          const void* cos_sin, int32_t max_pos, void* k_cache, void* v_cache,
                          int32_t block_size, int64_t T, int32_t Hq, int32_t Hkv, int32_t hd,

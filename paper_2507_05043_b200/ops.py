@@ -102,6 +102,39 @@ def gemm(x: torch.Tensor, w: torch.Tensor, epilogue: int = EPI_NONE,
     return ids if epilogue == EPI_ARGMAX else out
 
 
+def pack_weight(w: torch.Tensor, interleave: bool = False) -> torch.Tensor:
+    """w [N, K] -> the packed, pre-swizzled tile layout of the decode GEMMs (same shape/dtype;
+    interleave=True for a gate_up weight used with EPI_SWIGLU)."""
+    _need_cuda(w)
+    Nw, K = w.shape
+    out = torch.empty_like(w)
+    N.call("pl_pack_weight", _ptr(w), w.stride(0), Nw, K, int(interleave), _ptr(out), _stream())
+    return out
+
+
+def gemm_packed(x: torch.Tensor, wp: torch.Tensor, epilogue: int = EPI_NONE,
+                bias: torch.Tensor | None = None, residual: torch.Tensor | None = None,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """gemm() with a weight from pack_weight (interleaved iff epilogue == EPI_SWIGLU)."""
+    _need_cuda(x, wp, bias, residual, out)
+    T, K = x.shape
+    Nw, Kw = wp.shape
+    if K != Kw:
+        raise N.ConfigError(f"gemm: K mismatch {K} vs {Kw}")
+    ws_bytes = N.lib().pl_gemm_workspace_bytes(T, Nw, K, epilogue)
+    ws = _workspace(x.device, ws_bytes)
+    ids = None
+    if epilogue == EPI_ARGMAX:
+        ids = torch.empty(T, dtype=torch.int64, device=x.device)
+    elif out is None:
+        out = torch.empty(T, Nw // 2 if epilogue == EPI_SWIGLU else Nw, dtype=BF16, device=x.device)
+    N.call("pl_gemm_packed", _ptr(x), x.stride(0), _ptr(wp), _ptr(bias), _ptr(out),
+           out.stride(0) if out is not None else 0, _ptr(residual),
+           residual.stride(0) if residual is not None else 0, T, Nw, K, epilogue, _ptr(ws), ws_bytes,
+           _ptr(ids), _stream())
+    return ids if epilogue == EPI_ARGMAX else out
+
+
 def rope_kv_write(qkv: torch.Tensor, pos: torch.Tensor, slot: torch.Tensor | None,
                   cos_sin: torch.Tensor, k_cache: torch.Tensor | None, v_cache: torch.Tensor | None,
                   Hq: int, Hkv: int, hd: int, block_size: int = 64) -> None:

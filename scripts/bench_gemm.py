@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--model", default="l3")
     ap.add_argument("--shapes", nargs="*", default=None,
                     help="custom N,K pairs (plain store epilogue), e.g. 18944,4096 18944,1024")
+    ap.add_argument("--packed", action="store_true", help="pre-swizzled weights (pl_pack_weight), as served")
     a = ap.parse_args()
     spec = {"l3": LLAMA3_8B, "q2": QWEN2_72B}[a.model]
     dev = torch.device("cuda", 0)
@@ -59,6 +60,10 @@ def main():
         wbytes = N * K * 2
         copies = max(1, -(-300_000_000 // wbytes))
         ws = [torch.randn(N, K, device=dev).to(torch.bfloat16) * 0.02 for _ in range(copies)]
+        gemm = ops.gemm
+        if a.packed and N % 256 == 0:
+            ws = [ops.pack_weight(w, interleave=epi == ops.EPI_SWIGLU) for w in ws]
+            gemm = ops.gemm_packed
         for T in a.T:
             if epi == ops.EPI_ARGMAX and T > 256:
                 continue
@@ -68,14 +73,14 @@ def main():
 
             def fn(i):
                 if epi == ops.EPI_RESIDUAL:
-                    ops.gemm(x, ws[i % copies], epi, residual=res, out=res)
+                    gemm(x, ws[i % copies], epi, residual=res, out=res)
                 elif epi == ops.EPI_ARGMAX:
-                    ops.gemm(x, ws[i % copies], epi)
+                    gemm(x, ws[i % copies], epi)
                 else:
-                    ops.gemm(x, ws[i % copies], epi, out=out)
+                    gemm(x, ws[i % copies], epi, out=out)
 
             us = timeit(fn)
-            print(json.dumps({"kernel": name, "T": T, "N": N, "K": K, "us": round(us, 2),
+            print(json.dumps({"kernel": name, "T": T, "N": N, "K": K, "packed": gemm is not ops.gemm, "us": round(us, 2),
                               "GBps": round(wbytes / us / 1e3, 1)}), flush=True)
         del ws
         torch.cuda.empty_cache()

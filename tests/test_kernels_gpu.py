@@ -299,3 +299,29 @@ def test_cluster_splitk_bit_identical(tmp_path, T, R):
         if a.dtype == torch.bfloat16:
             a, b = a.view(torch.int16), b.view(torch.int16)
         assert torch.equal(a, b), f"output {i} differs between PL_CSK=0 and 7"
+
+
+@pytest.mark.parametrize("T,N,K,epi", [(16, 6144, 4096, 0), (64, 4096, 4096, 3), (64, 2048, 1024, 2),
+                                       (8, 128256 // 256 * 256, 256, 4), (300, 1024, 512, 1), (600, 1536, 512, 2)])
+def test_gemm_packed_bit_identical(ops, T, N, K, epi):
+    """pl_gemm_packed on pl_pack_weight tiles == pl_gemm on the row-major weight (decode
+    split-K / cluster paths, argmax, prefill single-CTA and CTA-pair paths)."""
+    g = torch.Generator().manual_seed(T + N + K + epi)
+    x = torch.randn(T, K, generator=g).to(BF16).to(dev())
+    w = (torch.randn(N, K, generator=g) * 0.05).to(BF16).to(dev())
+    b = torch.randn(N, generator=g).to(BF16).to(dev())
+    h = torch.randn(T, N, generator=g).to(BF16).to(dev())
+    wp = ops.pack_weight(w, interleave=epi == ops.EPI_SWIGLU)
+    if epi == ops.EPI_RESIDUAL:
+        h2 = h.clone()
+        ops.gemm(x, w, epi, residual=h, out=h)
+        ops.gemm_packed(x, wp, epi, residual=h2, out=h2)
+        a, c = h, h2
+    else:
+        kw = {"bias": b} if epi == ops.EPI_BIAS else {}
+        a = ops.gemm(x, w, epi, **kw)
+        c = ops.gemm_packed(x, wp, epi, **kw)
+    torch.cuda.synchronize()
+    if a.dtype == BF16:
+        a, c = a.view(torch.int16), c.view(torch.int16)
+    assert torch.equal(a.cpu(), c.cpu())
