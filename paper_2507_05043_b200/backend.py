@@ -62,6 +62,15 @@ class _MbRec:
     n_decode: int = 0    # mixed batch: leading decode requests (rows [0, n_decode))
 
 
+def local_device_index(default: int = 0) -> int:
+    """This process's GPU: LOCAL_RANK, folded onto PL_OVERSUBSCRIBE_GPUS devices when that
+    is set (testing only: e.g. an 8-rank, 8-stage pipeline on a 4-GPU box, two ranks per
+    GPU; every hop communicator still joins two distinct GPUs)."""
+    local = int(os.environ.get("LOCAL_RANK", default))
+    mod = int(os.environ.get("PL_OVERSUBSCRIBE_GPUS", "0") or 0)
+    return local % mod if mod > 0 else local
+
+
 class Placement:
     """Stage -> (rank, device).  Contiguous blocks of stages per rank."""
 
@@ -73,7 +82,7 @@ class Placement:
         per = n_stages // world_size
         self.stage_rank = [s // per for s in range(n_stages)]
         if world_size > 1:
-            local = int(os.environ.get("LOCAL_RANK", rank))
+            local = local_device_index(rank)
             self.stage_device = [torch.device("cuda", local) if self.stage_rank[s] == rank else None
                                  for s in range(n_stages)]
         else:

@@ -287,7 +287,17 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
 // holding the newest token waits for the predecessor kernel.
 
 constexpr int PAGE = 64;                 // tokens per KV block
-constexpr int MAX_PAGES_PER_SPLIT = 16;  // <= 1024 tokens per split, pages spread evenly
+// Pages per split of a request's context (pages spread evenly over ceil(pages / pps)
+// splits).  Depends on the request's own length only, so a request's result never
+// depends on the batch it rides in.  PL_ATTN_PPS overrides (experiments).
+int attn_pages_per_split() {
+  static const int v = [] {
+    const char* e = getenv("PL_ATTN_PPS");
+    const int x = e ? atoi(e) : 16;
+    return x > 0 ? x : 16;
+  }();
+  return v;
+}
 constexpr int HALF_TILE = 64 * 128;      // 64 tokens x 64 dims bf16 (one TMA box)
 constexpr int PAGE_BYTES = 4 * HALF_TILE;  // K lo | K hi | V lo | V hi
 constexpr int DEC_THREADS = 160;         // producer warp + 4 consumer warps
@@ -323,6 +333,7 @@ struct DecodeArgs {
   int max_blocks;
   const int32_t* ctx_len;
   int R, Hkv, nsplit;
+  int pps;  // pages per split
   float scale_log2;
   __nv_bfloat16* out;
   int64_t ldo;
@@ -343,7 +354,7 @@ PL_DEV ItemGeom decode_geom(const DecodeArgs& a, int it, int ctx) {
   g.r = it / (a.nsplit * a.Hkv);
   g.ctx = ctx;
   g.n_pages = (ctx + PAGE - 1) / PAGE;
-  const int ns_r = max(1, (g.n_pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
+  const int ns_r = max(1, (g.n_pages + a.pps - 1) / a.pps);
   const int pps = (g.n_pages + ns_r - 1) / ns_r;
   g.p0 = g.split * pps;
   g.np = max(0, min(g.n_pages, g.p0 + pps) - g.p0);
@@ -675,7 +686,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
 // Workspace: [R*Hkv arrival counters, zero between launches | o partials | (m, l)].
 int64_t attn_decode_workspace_bytes(int R, int Hq, int max_ctx, int hd) {
   const int pages = (max_ctx + PAGE - 1) / PAGE;
-  const int nsplit = std::max(1, (pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
+  const int nsplit = std::max(1, (pages + attn_pages_per_split() - 1) / attn_pages_per_split());
   if (nsplit == 1) return 0;
   const int64_t counters = ((static_cast<int64_t>(R) * Hq * 4 + 255) / 256) * 256;
   return counters + static_cast<int64_t>(R) * Hq * nsplit * (hd * 4 + 8);
@@ -694,7 +705,7 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
   if (ldq % 8) return set_error(PL_ERR_CONFIG, "attention: ldq % 8");
   const int G = Hq / Hkv;
   const int pages = (max_ctx + PAGE - 1) / PAGE;
-  const int nsplit = std::max(1, (pages + MAX_PAGES_PER_SPLIT - 1) / MAX_PAGES_PER_SPLIT);
+  const int nsplit = std::max(1, (pages + attn_pages_per_split() - 1) / attn_pages_per_split());
   const int64_t need = attn_decode_workspace_bytes(R, Hq, max_ctx, hd);
   if (need > 0 && (ws_bytes < need || !ws))
     return set_error(PL_ERR_CONFIG, "attn_decode: workspace too small (%lld < %lld)",
@@ -721,6 +732,7 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
   da.R = R;
   da.Hkv = Hkv;
   da.nsplit = nsplit;
+  da.pps = attn_pages_per_split();
   da.scale_log2 = scale * LOG2E;
   da.out = out;
   da.ldo = ldo;

@@ -11,13 +11,16 @@
 //          (16..256).  Weight bytes dominate, so the kernel is an HBM stream of
 //          W with split-K chosen from (N, K) only -- never from T -- which keeps
 //          every token's result independent of the batch it rides in.
-//   !SWAP (prefill): tokens are the A operand (M = 128 rows), features are N = 256.
+//   !SWAP (prefill): tokens are the A operand (M = 128 rows), features are N = 256;
+//          at T >= 512 gemm_pair_kernel (CTA pairs, cta_group::2, 256 x 256 tiles).
 //
-// Persistent and warp-specialized (192 threads, one CTA per SM): warp 0 lane 0
-// = TMA producer running the A and B smem rings continuously across work items,
-// warp 1 = TMEM allocator + MMA issuer (lane 0), warps 2-5 = epilogue, warp w
-// owning TMEM lanes [32(w%4), +32).  The accumulator is double-buffered in
-// TMEM so the epilogue of item i overlaps the main loop of item i+1.
+// Persistent and warp-specialized (224 threads): warp 0 lane 0 = weight TMA
+// producer, warp 6 lane 0 = activation TMA producer (each runs its smem ring
+// continuously across work items), warp 1 = TMEM allocator + MMA issuer (lane 0),
+// warps 2-5 = epilogue, warp w owning TMEM lanes [32(w%4), +32).  The accumulator
+// is double-buffered in TMEM so the epilogue of item i overlaps the main loop of
+// item i+1.  Decode split-K: partials + a reduce kernel, or (cluster split-K) a
+// DSMEM reduction inside the launch.
 //
 // Epilogues (rounding points follow HF modeling_llama.py: every bf16 tensor op
 // rounds its fp32 result to bf16):

@@ -28,14 +28,15 @@ def _port():
     return p
 
 
-def torchrun(script, *args, nproc=2, timeout=600):
-    if torch.cuda.device_count() < nproc:
-        pytest.skip(f"needs {nproc} GPUs")
+def torchrun(script, *args, nproc=2, timeout=600, gpus=None, env=None):
+    gpus = gpus or nproc
+    if torch.cuda.device_count() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "scripts" / script),
            *args]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout,
-                       env={**os.environ, "PYTHONPATH": str(ROOT)})
+                       env={**os.environ, "PYTHONPATH": str(ROOT), **(env or {})})
     assert p.returncode == 0, p.stdout[-6000:] + p.stderr[-2000:]
     return p.stdout
 
@@ -59,3 +60,11 @@ def test_live_nvlink_pipeline_token_parity():
 def test_live_nvlink_pipeline_four_stages():
     out = torchrun("check_live.py", nproc=4)
     assert "live 4-stage" in out and "token counts == virtual" in out and "20/20 requests identical" in out
+
+
+def test_eight_ranks_eight_stages_on_four_gpus():
+    """The 8-stage, 8-rank pipeline (the driver's N = 8 shape) on a 4-GPU box, two ranks
+    per GPU: schedule == pipelink's on every rank, greedy ids == the CPU oracle."""
+    out = torchrun("check_multigpu.py", "--stages", "8", "--model", "l3-2", "--requests", "4",
+                   "--prompt", "64", "--decode", "5", nproc=8, gpus=4, env={"PL_OVERSUBSCRIBE_GPUS": "4"})
+    assert "world 8, 8 stages: 4/4 requests identical" in out
