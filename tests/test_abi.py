@@ -48,3 +48,15 @@ def test_errors_map_to_reference_hierarchy():
     uid = (ctypes.c_uint8 * 8)()
     with pytest.raises(N.ConfigError):
         N.call("pl_nccl_unique_id", uid, 8)
+
+
+def test_packed_weight_entry_points_validate_before_touching_the_gpu():
+    import pytest
+
+    lib = N.lib()
+    assert lib.pl_pack_weight(None, 64, 256, 64, 0, None, None) == N.PL_ERR_CONFIG
+    assert "null argument" in N.last_error()
+    rc = lib.pl_gemm_packed(None, 0, None, None, None, 0, None, 0, 1, 256, 64, 0, None, 0, None, None)
+    with pytest.raises(N.ConfigError):
+        N.check(rc, "pl_gemm_packed")
+    assert "null operand" in N.last_error()
