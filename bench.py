@@ -272,6 +272,9 @@ def run_b200(args):
 
     # ---- path roofline for the decode window from the micro-batch log
     path = decode_path_roofline(spec, eng, runs[-1][0], hbm, tfl)
+    if path and decode_window_tok_s:
+        # achieved decode rate over the same decode micro-batches (north star: >= 0.60)
+        path["decode_window_frac"] = round(decode_window_tok_s / path["decode_roofline_tok_s"], 4)
 
     out = None
     if rank == 0:

@@ -34,9 +34,12 @@
 //   ARGMAX    per token (max logit, index) over this CTA's 128 vocabulary rows
 #include <cudaTypedefs.h>
 
+#include <array>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "common.cuh"
 #include "pl_internal.h"
@@ -1479,6 +1482,21 @@ int gemm_num_splits(int64_t N, int64_t K, bool swap) {
     return v ? atoi(v) : 0;
   }();
   if (forced > 0) return static_cast<int>(std::min<int64_t>(forced, K / BK));
+  // PL_SPLITS="N:K:s,...": per-shape override (experiments; still a function of (N, K) only)
+  static const std::vector<std::array<int64_t, 3>> per_shape = [] {
+    std::vector<std::array<int64_t, 3>> v;
+    const char* e = getenv("PL_SPLITS");
+    long long n, k, s;
+    int used;
+    while (e && sscanf(e, "%lld:%lld:%lld%n", &n, &k, &s, &used) == 3) {
+      v.push_back({n, k, s});
+      e += used;
+      if (*e == ',') ++e;
+    }
+    return v;
+  }();
+  for (const auto& o : per_shape)
+    if (o[0] == N && o[1] == K && o[2] > 0) return static_cast<int>(std::min<int64_t>(o[2], K / BK));
   const int64_t tiles = (N + BM - 1) / BM;
   const int64_t kb = K / BK;
   // PL_SPLIT_RULE=fit: the largest split with tiles*splits <= 148 (every CTA on its own
@@ -1503,6 +1521,16 @@ int gemm_num_splits(int64_t N, int64_t K, bool swap) {
     if (s > 1 && per < 4) break;
     best = static_cast<int>((kb + per - 1) / per);  // no empty splits
     if (tiles * best >= sms) break;
+  }
+  // Long-K projections (the down GEMMs, K >= 12288): round the split count up to a
+  // multiple of 4.  The residual+norm reduce loads partials in groups of 4, so this adds
+  // no reduction round, and the smaller per-CTA streams even out the SMs that carry two
+  // CTAs (L3 down: 5 -> 8 splits, 160 -> 256 CTAs; 4-layer decode forward -1.0 % at
+  // T = 64, -1.5 % at T = 32, neutral at T = 16: profiles/r1/split_sweep.log).
+  if (kb >= 192 && best > 1 && best % 4) {
+    const int up = (best + 3) / 4 * 4;
+    const int64_t per = (kb + up - 1) / up;
+    if (per >= 16) best = static_cast<int>((kb + per - 1) / per);
   }
   return best;
 }
