@@ -1030,7 +1030,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(224, 1)
 // summed in split order (deterministic).  Each thread owns one output feature and
 // 4 consecutive tokens: splits independent 16-byte loads in flight.
 __global__ void __launch_bounds__(256)
-    gemm_splitk_reduce_kernel(const float* __restrict__ partial, int splits, int T, int Tp, int N,
+    gemm_splitk_reduce_kernel(const float* partial, int splits, int T, int Tp, int N,
                               int epi, __nv_bfloat16* __restrict__ C, int64_t ldc,
                               const __nv_bfloat16* __restrict__ bias,
                               const __nv_bfloat16* __restrict__ residual, int64_t ldr, int swiglu_il) {
@@ -1085,7 +1085,7 @@ __global__ void __launch_bounds__(256)
 // splits' partials are in flight at once (latency-bound, not bandwidth-bound).
 template <int VPT>  // float4 chunks per thread
 __global__ void __launch_bounds__(1024)
-    reduce_residual_norm_kernel(const float* __restrict__ partial, int splits, int T, int N,
+    reduce_residual_norm_kernel(const float* partial, int splits, int T, int N,
                                 __nv_bfloat16* __restrict__ h, int64_t ldh,
                                 const __nv_bfloat16* __restrict__ w, float eps,
                                 __nv_bfloat16* __restrict__ a, int64_t lda) {
@@ -1109,26 +1109,34 @@ __global__ void __launch_bounds__(1024)
   }
   const int64_t stride = static_cast<int64_t>(T) * N;
   const float* prow = partial + static_cast<int64_t>(t) * N;
-  for (int s0 = 0; s0 < splits; s0 += 4) {
-    float4 x[4][VPT];
+  // Up to 8 splits' loads in flight per round at VPT = 1 (one L2 round trip for the L3
+  // residual GEMMs).  The loads are unconditional (split index and feature clamped to
+  // valid addresses) plain weak loads after griddepcontrol.wait (the PDL-documented
+  // way to read the previous grid's output), so they issue back to back before the
+  // first add; the predicated __ldcg form compiled to load -> add -> load.  `partial`
+  // is not __restrict__: that would turn these into .nc loads, whose read-only
+  // contract the early-launched (PDL) grid cannot promise.  Sum order = split order.
+  constexpr int G = VPT == 1 ? 8 : 4;
+  for (int s0 = 0; s0 < splits; s0 += G) {
+    float4 x[G][VPT];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < G; ++u)
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
         const int f = (threadIdx.x + nt * k) * 4;
-        x[u][k] = (s0 + u < splits && f < N)
-                      ? __ldcg(reinterpret_cast<const float4*>(prow + (s0 + u) * stride + f))
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int su = min(s0 + u, splits - 1);
+        x[u][k] = *reinterpret_cast<const float4*>(prow + su * stride + (f < N ? f : 0));
       }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < G; ++u)
+      if (s0 + u < splits)
 #pragma unroll
-      for (int k = 0; k < VPT; ++k) {  // split order (deterministic)
-        acc[k].x += x[u][k].x;
-        acc[k].y += x[u][k].y;
-        acc[k].z += x[u][k].z;
-        acc[k].w += x[u][k].w;
-      }
+        for (int k = 0; k < VPT; ++k) {  // split order (deterministic)
+          acc[k].x += x[u][k].x;
+          acc[k].y += x[u][k].y;
+          acc[k].z += x[u][k].z;
+          acc[k].w += x[u][k].w;
+        }
   }
   float hv[VPT][4];
   float ss = 0.f;
@@ -1169,7 +1177,7 @@ __global__ void __launch_bounds__(1024)
 // (HF per-op bf16 rounding, as rope_kv_kernel) + paged K/V append.  One thread per
 // (head, rotary pair i, 4 tokens); partials token-contiguous, [splits][N][Tp].
 __global__ void __launch_bounds__(256)
-    reduce_qkv_rope_kernel(const float* __restrict__ partial, int splits, int T, int Tp, int N,
+    reduce_qkv_rope_kernel(const float* partial, int splits, int T, int Tp, int N,
                            const __nv_bfloat16* __restrict__ bias, __nv_bfloat16* __restrict__ qkv,
                            int64_t ldqkv, const int32_t* __restrict__ pos,
                            const int32_t* __restrict__ slot, const __nv_bfloat16* __restrict__ cos_sin,
@@ -1226,16 +1234,19 @@ __global__ void __launch_bounds__(256)
     float4 a1 = make_float4(0.f, 0.f, 0.f, 0.f), a2 = a1;
     const float4* p1 = P + (static_cast<int64_t>(n1) * Tp + t0) / 4;
     const float4* p2 = P + (static_cast<int64_t>(n2) * Tp + t0) / 4;
-    for (int s0 = 0; s0 < splits; s0 += 4) {  // four splits' loads in flight, summed in split order
+    // four splits' loads in flight (unconditional weak loads after the PDL wait, as in
+    // reduce_residual_norm_kernel), summed in split order
+    for (int s0 = 0; s0 < splits; s0 += 4) {
       float4 x[4], y[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const bool ok = s0 + u < splits;
-        x[u] = ok ? __ldcg(p1 + (s0 + u) * split_stride) : make_float4(0.f, 0.f, 0.f, 0.f);
-        y[u] = ok ? __ldcg(p2 + (s0 + u) * split_stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int su = min(s0 + u, splits - 1);
+        x[u] = p1[su * split_stride];
+        y[u] = p2[su * split_stride];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
+        if (s0 + u >= splits) break;
         a1.x += x[u].x; a1.y += x[u].y; a1.z += x[u].z; a1.w += x[u].w;
         a2.x += y[u].x; a2.y += y[u].y; a2.z += y[u].z; a2.w += y[u].w;
       }
