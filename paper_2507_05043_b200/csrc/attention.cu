@@ -663,15 +663,36 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
         for (int g = 0; g < G; ++g) {
           const int head = kh * G + g;
           const int64_t base = (static_cast<int64_t>(r) * args.Hkv * G + head) * nsplit;
+          // four splits' loads in flight per round: unconditional weak loads (split
+          // index clamped), ordered after the other splits' writes by the acq_rel
+          // arrival + barrier; merged in split order as before
+          constexpr int MB = 4;
           float M = -INFINITY;
-          for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(&args.ws_ml[base + s2]).x);
+          for (int s0 = 0; s0 < nsplit; s0 += MB) {
+            float mx[MB];
+#pragma unroll
+            for (int u = 0; u < MB; ++u) mx[u] = args.ws_ml[base + min(s0 + u, nsplit - 1)].x;
+#pragma unroll
+            for (int u = 0; u < MB; ++u) M = fmaxf(M, mx[u]);  // clamped repeats are harmless
+          }
           float Lsum = 0.f, O = 0.f;
-          for (int s2 = 0; s2 < nsplit; ++s2) {
-            const float2 ml = __ldcg(&args.ws_ml[base + s2]);
-            if (ml.x == -INFINITY) continue;
-            const float w = exp2f(ml.x - M);
-            Lsum += ml.y * w;
-            O += __ldcg(&args.ws_o[(base + s2) * HD + e]) * w;
+          for (int s0 = 0; s0 < nsplit; s0 += MB) {
+            float2 ml[MB];
+            float ov[MB];
+#pragma unroll
+            for (int u = 0; u < MB; ++u) {
+              const int64_t sb = base + min(s0 + u, nsplit - 1);
+              ml[u] = args.ws_ml[sb];
+              ov[u] = args.ws_o[sb * HD + e];
+            }
+#pragma unroll
+            for (int u = 0; u < MB; ++u) {
+              if (s0 + u >= nsplit) break;
+              if (ml[u].x == -INFINITY) continue;
+              const float w = exp2f(ml[u].x - M);
+              Lsum += ml[u].y * w;
+              O += ov[u] * w;
+            }
           }
           args.out[static_cast<int64_t>(r) * args.ldo + head * HD + e] =
               f2bf(Lsum > 0.f ? O / Lsum : 0.f);

@@ -766,16 +766,19 @@ __global__ void __launch_bounds__(224, CTAS)
 #pragma unroll
               for (int c = 0; c < 16; ++c) v[c] = 0.f;
               const int npc = pc.c_last - pc.c_first + 1;
-              for (int b0 = 0; b0 < npc; b0 += 2) {  // two pieces' loads in flight, summed in k order
+              // two pieces' loads in flight, summed in k order.  Unconditional weak loads
+              // (piece index clamped): ordered after the other pieces' writes by the
+              // acq_rel counter atomic + epi_sync; the predicated __ldcg form compiled
+              // to one dependent L2 round trip per element.
+              for (int b0 = 0; b0 < npc; b0 += 2) {
                 float x[2][16];
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                  const bool ok = b0 + u < npc;
-                  const float* p = args.sk_slots +
-                                   (int64_t)sk_slot(args, pc.c_first + (ok ? b0 + u : 0), tile) * (BM * BN) +
+                  const int b = b0 + u < npc ? b0 + u : b0;
+                  const float* p = args.sk_slots + (int64_t)sk_slot(args, pc.c_first + b, tile) * (BM * BN) +
                                    row + c0 * BM;
 #pragma unroll
-                  for (int c = 0; c < 16; ++c) x[u][c] = ok ? __ldcg(p + c * BM) : 0.f;
+                  for (int c = 0; c < 16; ++c) x[u][c] = p[c * BM];
                 }
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
@@ -1558,9 +1561,9 @@ bool streamk_enabled() {
 }
 
 // DP + stream-K hybrid for tile counts between one and two waves: opt-in (PL_SK_HYBRID=1).
-// Measured no faster than split-K on Llama-3 gate_up (47.5 vs 44 us at T=64), and its tile
-// counters share the workspace offset of other GEMMs' split-K partials, so it is only
-// safe when every GEMM sharing the workspace also runs stream-K (PL_STREAMK=1).
+// Measured no faster than split-K on Llama-3 gate_up (47.5 vs 44 us at T=64, with the
+// fix-up's loads still serialised).  Tile counters sit in their own region ahead of the
+// split-K partials, so GEMMs of both kinds can share a workspace.
 bool hybrid_enabled() {
   static const bool on = [] {
     const char* v = getenv("PL_SK_HYBRID");
