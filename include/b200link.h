@@ -210,9 +210,11 @@ PL_API int32_t pl_stage_pack_weights(void* handle, void* stream);
 PL_API int32_t pl_stage_destroy(void* handle);
 
 /* Live kernel timing for bench.py: CUDA events around the kernel groups of one
- * layer (layer < 0 disables).  pl_stage_probe_read returns, per recorded
- * forward, out_ms[5] = {qkv gemm, rope+attention, o gemm, gate_up gemm, down
- * gemm} and out_meta[2] = {phase, T}; the stream must be synchronized first. */
+ * layer (a new pass: earlier records cleared; layer < 0 stops recording and keeps
+ * them).  pl_stage_probe_read returns, per recorded forward, out_meta[3] = {phase,
+ * T, kind} and out_ms[5]: kind 0 (one kernel per projection) = {qkv gemm,
+ * rope+attention, o gemm, gate_up gemm, down gemm}; kind 1 (persistent decode
+ * chain) = {decode attention, chain kernel, 0, 0, 0}.  Synchronize the stream first. */
 PL_API int32_t pl_stage_probe(void* handle, int32_t layer);
 PL_API int32_t pl_stage_probe_read(void* handle, float* out_ms_host, int32_t* out_meta_host, int32_t cap,
                             int32_t* n_host);

@@ -63,9 +63,36 @@ def rmsnorm_ref(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
     return (w.float() * y).to(BF16)
 
 
+_ACC = {"splits": 0}
+
+
+class accumulation_order:
+    """Context manager: linear layers sum K in `splits` fp32 partial products added in
+    REVERSED order (a bf16-faithful variant that differs from the default single pass
+    only in fp32 summation order -- the yardstick for the logits tolerance)."""
+
+    def __init__(self, splits: int):
+        self.splits = splits
+
+    def __enter__(self):
+        self.prev, _ACC["splits"] = _ACC["splits"], self.splits
+
+    def __exit__(self, *exc):
+        _ACC["splits"] = self.prev
+
+
 def linear_acc(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     """fp32 accumulator of x[T,K] . w[N,K]^T."""
-    return x.float() @ w.float().t()
+    s = _ACC["splits"]
+    if s <= 1:
+        return x.float() @ w.float().t()
+    K = x.shape[1]
+    step = -(-K // s)
+    parts = [x[:, k:k + step].float() @ w[:, k:k + step].float().t() for k in range(0, K, step)]
+    acc = parts[-1]
+    for p in reversed(parts[:-1]):
+        acc = acc + p
+    return acc
 
 
 def swiglu_ref(acc_gate: torch.Tensor, acc_up: torch.Tensor) -> torch.Tensor:
@@ -161,7 +188,10 @@ class LayerW:
     w_down: torch.Tensor
 
 
-def make_layer(spec: OracleSpec, layer: int, seed: int) -> LayerW:
+def make_layer(spec: OracleSpec, layer: int, seed: int, mk=None) -> LayerW:
+    """Layer weights from the counter hash; `mk(shape, seed, tensor_id, scale, offset)`
+    builds one tensor (default: the numpy generator)."""
+    hash_tensor = mk or globals()["hash_tensor"]
     tid = lambda k: (layer << 4) | k  # noqa: E731
     s, d = spec.weight_scale, spec.d
     qkv_dim = (spec.Hq + 2 * spec.Hkv) * spec.hd
@@ -182,15 +212,17 @@ def make_layer(spec: OracleSpec, layer: int, seed: int) -> LayerW:
     )
 
 
-def make_embed(spec: OracleSpec, seed: int) -> torch.Tensor:
+def make_embed(spec: OracleSpec, seed: int, mk=None) -> torch.Tensor:
+    hash_tensor = mk or globals()["hash_tensor"]
     scale = spec.peaked_embed_scale if spec.peaked else spec.embed_scale
     return hash_tensor((spec.vocab, spec.d), seed, T_EMBED, scale)
 
 
-def make_head(spec: OracleSpec, seed: int) -> tuple[torch.Tensor, torch.Tensor]:
+def make_head(spec: OracleSpec, seed: int, mk=None) -> tuple[torch.Tensor, torch.Tensor]:
+    hash_tensor = mk or globals()["hash_tensor"]
     final_norm = hash_tensor((spec.d,), seed, T_FINAL_NORM, spec.norm_jitter, 1.0)
     if spec.peaked:
-        e = make_embed(spec, seed)
+        e = make_embed(spec, seed, mk)
         lm = (torch.roll(e, shifts=-1, dims=0).float() * spec.lm_alpha).to(BF16)
     else:
         lm = hash_tensor((spec.vocab, spec.d), seed, T_LM_HEAD, spec.weight_scale)
@@ -292,3 +324,37 @@ class OracleModel:
         rows = torch.arange(prompt_ids.numel() - 1, seq.numel())
         hn = rmsnorm_ref(h[rows], self.final_norm, self.spec.eps)
         return linear_acc(hn, self.lm_head)
+
+
+# ------------------------------------------------------ layer-streamed model --
+
+def torch_hash_maker(device="cpu"):
+    """Tensor factory for make_layer & co. on torch (host threads or a GPU's elementwise
+    ops): bit-identical to hash_tensor, the result always on the host."""
+    def mk(shape, seed, tensor_id, scale, offset=0.0):
+        return H.hash_bf16_torch(tuple(shape), seed, tensor_id, scale, offset, device=device).cpu()
+    return mk
+
+
+def stream_forward(spec: OracleSpec, seed: int, seqs: list[torch.Tensor], rows: list[torch.Tensor],
+                   mk=None, lo: int = 0, hi: int | None = None, max_pos: int = 4096):
+    """Whole-model causal forward of independent sequences, ONE LAYER RESIDENT AT A TIME
+    (a 32-layer Llama-3-8B or an 80-layer Qwen2-72B slice never sits in host memory at
+    once).  Returns (hn [sum rows, d] bf16 after the final norm, fp32 logits) at the
+    positions `rows[i]` of sequence i -- e.g. the rows predicting each generated token."""
+    hi = spec.num_layers if hi is None else hi
+    table = rope_table_ref(spec.rope_theta, spec.hd, max_pos)
+    ids = torch.cat(seqs)
+    pos = torch.cat([torch.arange(s.numel()) for s in seqs])
+    seg = [s.numel() for s in seqs]
+    h = make_embed(spec, seed, mk)[ids]
+    e = torch.empty(0, spec.Hkv, spec.hd, dtype=BF16)
+    for l in range(lo, hi):
+        W = make_layer(spec, l, seed, mk)
+        h = layer_forward(spec, W, h, pos, table, [(e, e) for _ in seqs], seg)
+        del W
+    off = np.concatenate([[0], np.cumsum(seg)[:-1]])
+    sel = torch.cat([torch.as_tensor(r, dtype=torch.int64) + int(o) for r, o in zip(rows, off)])
+    final_norm, lm_head = make_head(spec, seed, mk)
+    hn = rmsnorm_ref(h[sel], final_norm, spec.eps)
+    return hn, linear_acc(hn, lm_head)

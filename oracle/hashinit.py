@@ -85,3 +85,51 @@ def hash_bf16_bits(n: int, seed: int, tensor_id: int, scale: float, offset: floa
 def hash_tokens(n: int, seed: int, tensor_id: int, vocab: int, start: int = 0) -> np.ndarray:
     """Prompt token ids: hash mod vocab (int64)."""
     return (hash_u32(n, seed, tensor_id, start).astype(np.int64) % vocab).astype(np.int64)
+
+
+# ------------------------------------------------------------------ torch --
+# The same generator restated on torch int64 tensors (uint32 arithmetic kept in the low
+# 32 bits; int64 products wrap modulo 2^64, which preserves them), so the oracle can
+# build multi-GB weight sets on many host threads -- or on a GPU through torch's own
+# elementwise ops, independent of this repo's kernels.  Bit-identical to
+# hash_bf16_bits / hash_tokens (tests/test_oracle_hash.py).
+
+_M = 0xFFFFFFFF
+
+
+def _mix_t(x):
+    x = x ^ (x >> 16)
+    x = (x * 0x7FEB352D) & _M
+    x = x ^ (x >> 15)
+    x = (x * 0x846CA68B) & _M
+    return x ^ (x >> 16)
+
+
+def hash_u32_torch(n: int, seed: int, tensor_id: int, start: int = 0, device="cpu"):
+    import torch
+
+    key, key2 = keys(seed, tensor_id)
+    h = torch.arange(n, dtype=torch.int64, device=device)
+    h = (h + ((start + key) & _M)) & _M
+    h = _mix_t(h) ^ key2
+    return _mix_t(h)
+
+
+def hash_bf16_torch(shape, seed: int, tensor_id: int, scale: float, offset: float = 0.0,
+                    device="cpu", chunk: int = 1 << 26):
+    """bf16 tensor of `shape` with the bits of hash_bf16_bits (fp32 multiply, then add,
+    then round-to-nearest-even to bf16 -- two separate torch ops, never fused)."""
+    import torch
+
+    n = int(np.prod(shape))
+    mult = float(np.float32(scale) * np.float32(2.0 ** -23))
+    off = float(np.float32(offset))
+    out = torch.empty(n, dtype=torch.bfloat16, device=device)
+    for a in range(0, n, chunk):
+        m = min(chunk, n - a)
+        h = hash_u32_torch(m, seed, tensor_id, a, device)
+        w = ((h >> 8) - 8388608).to(torch.float32) * mult
+        if offset:
+            w = w + off
+        out[a:a + m] = w.to(torch.bfloat16)
+    return out.reshape(shape)

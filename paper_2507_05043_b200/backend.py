@@ -453,9 +453,6 @@ class GpuBackend(Backend):
         ev.record(stream)
         self.fb_events.append((ev, rec.rids))
 
-    def delivered(self, link: int, payload, mb, now_ns: int) -> None:
-        pass
-
     def feedback(self, mb, now_ns: int) -> None:
         rec = self.mbs.pop(mb.id)
         self.free_slots.append(rec.slot)

@@ -62,6 +62,7 @@ int32_t pl_preload_kernels(void) {
   if (!rc) rc = attention_preload();
   if (!rc) rc = kernels_preload();
   if (!rc) rc = transport_preload();
+  if (!rc) rc = chain_preload();
   return rc;
 }
 

@@ -281,7 +281,7 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
 // tokens of every page: S = Q K^T and O += P V on m16n8k16 tensor cores with Q =
 // the GQA group padded to 16 rows (fragments loaded straight from global), per-warp
 // online softmax, warps merged in shared memory.  A request's context is cut into
-// ceil(pages / 8) even splits (its own length only -- batch invariant); the last
+// ceil(pages / 16) even splits (its own length only -- batch invariant); the last
 // split CTA to finish merges the splits in split order.  PDL: pages that were
 // complete before this step are streamed before griddepcontrol.wait; only the page
 // holding the newest token waits for the predecessor kernel.
@@ -294,7 +294,7 @@ int attn_pages_per_split() {
   static const int v = [] {
     const char* e = getenv("PL_ATTN_PPS");
     const int x = e ? atoi(e) : 16;
-    return x > 0 ? x : 16;
+    return (x > 0 && x <= 32) ? x : 16;  // <= 32: block-table entries travel one per lane
   }();
   return v;
 }
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
       // barrier) before the arrival, and the merger's loads after it
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (ct == 0)
-        *last_flag = atomic_add_acq_rel_gpu(&args.counters[r * args.Hkv + kh], 1) == nsplit - 1;
+        *last_flag = atomic_add_acq_rel_gpu(&args.counters[-1 - (r * args.Hkv + kh)], 1) == nsplit - 1;
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*last_flag) {
 #pragma unroll
@@ -697,14 +697,20 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
           args.out[static_cast<int64_t>(r) * args.ldo + head * HD + e] =
               f2bf(Lsum > 0.f ? O / Lsum : 0.f);
         }
-        if (ct == 0) args.counters[r * args.Hkv + kh] = 0;
+        if (ct == 0) args.counters[-1 - (r * args.Hkv + kh)] = 0;
       }
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");  // red_* reused by the next item
   }
 }
 
-// Workspace: [R*Hkv arrival counters, zero between launches | o partials | (m, l)].
+// Workspace: [o partials | (m, l) partials | ... free ... | arrival counters].  The
+// counters sit at the END of the buffer, slot i at word -(1 + i), so a counter's
+// address depends only on (r, kv head) and the buffer size -- never on this launch's R
+// or max_ctx.  They must read zero between launches (the merger resets its own); the
+// partials of any launch that fits the workspace end below every counter slot of any
+// other launch that fits it (the size below reserves R*Hq words for counters), so
+// launches of different shapes can share one workspace sized for the largest.
 int64_t attn_decode_workspace_bytes(int R, int Hq, int max_ctx, int hd) {
   const int pages = (max_ctx + PAGE - 1) / PAGE;
   const int nsplit = std::max(1, (pages + attn_pages_per_split() - 1) / attn_pages_per_split());
@@ -736,11 +742,9 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
   const int64_t rows = num_blocks * Hkv * PAGE;
   if ((rc = make_tma_2d(&mk, k_cache, rows, HD, HD, 64))) return rc;
   if ((rc = make_tma_2d(&mv, v_cache, rows, HD, HD, 64))) return rc;
-  // counters are sized for R*Hq (>= R*Hkv) so the layout only depends on (R, Hq, max_ctx)
-  const int64_t counter_bytes = ((static_cast<int64_t>(R) * Hq * 4 + 255) / 256) * 256;
-  int* counters = need > 0 ? reinterpret_cast<int*>(ws) : nullptr;
-  float* ws_o = need > 0 ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + counter_bytes)
-                         : nullptr;
+  int* counters = need > 0 ? reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + (ws_bytes & ~int64_t(3)))
+                           : nullptr;  // one past the last word; slot i at counters[-1 - i]
+  float* ws_o = need > 0 ? reinterpret_cast<float*>(ws) : nullptr;
   float2* ws_ml = need > 0 ? reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(ws_o) +
                                                        static_cast<int64_t>(R) * Hq * nsplit * hd * 4)
                            : nullptr;

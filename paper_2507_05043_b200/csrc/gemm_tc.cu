@@ -69,26 +69,15 @@ struct GemmArgs {
   float* partial;     // split-K partials, fp32: pmode 0 [splits][N][Tp], pmode 1 [splits][T][N]
   int Tp;             // T rounded up to the BN tile
   int pmode;
-  int l2_prefetch;    // weight k-blocks warmed in L2 beyond the smem ring before the PDL wait
   float2* argmax_ws;  // [N/128 tiles][T] (value, index-as-float-bits)
-  // stream-K (decode / SWAP): CTA c owns the flattened (tile, k-block) iterations
-  // [c*base + min(c, extra), +base + (c < extra)); tiles shared by several CTAs are
-  // reduced by the last arriving CTA from per-piece fp32 slots, in k order.
   const uint8_t* wp;  // pre-packed weights (pl_pack_weight): 16 KB SW128 tile images, [N/128][K/64]
   int swiglu_il;      // packed gate_up: rows alternate gate_j, up_j inside each 128-row tile
   int raster_m;       // > 0: grouped tile raster, bands of raster_m row tiles (prefill)
-  int streamk;
-  int sk_dp;          // hybrid: CTAs [0, sk_dp) each own full tile blockIdx (data-parallel);
-                      // the stream-K part covers tiles [sk_dp, tiles_m) with CTAs sk_dp..grid-1
-  int sk_base, sk_extra;
-  float* sk_slots;    // [2 * stream-K CTAs][BN][BM] fp32 (column-major: coalesced per column)
-  int* sk_counters;   // [tiles_m], zero between launches (the fixer resets its tile)
   // cluster split-K (decode / SWAP): the `splits` CTAs of one weight tile form a cluster,
   // each parks its fp32 partial in its own (idle) ring memory and the cluster reduces
   // over distributed shared memory -- no partial round trip through HBM/L2, no reduce
   // kernel.  rope: the reduction also applies RoPE + the paged K/V append
   // (reduce_qkv_rope_kernel's math; a 128-feature tile is one head).
-  int act_lane;       // experiments (PL_ACT_LANE=1): activation producer on warp 0 lane 1
   int csk;
   int rope;
   const int32_t* pos;
@@ -103,89 +92,17 @@ struct GemmArgs {
 // One unit of work: k-blocks [kb0, kb0 + nkb) of output tile (m_tile, n_tile).
 struct Piece {
   int m_tile, n_tile, split, kb0, nkb;
-  int partial;        // stream-K: the tile is shared with other CTAs
-  int slot;           // stream-K: this piece's fp32 slot
-  int c_first, c_last;  // stream-K: CTAs covering the tile (k order)
 };
 
-// Stream-K coordinates are local: CTA c = blockIdx - sk_dp, iteration 0 = the first
-// k-block of tile sk_dp.
-PL_DEV int sk_start(const GemmArgs& a, int c) { return c * a.sk_base + min(c, a.sk_extra); }
-PL_DEV int sk_cta_of(const GemmArgs& a, int it) {
-  const int big = a.sk_extra * (a.sk_base + 1);
-  return it < big ? it / (a.sk_base + 1) : a.sk_extra + (it - big) / a.sk_base;
-}
-// slot of CTA c's piece in local tile t: its second slot when c's range began in an
-// earlier tile (then the piece is c's last), else its first
-PL_DEV int sk_slot(const GemmArgs& a, int c, int tile) {
-  return (sk_start(a, c) < tile * a.num_kb) ? 2 * c + 1 : 2 * c;
-}
-
-// Walks this CTA's pieces (identical in the producer, MMA and epilogue roles).
-// Stream-K order: the piece in the CTA's LAST tile first, then the rest in k order.
-// A shared tile's head is the last piece of one CTA and its tail the first piece of
-// the next, so both finish early in their CTAs and the fix-up overlaps the mainloop
-// of the CTA's remaining (full) tiles instead of trailing the kernel.
+// Walks this CTA's pieces (identical in the producer, MMA and epilogue roles):
+// items blockIdx.x, blockIdx.x + gridDim.x, ...
 struct PieceWalk {
-  int it, end;        // cursor / end of the in-order part
-  int last0, last1;   // the hoisted last-tile piece [last0, last1), empty when done
-  int dp;             // hybrid data-parallel CTA: one full tile, then done
+  int it, end;
   PL_DEV void init(const GemmArgs& a) {
-    dp = a.streamk && static_cast<int>(blockIdx.x) < a.sk_dp;
-    if (dp) {
-      it = 0, end = 1, last0 = last1 = 0;
-      return;
-    }
-    if (a.streamk) {
-      const int c = static_cast<int>(blockIdx.x) - a.sk_dp;
-      const int s0 = sk_start(a, c);
-      const int e0 = s0 + a.sk_base + (c < a.sk_extra ? 1 : 0);
-      const int lt = max(s0, ((e0 - 1) / a.num_kb) * a.num_kb);  // start of the last tile's piece
-      if (lt > s0) {
-        last0 = lt, last1 = e0;
-        it = s0, end = lt;
-      } else {
-        last0 = last1 = 0;
-        it = s0, end = e0;
-      }
-    } else {
-      it = blockIdx.x;
-      end = a.num_items;
-      last0 = last1 = 0;
-    }
+    it = blockIdx.x;
+    end = a.num_items;
   }
   PL_DEV bool next(const GemmArgs& a, Piece& p) {
-    if (dp) {
-      if (it >= end) return false;
-      it = end;
-      p.m_tile = blockIdx.x, p.n_tile = 0, p.split = 0, p.kb0 = 0, p.nkb = a.num_kb;
-      p.partial = 0, p.slot = 0, p.c_first = p.c_last = 0;
-      return true;
-    }
-    if (a.streamk) {
-      int k_it, k_end;
-      if (last1 > last0) {
-        k_it = last0, k_end = last1;
-        last0 = last1 = 0;
-      } else {
-        if (it >= end) return false;
-        k_it = it, k_end = end;
-      }
-      const int tile = k_it / a.num_kb;  // local tile
-      const int k0 = k_it % a.num_kb;
-      const int k1 = min(a.num_kb, k0 + (k_end - k_it));
-      p.m_tile = a.sk_dp + tile;
-      p.n_tile = 0;
-      p.split = 0;
-      p.kb0 = k0;
-      p.nkb = k1 - k0;
-      p.c_first = sk_cta_of(a, tile * a.num_kb);
-      p.c_last = sk_cta_of(a, tile * a.num_kb + a.num_kb - 1);
-      p.partial = p.c_first != p.c_last;
-      p.slot = sk_slot(a, static_cast<int>(blockIdx.x) - a.sk_dp, tile);
-      if (k_it == it) it += k1 - k0;
-      return true;
-    }
     if (it >= end) return false;
     p.split = it % a.splits;
     const int tile = it / a.splits;
@@ -206,7 +123,6 @@ struct PieceWalk {
     }
     p.kb0 = p.split * a.kb_per_split;
     p.nkb = min(a.num_kb, p.kb0 + a.kb_per_split) - p.kb0;
-    p.partial = 0;
     it += gridDim.x;
     return true;
   }
@@ -519,25 +435,14 @@ __global__ void __launch_bounds__(224, CTAS)
       PieceWalk walk;
       walk.init(args);
       Piece pc;
-      bool first = true;
       while (walk.next(args, pc)) {
         const int m_tile = pc.m_tile, n_tile = pc.n_tile, kb0 = pc.kb0, nkb = pc.nkb;
-        if (SWAP && first && args.l2_prefetch) {
-          const int pf_end = min(nkb, AS + args.l2_prefetch);
-          for (int j = AS; j < pf_end; ++j) {
-            if (args.wp)
-              bulk_prefetch_l2(args.wp + ((int64_t)m_tile * args.num_kb + kb0 + j) * A_TILE_BYTES, A_TILE_BYTES);
-            else
-              tma_prefetch_l2_2d(&tmA, (kb0 + j) * BK, m_tile * BM);
-          }
-        }
-        first = false;
         for (int i = 0; i < nkb; ++i) {
           if (SWAP) issue_a(kb0 + i, m_tile);
           else issue_b(kb0 + i, n_tile);
         }
       }
-    } else if (args.act_lane ? (warp == 0 && lane == 1) : (warp == GEMM_ACT_WARP && lane == 0)) {
+    } else if (warp == GEMM_ACT_WARP && lane == 0) {
       const uint64_t pol_x = policy_evict_last();
       const uint64_t polA = pol_x, polB = pol_x;
       int sa = 0, sb = 0;
@@ -620,7 +525,6 @@ __global__ void __launch_bounds__(224, CTAS)
     const int ep = threadIdx.x - 64;              // 0..127
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const int epi = args.epi;
-    int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
     int acc = 0;
     uint32_t aphase = 0;
     PieceWalk walk;
@@ -740,59 +644,6 @@ __global__ void __launch_bounds__(224, CTAS)
           for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(r[c]);
         };
 
-        if (args.streamk && pc.partial) {
-          // stream-K piece of a shared tile: fp32 slot, then the last arriver reduces
-          float* sp = args.sk_slots + (int64_t)pc.slot * (BM * BN) + row;  // [col][BM]: lanes coalesce
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            float v[16];
-            fetch_tmem(c0, v);
-#pragma unroll
-            for (int c = 0; c < 16; ++c) sp[(c0 + c) * BM] = v[c];
-          }
-          release_tmem();
-          epi_sync();
-          if (ep == 0) {
-            int old;
-            asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;"
-                         : "=r"(old)
-                         : "l"(args.sk_counters + m_tile), "r"(1)
-                         : "memory");
-            *sk_flag = old == pc.c_last - pc.c_first;
-          }
-          epi_sync();
-          if (*sk_flag) {
-            const int tile = m_tile - args.sk_dp;  // local
-            auto fetch_slots = [&](int c0, float (&v)[16]) {
-#pragma unroll
-              for (int c = 0; c < 16; ++c) v[c] = 0.f;
-              const int npc = pc.c_last - pc.c_first + 1;
-              // two pieces' loads in flight, summed in k order.  Unconditional weak loads
-              // (piece index clamped): ordered after the other pieces' writes by the
-              // acq_rel counter atomic + epi_sync; the predicated __ldcg form compiled
-              // to one dependent L2 round trip per element.
-              for (int b0 = 0; b0 < npc; b0 += 2) {
-                float x[2][16];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                  const int b = b0 + u < npc ? b0 + u : b0;
-                  const float* p = args.sk_slots + (int64_t)sk_slot(args, pc.c_first + b, tile) * (BM * BN) +
-                                   row + c0 * BM;
-#pragma unroll
-                  for (int c = 0; c < 16; ++c) x[u][c] = p[c * BM];
-                }
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                  if (b0 + u >= npc) break;
-#pragma unroll
-                  for (int c = 0; c < 16; ++c) v[c] += x[u][c];
-                }
-              }
-            };
-            final_epi(fetch_slots);
-            if (ep == 0) args.sk_counters[m_tile] = 0;
-          }
-          continue;
-        }
         if (args.csk) {
           // cluster split-K: park this split's tile in the ring (all its loads were
           // consumed by now), column-major [token][feature] so the reducers' lanes coalesce
@@ -1438,10 +1289,9 @@ int launch_pair_s(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& 
   return launch_k("gemm_pair_kernel", gemm_pair_kernel<S>, dim3(grid), dim3(GEMM_THREADS), PairSmem<S>::TOTAL, st, ma, mb,
                   a);
 }
-// ring depth: PL_PAIR_STAGES=6 (default 7 = 224 KB of 32 KB stages)
+// ring depth 7 = 224 KB of 32 KB stages
 int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid, cudaStream_t st) {
-  static const int stages = [] { const char* v = getenv("PL_PAIR_STAGES"); return v ? atoi(v) : 7; }();
-  return stages == 6 ? launch_pair_s<6>(ma, mb, a, grid, st) : launch_pair_s<7>(ma, mb, a, grid, st);
+  return launch_pair_s<7>(ma, mb, a, grid, st);
 }
 
 template <int BN, bool SWAP, int CTAS = (BN <= 128 ? 2 : 1)>
@@ -1491,44 +1341,9 @@ int make_tma_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, i
 // split keeping >= 4 k-blocks.
 int gemm_num_splits(int64_t N, int64_t K, bool swap) {
   if (!swap) return 1;
-  static const int forced = [] {  // experiments only (scripts/bench_gemm.py --splits)
-    const char* v = getenv("PL_SPLITK_FORCE");
-    return v ? atoi(v) : 0;
-  }();
-  if (forced > 0) return static_cast<int>(std::min<int64_t>(forced, K / BK));
-  // PL_SPLITS="N:K:s,...": per-shape override (experiments; still a function of (N, K) only)
-  static const std::vector<std::array<int64_t, 3>> per_shape = [] {
-    std::vector<std::array<int64_t, 3>> v;
-    const char* e = getenv("PL_SPLITS");
-    long long n, k, s;
-    int used;
-    while (e && sscanf(e, "%lld:%lld:%lld%n", &n, &k, &s, &used) == 3) {
-      v.push_back({n, k, s});
-      e += used;
-      if (*e == ',') ++e;
-    }
-    return v;
-  }();
-  for (const auto& o : per_shape)
-    if (o[0] == N && o[1] == K && o[2] > 0) return static_cast<int>(std::min<int64_t>(o[2], K / BK));
   const int64_t tiles = (N + BM - 1) / BM;
   const int64_t kb = K / BK;
-  // PL_SPLIT_RULE=fit: the largest split with tiles*splits <= 148 (every CTA on its own
-  // SM, so the next GEMM's CTAs can become resident beside it); default: the smallest
-  // split with tiles*splits >= 148
-  static const bool fit = [] { const char* v = getenv("PL_SPLIT_RULE"); return v && v[0] == 'f'; }();
   const int64_t sms = 148;
-  if (fit) {
-    int best = 1;
-    for (int s = 1; s <= 16; ++s) {
-      const int64_t per = (kb + s - 1) / s;
-      if (s > 1 && per < 4) break;
-      const int eff = static_cast<int>((kb + per - 1) / per);
-      if (tiles * eff > sms) break;
-      best = eff;
-    }
-    return best;
-  }
   int best = 1;
   for (int s = 1; s <= 16; ++s) {
     const int64_t per = (kb + s - 1) / s;
@@ -1549,28 +1364,6 @@ int gemm_num_splits(int64_t N, int64_t K, bool swap) {
   return best;
 }
 
-// Stream-K (decode / SWAP path) is opt-in (PL_STREAMK=1): at 296 CTAs the pieces of
-// the small projections are a few k-blocks and the serial last-arriver fix-up costs
-// more than the balance it buys.  Default: uniform split-K + parallel reduce kernels.
-bool streamk_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("PL_STREAMK");
-    return v && v[0] == '1';
-  }();
-  return on;
-}
-
-// DP + stream-K hybrid for tile counts between one and two waves: opt-in (PL_SK_HYBRID=1).
-// Measured no faster than split-K on Llama-3 gate_up (47.5 vs 44 us at T=64, with the
-// fix-up's loads still serialised).  Tile counters sit in their own region ahead of the
-// split-K partials, so GEMMs of both kinds can share a workspace.
-bool hybrid_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("PL_SK_HYBRID");
-    return v && v[0] == '1';
-  }();
-  return on;
-}
 // Prefill (!SWAP) GEMMs on CTA pairs (cta_group::2, 256 x 256 tiles).  PL_GEMM_PAIR=0 /
 // 1 forces it off / on; default on for >= 512 tokens.
 bool use_pair(bool swap, int64_t T) {
@@ -1579,49 +1372,16 @@ bool use_pair(bool swap, int64_t T) {
   return env == 1 || T >= 512;
 }
 
-int64_t sk_dp_tiles(int64_t N);
-bool use_streamk(bool swap, int64_t N) {
-  return swap && (streamk_enabled() || (hybrid_enabled() && sk_dp_tiles(N) > 0));
-}
-
-// Stream-K grid: a constant (two CTAs per SM) so piece boundaries -- and therefore
-// every token's summation order -- depend on (N, K) only, never on T.
-// Hybrid for SMs < tiles < 2*SMs (Llama-3 gate_up: 224 tiles): one full tile per SM
-// data-parallel (no fix-up) plus the remaining tiles stream-K'd over one more CTA per
-// SM, so every SM streams the same weight bytes; otherwise plain stream-K.
-int64_t sk_dp_tiles(int64_t N) {
-  const int64_t tiles = (N + BM - 1) / BM, sms = num_sms();
-  return (tiles > sms && tiles < 2 * sms) ? sms : 0;
-}
-int64_t sk_grid(int64_t N, int64_t K) {
-  const int64_t tiles = (N + BM - 1) / BM;
-  const int64_t dp = sk_dp_tiles(N);
-  if (dp) return 2 * num_sms();  // dp + num_sms() stream-K CTAs, two CTAs per SM
-  return std::min<int64_t>(num_sms(), tiles * (K / BK));  // one CTA per SM, deep ring
-}
-
-// Tile counters sit at the same offset for every stream-K GEMM sharing a workspace
-// (the fixer of each tile zeroes its counter, so they stay zero between launches).
-constexpr int64_t SK_COUNTER_BYTES = 64 * 1024;  // up to 16384 weight tiles
-
-// Workspace (SWAP):  stream-K  [tile counters | argmax partials | 2*grid fp32 slots]
-//                    split-K   [splits][N][Tp] fp32 partials, or argmax partials [tiles][T]
+// Workspace (SWAP): split-K partials [splits][N][Tp] fp32, or argmax partials [tiles][T].
 int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi) {
   const bool swap = use_swap(T, epi);
   const int64_t tiles = (N + BM - 1) / BM;
-  const int64_t argmax = epi == EPI_ARGMAX ? align256(tiles * T * 8) : 0;
-  if (use_streamk(swap, N)) {
-    const int64_t bn = swap_bn(T);
-    return SK_COUNTER_BYTES + argmax + 2 * sk_grid(N, K) * BM * bn * 4;
-  }
-  // split-K partials / argmax partials sit after the (untouched) stream-K counter region,
-  // so GEMMs of either kind can share one workspace
-  if (epi == EPI_ARGMAX) return SK_COUNTER_BYTES + tiles * T * 8;
+  if (epi == EPI_ARGMAX) return tiles * T * 8;
   const int splits = gemm_num_splits(N, K, swap);
   if (splits <= 1) return 0;
   const int64_t bn = swap_bn(T);
   const int64_t tiles_n = (T + bn - 1) / bn;
-  return SK_COUNTER_BYTES + static_cast<int64_t>(splits) * N * (tiles_n * bn) * 4;
+  return static_cast<int64_t>(splits) * N * (tiles_n * bn) * 4;
 }
 
 int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int64_t ldw,
@@ -1646,8 +1406,6 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     return set_error(PL_ERR_CONFIG, "gemm: N and leading dims must be multiples of 16/8");
 
   GemmArgs a{};
-  static const int act_lane = [] { const char* v = getenv("PL_ACT_LANE"); return v ? atoi(v) : 0; }();
-  a.act_lane = act_lane;
   a.T = static_cast<int>(T);
   a.N = static_cast<int>(N);
   if (w_packed) {
@@ -1663,62 +1421,34 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   a.bias = bias;
   a.residual = residual;
   a.ldr = ldr;
-  const bool sk = use_streamk(swap, N);
-  a.splits = (epi == EPI_ARGMAX || sk) ? 1 : gemm_num_splits(N, K, swap);
+  a.splits = epi == EPI_ARGMAX ? 1 : gemm_num_splits(N, K, swap);
   a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
   const int bn = swap ? swap_bn(T) : 256;
   a.tiles_m = static_cast<int>(swap ? (N + BM - 1) / BM : (T + BM - 1) / BM);
   const int tiles_n = static_cast<int>(swap ? (T + bn - 1) / bn : (N + bn - 1) / bn);
   a.num_items = a.tiles_m * tiles_n * a.splits;
-  static const int raster = [] { const char* v = getenv("PL_RASTER_M"); return v ? atoi(v) : 32; }();
+  constexpr int raster = 32;  // prefill tile band (profiles/r1/prefill_raster_sweep.log)
   a.raster_m = (!swap && tiles_n > 1 && a.tiles_m > raster) ? raster : 0;
   a.Tp = tiles_n * bn;
-  // split-K: the fused epilogues are the partial reduction kernels; stream-K: the GEMM
-  // writes final values and the fusion's second half runs as its own small kernel
-  const int fkind = (fuse && swap && (a.splits > 1 || sk)) ? fuse->kind : FUSE_NONE;
+  // split-K: the fused epilogues are the partial reduction kernels
+  const int fkind = (fuse && swap && a.splits > 1) ? fuse->kind : FUSE_NONE;
   if (fkind == FUSE_RESIDUAL_NORM && (epi != EPI_RESIDUAL || N > 8192 || N % 4))
     return set_error(PL_ERR_CONFIG, "gemm: residual+norm fusion needs a RESIDUAL GEMM, N <= 8192");
   if (fkind == FUSE_QKV_ROPE && (epi != EPI_STORE && epi != EPI_BIAS))
     return set_error(PL_ERR_CONFIG, "gemm: qkv+rope fusion needs a STORE/BIAS GEMM");
-  a.pmode = (fkind == FUSE_RESIDUAL_NORM && !sk) ? 1 : 0;
-  // L2 warm-up only for weights that comfortably fit the 126 MB L2 (PL_L2PF overrides)
-  // measured (scripts/l2pf_sweep.sh): warming L2 beyond the ring only slows the decode chain
-  static const int l2pf = [] { const char* v = getenv("PL_L2PF"); return v ? atoi(v) : 0; }();
-  static const int64_t l2pf_max = [] {
-    const char* v = getenv("PL_L2PF_MAXMB");
-    return (v ? atoll(v) : 64) << 20;
-  }();
-  a.l2_prefetch = (swap && N * K * 2 <= l2pf_max) ? l2pf : 0;
+  a.pmode = fkind == FUSE_RESIDUAL_NORM ? 1 : 0;
   const int64_t need = gemm_workspace_bytes(T, N, K, epi);
   if (need > 0 && (ws_bytes < need || !ws))
     return set_error(PL_ERR_CONFIG, "gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
                      (long long)need);
   int grid, cluster = 0;
-  // PL_GEMM_WIDE=1: one CTA per SM with a deep (~196 KB) ring instead of two shallower ones
-  static const bool wide = [] { const char* v = getenv("PL_GEMM_WIDE"); return v && v[0] == '1'; }();
-  if (sk) {
-    if (a.tiles_m * 4 > SK_COUNTER_BYTES) return set_error(PL_ERR_CONFIG, "gemm: N too large");
-    uint8_t* w8 = static_cast<uint8_t*>(ws);
-    const int64_t argmax_bytes = epi == EPI_ARGMAX ? align256(a.tiles_m * T * 8) : 0;
-    a.sk_counters = reinterpret_cast<int*>(w8);
-    if (epi == EPI_ARGMAX) a.argmax_ws = reinterpret_cast<float2*>(w8 + SK_COUNTER_BYTES);
-    a.sk_slots = reinterpret_cast<float*>(w8 + SK_COUNTER_BYTES + argmax_bytes);
-    grid = static_cast<int>(sk_grid(N, K));
-    a.streamk = 1;
-    a.sk_dp = static_cast<int>(sk_dp_tiles(N));
-    const int sk_ctas = grid - a.sk_dp;
-    const int64_t total = static_cast<int64_t>(a.tiles_m - a.sk_dp) * a.num_kb;
-    a.sk_base = static_cast<int>(total / sk_ctas);
-    a.sk_extra = static_cast<int>(total % sk_ctas);
-    a.num_items = static_cast<int>(total);
-  } else {
+  {
     if (epi == EPI_ARGMAX) {
-      a.argmax_ws = reinterpret_cast<float2*>(static_cast<uint8_t*>(ws) + SK_COUNTER_BYTES);
+      a.argmax_ws = static_cast<float2*>(ws);
     } else if (a.splits > 1) {
-      a.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + SK_COUNTER_BYTES);
+      a.partial = static_cast<float*>(ws);
     }
-    static const int per_sm_env = [] { const char* v = getenv("PL_GRID_PER_SM"); return v ? atoi(v) : 0; }();
-    const int per_sm = per_sm_env > 0 ? per_sm_env : (swap && bn <= 128 && !wide) ? 2 : 1;
+    const int per_sm = (swap && bn <= 128) ? 2 : 1;
     grid = std::min(a.num_items, num_sms() * per_sm);
     // cluster split-K (default on; PL_CSK=0 restores partials + reduce kernels): one wave,
     // one tile per cluster of `splits` CTAs
@@ -1757,12 +1487,11 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   if (swap) {
     if ((rc = make_map(&ma, W, N, K, ldw, BM))) return rc;
     if ((rc = make_map(&mb, X, T, K, ldx, bn))) return rc;
-    const bool w1 = wide || (sk && !sk_dp_tiles(N));  // pure stream-K: one CTA per SM, deep ring
     switch (bn) {
-      case 16: rc = w1 ? launch_tc<16, true, 1>(ma, mb, a, grid, st, cluster) : launch_tc<16, true>(ma, mb, a, grid, st, cluster); break;
-      case 32: rc = w1 ? launch_tc<32, true, 1>(ma, mb, a, grid, st, cluster) : launch_tc<32, true>(ma, mb, a, grid, st, cluster); break;
-      case 64: rc = w1 ? launch_tc<64, true, 1>(ma, mb, a, grid, st, cluster) : launch_tc<64, true>(ma, mb, a, grid, st, cluster); break;
-      case 128: rc = w1 ? launch_tc<128, true, 1>(ma, mb, a, grid, st, cluster) : launch_tc<128, true>(ma, mb, a, grid, st, cluster); break;
+      case 16: rc = launch_tc<16, true>(ma, mb, a, grid, st, cluster); break;
+      case 32: rc = launch_tc<32, true>(ma, mb, a, grid, st, cluster); break;
+      case 64: rc = launch_tc<64, true>(ma, mb, a, grid, st, cluster); break;
+      case 128: rc = launch_tc<128, true>(ma, mb, a, grid, st, cluster); break;
       default: rc = launch_tc<256, true>(ma, mb, a, grid, st, cluster); break;
     }
   } else if (use_pair(swap, T)) {
@@ -1805,16 +1534,6 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
                       fuse->norm_out, fuse->ld_norm);
     }
     return PL_OK;
-  }
-  if (sk && fkind == FUSE_RESIDUAL_NORM) {  // h (= C) is final: the next RMSNorm reads it
-    if (fused) *fused = true;
-    return rmsnorm_launch(C, ldc, nullptr, fuse->norm_w, fuse->eps, T, static_cast<int>(N), fuse->norm_out,
-                          fuse->ld_norm, st);
-  }
-  if (sk && fkind == FUSE_QKV_ROPE) {  // qkv (= C) is final: RoPE + paged KV append
-    if (fused) *fused = true;
-    return rope_kv_launch(C, ldc, fuse->pos, fuse->slot, fuse->cos_sin, fuse->max_pos, fuse->k_cache,
-                          fuse->v_cache, fuse->block_size, T, fuse->Hq, fuse->Hkv, 128, st);
   }
   if (fkind == FUSE_RESIDUAL_NORM) {
     if (fused) *fused = true;
@@ -1892,13 +1611,8 @@ int gemm_preload() {
   if (!rc) rc = preload_one(gemm_tc_kernel<32, true, 2>, "gemm_tc_kernel");
   if (!rc) rc = preload_one(gemm_tc_kernel<64, true, 2>, "gemm_tc_kernel");
   if (!rc) rc = preload_one(gemm_tc_kernel<128, true, 2>, "gemm_tc_kernel");
-  if (!rc) rc = preload_one(gemm_tc_kernel<16, true, 1>, "gemm_tc_kernel");
-  if (!rc) rc = preload_one(gemm_tc_kernel<32, true, 1>, "gemm_tc_kernel");
-  if (!rc) rc = preload_one(gemm_tc_kernel<64, true, 1>, "gemm_tc_kernel");
-  if (!rc) rc = preload_one(gemm_tc_kernel<128, true, 1>, "gemm_tc_kernel");
   if (!rc) rc = preload_one(gemm_tc_kernel<256, true, 1>, "gemm_tc_kernel");
   if (!rc) rc = preload_one(gemm_tc_kernel<256, false, 1>, "gemm_tc_kernel");
-  if (!rc) rc = preload_one(gemm_pair_kernel<6>, "gemm_pair_kernel");
   if (!rc) rc = preload_one(gemm_pair_kernel<7>, "gemm_pair_kernel");
   if (!rc) rc = preload_one(argmax_reduce_kernel, "argmax_reduce_kernel");
   if (!rc) rc = preload_one(reduce_residual_norm_kernel<1>, "reduce_residual_norm_kernel");

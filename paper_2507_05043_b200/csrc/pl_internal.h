@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "../../include/b200link.h"
 
@@ -138,6 +139,42 @@ int rope_kv_launch(__nv_bfloat16* qkv, int64_t ldqkv, const int32_t* pos, const 
 int token_scatter_launch(const int64_t* ids, const int32_t* req_slot, const int32_t* out_pos,
                          int R, int64_t* last_token, int64_t* gen_tokens, int gen_stride,
                          cudaStream_t st);
+
+// chain.cu -- persistent decode-layer kernel (o -> norm -> gate_up -> down -> norm -> qkv)
+enum ChainKind : int { CHAIN_O = 0, CHAIN_GATE_UP = 1, CHAIN_DOWN = 2, CHAIN_QKV = 3 };
+struct ChainLaunch {
+  int T = 0, Tp = 0, njobs = 0, d = 0, ffn = 0, attn_dim = 0, grid = 0;
+  int kind[4] = {0, 0, 0, 0};
+  int64_t N[4] = {0, 0, 0, 0}, K[4] = {0, 0, 0, 0};
+  int splits[4] = {1, 1, 1, 1};
+  const void* w[4] = {nullptr, nullptr, nullptr, nullptr};  // packed weights (pack_weight_launch)
+  float* partial[4] = {nullptr, nullptr, nullptr, nullptr};
+  int* arrive[4] = {nullptr, nullptr, nullptr, nullptr};
+  const int4* units = nullptr;
+  const int* unit_off = nullptr;
+  const __nv_bfloat16* o_attn = nullptr;
+  __nv_bfloat16 *h = nullptr, *a = nullptr, *m = nullptr, *q_out = nullptr;
+  int64_t ld_q = 0;
+  float* ss = nullptr;
+  const __nv_bfloat16* norm_w[2] = {nullptr, nullptr};
+  int has_norm[2] = {0, 0};
+  float eps = 0.f;
+  const __nv_bfloat16* bias = nullptr;
+  const int32_t *pos = nullptr, *slot = nullptr;
+  const __nv_bfloat16* cos_sin = nullptr;
+  int max_pos = 0;
+  __nv_bfloat16 *k_cache = nullptr, *v_cache = nullptr;
+  int block_size = 0, Hq = 0, Hkv = 0;
+  unsigned long long* ctr = nullptr;
+  unsigned long long tgt[4] = {0, 0, 0, 0};
+  int* gu_flag = nullptr;
+  int seq = 0;
+};
+int chain_plan(const int* kinds, int njobs, const int64_t* N, const int64_t* K, int grid, int ring,
+               int* splits_out, std::vector<int4>& units, std::vector<int>& offs);
+int chain_ring_kb(int BN);
+int chain_launch(const ChainLaunch& c, cudaStream_t st);
+int chain_preload();
 
 // attention.cu
 int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* cu_seqlens, int R,

@@ -295,7 +295,7 @@ class Engine {
 
   int64_t cns(int s, int phase, int64_t tokens) {
     auto& m = cns_[phase];
-    const int64_t key = tokens * 64 + s;
+    const int64_t key = tokens * static_cast<int64_t>(c_.profiles.size()) + s;  // unique for any S
     auto it = m.find(key);
     if (it != m.end()) return it->second;
     const int64_t v = compute_ns(c_.profiles[s], phase, tokens);

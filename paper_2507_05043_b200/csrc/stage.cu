@@ -29,8 +29,93 @@ namespace {
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 struct Layout {
-  int64_t a, qkv, o, m, hn, gemm_ws, attn_ws, total;
+  int64_t a, qkv, o, m, hn, gemm_ws, attn_ws, chain, total;
 };
+
+// Decode layers run as persistent chain kernels (chain.cu) when the stage's projection
+// weights are packed and T <= 256.  Three chain shapes per stage: the first layer's qkv,
+// a middle layer (o, gate_up, down, next qkv) and the last layer (o, gate_up, down).
+enum ChainType { CH_QKV_ONLY = 0, CH_FULL = 1, CH_LAST = 2, CH_TYPES = 3 };
+
+struct ChainPlan {
+  int njobs = 0;
+  int kind[4] = {0, 0, 0, 0};
+  int64_t N[4] = {0, 0, 0, 0}, K[4] = {0, 0, 0, 0};
+  int splits[4] = {1, 1, 1, 1};
+  std::vector<int4> units;
+  std::vector<int> offs;
+  int64_t units_off = 0, offs_off = 0;  // byte offsets inside the chain region
+};
+
+struct ChainLayout {
+  ChainPlan plan[CH_TYPES];
+  int grid = 0, Tp_max = 0;
+  int64_t partial[4] = {0, 0, 0, 0}, arrive[4] = {0, 0, 0, 0};  // by ChainKind
+  int64_t ss = 0, ctr = 0, gu_flag = 0, bytes = 0;
+};
+
+int chain_tp(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
+
+ChainLayout chain_layout(const pl_stage_config& c, int grid) {
+  ChainLayout C;
+  C.grid = grid;
+  if (grid <= 0 || c.num_layers <= 0) return C;
+  const int64_t d = c.d, qkv_dim = static_cast<int64_t>(c.Hq + 2 * c.Hkv) * c.hd;
+  const int64_t attn_dim = static_cast<int64_t>(c.Hq) * c.hd, ffn = c.ffn;
+  C.Tp_max = chain_tp(std::min(c.max_reqs, 256));
+  const int64_t NN[4] = {d, 2 * ffn, d, qkv_dim}, KK[4] = {attn_dim, d, ffn, d};
+  const int kinds[CH_TYPES][4] = {{CHAIN_QKV, 0, 0, 0}, {CHAIN_O, CHAIN_GATE_UP, CHAIN_DOWN, CHAIN_QKV},
+                                  {CHAIN_O, CHAIN_GATE_UP, CHAIN_DOWN, 0}};
+  const int nj[CH_TYPES] = {1, 4, 3};
+  int max_split[4] = {1, 1, 1, 1};
+  const int ring = chain_ring_kb(64);  // planning uses one ring depth for every T
+  for (int t = 0; t < CH_TYPES; ++t) {
+    ChainPlan& P = C.plan[t];
+    P.njobs = nj[t];
+    for (int j = 0; j < P.njobs; ++j) {
+      P.kind[j] = kinds[t][j];
+      P.N[j] = NN[P.kind[j]];
+      P.K[j] = KK[P.kind[j]];
+    }
+    chain_plan(P.kind, P.njobs, P.N, P.K, grid, ring, P.splits, P.units, P.offs);
+    for (int j = 0; j < P.njobs; ++j) max_split[P.kind[j]] = std::max(max_split[P.kind[j]], P.splits[j]);
+  }
+  int64_t off = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int64_t tiles = NN[k] / 128;
+    C.partial[k] = off;
+    off += align256(max_split[k] > 1 ? max_split[k] * tiles * C.Tp_max * 128 * 4 : 0);
+    C.arrive[k] = off;
+    off += align256(tiles * 4);
+  }
+  C.ss = off;
+  off += align256(2 * (d / 128) * C.Tp_max * 4);
+  C.ctr = off;
+  off += 256;
+  C.gu_flag = off;
+  off += align256(ffn / 64 * 4);
+  for (int t = 0; t < CH_TYPES; ++t) {
+    C.plan[t].units_off = off;
+    off += align256(static_cast<int64_t>(C.plan[t].units.size()) * 16);
+    C.plan[t].offs_off = off;
+    off += align256(static_cast<int64_t>(C.plan[t].offs.size()) * 4);
+  }
+  C.bytes = off;
+  return C;
+}
+
+bool chain_shapes_ok(const pl_stage_config& c) {
+  const int64_t qkv_dim = static_cast<int64_t>(c.Hq + 2 * c.Hkv) * c.hd;
+  return c.hd == 128 && c.d % 256 == 0 && (2 * static_cast<int64_t>(c.ffn)) % 256 == 0 && c.ffn % 64 == 0 &&
+         qkv_dim % 256 == 0 && (static_cast<int64_t>(c.Hq) * c.hd) % 64 == 0 && c.d <= 16384;
+}
+
+int device_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  return n;
+}
 
 Layout stage_layout(const pl_stage_config& c) {
   const int64_t T = c.max_tokens, R = c.max_reqs;
@@ -62,6 +147,8 @@ Layout stage_layout(const pl_stage_config& c) {
   off += align256(gws);
   L.attn_ws = off;
   off += align256(attn_decode_workspace_bytes(static_cast<int>(R), c.Hq, c.max_ctx, c.hd));
+  L.chain = off;
+  if (chain_shapes_ok(c)) off += align256(chain_layout(c, device_sms()).bytes);
   L.total = off;
   return L;
 }
@@ -70,7 +157,7 @@ Layout stage_layout(const pl_stage_config& c) {
 
 struct ProbeRec {
   cudaEvent_t ev[7];
-  int phase, T;
+  int phase, T, kind;  // kind 0: per-projection kernels, 1: attention + chain kernel
 };
 
 struct Stage {
@@ -83,6 +170,98 @@ struct Stage {
   size_t probe_used = 0;
   // weights repacked into pre-swizzled 16 KB tiles (pl_stage_pack_weights)
   bool pk_qkv = false, pk_o = false, pk_gu = false, pk_down = false, pk_lm = false;
+  // persistent decode-layer kernels
+  bool chain_ok = false;
+  ChainLayout CL;
+  unsigned long long ch_exp[4] = {0, 0, 0, 0};  // counter values after the last chain launch
+  int ch_seq = 0;
+
+  int init_chain() {
+    chain_ok = false;
+    if (!chain_shapes_ok(cfg)) return PL_OK;
+    CL = chain_layout(cfg, device_sms());
+    if (CL.bytes == 0) return PL_OK;
+    for (int t = 0; t < CH_TYPES; ++t) {
+      const ChainPlan& P = CL.plan[t];
+      cudaError_t e = cudaMemcpy(ws + L.chain + P.units_off, P.units.data(), P.units.size() * sizeof(int4),
+                                 cudaMemcpyHostToDevice);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(ws + L.chain + P.offs_off, P.offs.data(), P.offs.size() * sizeof(int),
+                       cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return set_cuda_error(e, "chain unit tables");
+    }
+    return PL_OK;
+  }
+
+  bool use_chain(int T) const {
+    static const bool on = [] { const char* v = getenv("PL_CHAIN"); return !(v && v[0] == '0'); }();
+    return on && CL.bytes > 0 && pk_qkv && pk_o && pk_gu && pk_down && T <= CL.Tp_max && T <= 256;
+  }
+
+  // one chain launch of type `t` for layer l (CH_QKV_ONLY: layer l's qkv; CH_FULL: layer
+  // l's o, gate_up, down and layer l+1's qkv; CH_LAST: layer l's o, gate_up, down)
+  int launch_chain(int t, int l, int T, const int32_t* pos, const int32_t* slot, __nv_bfloat16* hid,
+                   cudaStream_t st) {
+    const pl_stage_config& c = cfg;
+    const ChainPlan& P = CL.plan[t];
+    const pl_layer_weights& w = layers[l];
+    const pl_layer_weights& wq = (t == CH_FULL) ? layers[l + 1] : w;
+    uint8_t* base = ws + L.chain;
+    ChainLaunch k;
+    k.T = T;
+    k.Tp = chain_tp(T);
+    k.njobs = P.njobs;
+    k.d = c.d;
+    k.ffn = c.ffn;
+    k.attn_dim = c.Hq * c.hd;
+    k.grid = CL.grid;
+    const void* wts[4] = {w.w_o, w.w_gate_up, w.w_down, wq.w_qkv};
+    for (int j = 0; j < P.njobs; ++j) {
+      const int kd = P.kind[j];
+      k.kind[j] = kd;
+      k.N[j] = P.N[j];
+      k.K[j] = P.K[j];
+      k.splits[j] = P.splits[j];
+      k.w[j] = wts[kd];
+      k.partial[j] = reinterpret_cast<float*>(base + CL.partial[kd]);
+      k.arrive[j] = reinterpret_cast<int*>(base + CL.arrive[kd]);
+    }
+    k.units = reinterpret_cast<const int4*>(base + P.units_off);
+    k.unit_off = reinterpret_cast<const int*>(base + P.offs_off);
+    k.o_attn = buf(L.o);
+    k.h = hid;
+    k.a = buf(L.a);
+    k.m = buf(L.m);
+    k.q_out = buf(L.qkv);
+    k.ld_q = static_cast<int64_t>(c.Hq + 2 * c.Hkv) * c.hd;
+    k.ss = reinterpret_cast<float*>(base + CL.ss);
+    k.has_norm[0] = t != CH_QKV_ONLY;
+    k.has_norm[1] = t == CH_FULL;
+    k.norm_w[0] = static_cast<const __nv_bfloat16*>(w.mlp_norm);
+    k.norm_w[1] = t == CH_FULL ? static_cast<const __nv_bfloat16*>(wq.attn_norm) : nullptr;
+    k.eps = c.eps;
+    k.bias = static_cast<const __nv_bfloat16*>(wq.b_qkv);
+    k.pos = pos;
+    k.slot = slot;
+    k.cos_sin = static_cast<const __nv_bfloat16*>(c.cos_sin);
+    k.max_pos = c.max_pos;
+    k.k_cache = static_cast<__nv_bfloat16*>(wq.k_cache);
+    k.v_cache = static_cast<__nv_bfloat16*>(wq.v_cache);
+    k.block_size = c.block_size;
+    k.Hq = c.Hq;
+    k.Hkv = c.Hkv;
+    k.ctr = reinterpret_cast<unsigned long long*>(base + CL.ctr);
+    k.gu_flag = reinterpret_cast<int*>(base + CL.gu_flag);
+    const bool has_o = t != CH_QKV_ONLY;
+    unsigned long long tgt[4] = {ch_exp[0] + (has_o ? c.d / 128 : 0), ch_exp[1] + (k.has_norm[0] ? CL.grid : 0),
+                                 ch_exp[2] + (has_o ? c.d / 128 : 0), ch_exp[3] + (k.has_norm[1] ? CL.grid : 0)};
+    for (int i = 0; i < 4; ++i) k.tgt[i] = tgt[i];
+    k.seq = ++ch_seq;
+    const int rc = chain_launch(k, st);
+    if (rc) return rc;
+    for (int i = 0; i < 4; ++i) ch_exp[i] = tgt[i];
+    return PL_OK;
+  }
 
   int pack(cudaStream_t st) {
     const pl_stage_config& c = cfg;
@@ -130,7 +309,7 @@ struct Stage {
 
   __nv_bfloat16* buf(int64_t off) const { return reinterpret_cast<__nv_bfloat16*>(ws + off); }
 
-  cudaEvent_t* next_probe(int phase, int T) {
+  cudaEvent_t* next_probe(int phase, int T, int kind = 0) {
     if (probe_used == probes.size()) {
       if (probes.size() >= 65536) return nullptr;
       ProbeRec r{};
@@ -141,6 +320,7 @@ struct Stage {
     ProbeRec& r = probes[probe_used++];
     r.phase = phase;
     r.T = T;
+    r.kind = kind;
     return r.ev;
   }
 
@@ -198,6 +378,30 @@ struct Stage {
       }
     }
 
+    if (decode && use_chain(T)) {
+      // persistent chain kernels: per layer one attention launch and one chain launch
+      for (int l = 0; l < c.num_layers; ++l) {
+        const pl_layer_weights& w = layers[l];
+        cudaEvent_t* ev = (l == probe_layer) ? next_probe(mb.phase, T, 1) : nullptr;
+        if (l == 0) {
+          if ((rc = rmsnorm_launch(hid, d, nullptr, static_cast<const __nv_bfloat16*>(w.attn_norm), c.eps, T,
+                                   c.d, a, d, st)))
+            return rc;
+          if ((rc = launch_chain(CH_QKV_ONLY, 0, T, pos, slot, hid, st))) return rc;
+        }
+        if (ev) cudaEventRecord(ev[0], st);
+        rc = attn_decode_launch(qkv, qkv_dim, static_cast<const __nv_bfloat16*>(w.k_cache),
+                                static_cast<const __nv_bfloat16*>(w.v_cache), c.num_blocks, c.block_size, bt,
+                                c.max_blocks_per_req, ctx, R, mb.max_ctx, c.Hq, c.Hkv, c.hd, scale, o, attn_dim,
+                                ws + L.attn_ws, L.chain - L.attn_ws, st);
+        if (rc) return rc;
+        if (ev) cudaEventRecord(ev[1], st);
+        if ((rc = launch_chain(l + 1 < c.num_layers ? CH_FULL : CH_LAST, l, T, pos, slot, hid, st))) return rc;
+        if (ev) cudaEventRecord(ev[2], st);
+      }
+      return finish_last(mb, hid, last_idx, R, gws, gws_bytes, st);
+    }
+
     // Decode-path fusions (split-K reductions double as epilogues): QKV reduce + RoPE +
     // KV append, and residual reduce + the next RMSNorm.  `a_ready` tracks whether the
     // previous fused reduction already produced this layer's normalized input.
@@ -245,7 +449,7 @@ struct Stage {
                                 static_cast<const __nv_bfloat16*>(w.v_cache), c.num_blocks,
                                 c.block_size, bt,
                                 c.max_blocks_per_req, ctx, Rd, mb.max_ctx, c.Hq, c.Hkv, c.hd, scale, o,
-                                attn_dim, ws + L.attn_ws, L.total - L.attn_ws, st);
+                                attn_dim, ws + L.attn_ws, L.chain - L.attn_ws, st);
         if (rc) return rc;
       }
       if (Rp > 0) {  // causal attention over the prompt rows (cu_seqlens are absolute rows)
@@ -291,6 +495,15 @@ struct Stage {
       mark(6);
     }
 
+    return finish_last(mb, hid, last_idx, R, gws, gws_bytes, st);
+  }
+
+  // last stage: final norm of each request's newest row, lm_head + argmax (engine.py:409)
+  int finish_last(const pl_microbatch& mb, __nv_bfloat16* hid, const int32_t* last_idx, int R, void* gws,
+                  int64_t gws_bytes, cudaStream_t st) {
+    const pl_stage_config& c = cfg;
+    const int64_t d = c.d;
+    int rc;
     if (c.is_last) {
       if (!mb.out_ids) return set_error(PL_ERR_CONFIG, "stage_forward: last stage needs out_ids");
       __nv_bfloat16* hn = buf(L.hn);
@@ -342,6 +555,11 @@ int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* laye
   s->layers.assign(layers, layers + cfg->num_layers);
   s->ws = static_cast<uint8_t*>(workspace);
   s->L = L;
+  const int rc = s->init_chain();
+  if (rc) {
+    delete s;
+    return rc;
+  }
   *handle = s;
   return PL_OK;
 }
@@ -367,16 +585,19 @@ int32_t pl_stage_destroy(void* handle) {
 
 // Timing probe: CUDA events around each kernel group of one layer, recorded on
 // the launch stream (bench.py reads kernel durations live, not under ncu).
+// layer >= 0 starts a new pass (records cleared); layer < 0 stops recording.
 int32_t pl_stage_probe(void* handle, int32_t layer) {
   Stage* s = static_cast<Stage*>(handle);
   if (!s) return set_error(PL_ERR_CONFIG, "stage_probe: null handle");
   s->probe_layer = layer;
-  s->probe_used = 0;
+  if (layer >= 0) s->probe_used = 0;  // a new pass; layer < 0 stops and keeps the records
   return PL_OK;
 }
 
-// out_ms[i*5 + {0..4}] = {qkv gemm, rope+attention, o gemm, gate_up gemm, down gemm};
-// out_meta[i*2 + {0,1}] = {phase, T}.  Requires the stream to be synchronized.
+// Per recorded forward: out_meta[i*3 + {0,1,2}] = {phase, T, kind}; kind 0 (per-projection
+// kernels): out_ms[i*5 + {0..4}] = {qkv gemm, rope+attention, o gemm, gate_up gemm, down gemm};
+// kind 1 (persistent chain): out_ms[i*5 + {0,1}] = {decode attention, chain kernel}, rest 0.
+// Requires the stream to be synchronized.
 int32_t pl_stage_probe_read(void* handle, float* out_ms, int32_t* out_meta, int32_t cap, int32_t* n) {
   Stage* s = static_cast<Stage*>(handle);
   if (!s || !n) return set_error(PL_ERR_CONFIG, "stage_probe_read: null argument");
@@ -384,14 +605,18 @@ int32_t pl_stage_probe_read(void* handle, float* out_ms, int32_t* out_meta, int3
   for (int i = 0; i < cnt; ++i) {
     const ProbeRec& r = s->probes[i];
     const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 5}, {5, 6}};
+    const int npairs = r.kind == 1 ? 2 : 5;
     for (int k = 0; k < 5; ++k) {
       float ms = 0.f;
-      cudaError_t e = cudaEventElapsedTime(&ms, r.ev[pairs[k][0]], r.ev[pairs[k][1]]);
-      if (e != cudaSuccess) return set_cuda_error(e, "probe elapsed time");
+      if (k < npairs) {
+        cudaError_t e = cudaEventElapsedTime(&ms, r.ev[pairs[k][0]], r.ev[pairs[k][1]]);
+        if (e != cudaSuccess) return set_cuda_error(e, "probe elapsed time");
+      }
       out_ms[i * 5 + k] = ms;
     }
-    out_meta[i * 2] = r.phase;
-    out_meta[i * 2 + 1] = r.T;
+    out_meta[i * 3] = r.phase;
+    out_meta[i * 3 + 1] = r.T;
+    out_meta[i * 3 + 2] = r.kind;
   }
   *n = cnt;
   s->probe_used = 0;

@@ -80,6 +80,27 @@ class B200Stats:
         return nearest_rank(sorted(ts[0] for ts in self.token_times_s.values()), 50)
 
 
+def schedule_key(res) -> dict:
+    """Everything the reference scheduler decides in a RunResult (engine.py:108-127): event
+    log, link log (chunk boundaries and times), controller decisions, busy intervals,
+    token emissions and request lifecycles.  Two runs made the same schedule iff their
+    keys are equal."""
+    return {
+        "events": [(e.time_ns, int(e.kind), e.subject, e.stage) for e in res.events],
+        "links": [(e.time_ns, e.link, e.payload_id, e.chunk_index, e.size_bytes, e.phase_class.value,
+                   e.event) for e in res.link_events],
+        "decisions": [(i, d.n_microbatches, d.token_budget_per_microbatch, d.predicted_bubble_fraction)
+                      for i, d in res.decisions],
+        "busy": res.stage_busy_ns,
+        "emissions": res.token_emissions,
+        "first": sorted(res.first_compute_ns.items()),
+        "end": res.end_ns,
+        "done": res.all_finished,
+        "reqs": [(r.id, r.state.value, r.tokens_emitted, r.first_token_time, r.finish_time,
+                  r.arrival_time) for r in res.requests],
+    }
+
+
 def create_link_comms(placement: Placement) -> dict:
     """One 2-rank NCCL communicator per directed hop whose stages sit on different ranks.
     Unique ids travel over the default torch.distributed group (rendezvous only)."""

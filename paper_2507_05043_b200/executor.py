@@ -185,18 +185,74 @@ class StageExecutor:
         if rc:
             N.check(rc, "pl_stage_forward")
 
+    # --------------------------------------------------- direct requests
+    def greedy(self, prompts: list, n_steps: int, slot: int = 0):
+        """Greedy generation for explicit requests without the scheduler (whole model in
+        this stage: first and last): one prefill micro-batch of every prompt, then
+        n_steps - 1 decode micro-batches, each fed this stage's own argmax ids.  Returns
+        (ids [R, n_steps] int64, hn [n_steps, R, d] bf16 on the host), hn = the final
+        RMSNorm of each request's newest row -- what the lm_head / argmax read."""
+        if not (self.is_first and self.is_last):
+            raise ValueError("greedy() needs a stage holding the whole model")
+        lens = [len(p) for p in prompts]
+        R, T = len(lens), sum(lens)
+        if T > self.max_tokens or R > self.max_reqs or max(lens) + n_steps > self.max_ctx:
+            raise ValueError("requests exceed the stage's capacity")
+        mb_ = self.max_blocks
+        need = [-(-(n + n_steps) // BLOCK_SIZE) for n in lens]
+        if sum(need) > self.num_blocks:
+            raise ValueError("paged KV cache too small")
+        rows = np.zeros((R, mb_), dtype=np.int32)
+        b = 0
+        for r, k in enumerate(need):
+            rows[r, :k] = np.arange(b, b + k)
+            b += k
+        cu = np.concatenate([[0], np.cumsum(lens)])
+        pos = np.concatenate([np.arange(n) for n in lens])
+        req_of = np.repeat(np.arange(R), lens)
+        slots = rows[req_of, pos // BLOCK_SIZE] * BLOCK_SIZE + pos % BLOCK_SIZE
+        last_token = torch.zeros(R, dtype=torch.int64, device=self.device)
+        ids_out, hn_out = [], []
+        with torch.cuda.device(self.device):
+            for step in range(n_steps):
+                if step == 0:
+                    meta = build_meta(T, R, mb_, pos, slots, req_of, cu, lens, cu[1:] - 1, rows)
+                    ids = np.concatenate([np.asarray(p, dtype=np.int64) for p in prompts])
+                    self.ids_dev[:T].copy_(torch.from_numpy(ids))
+                    last = torch.tensor(cu[1:] - 1, dtype=torch.int32, device=self.device)
+                else:
+                    p = np.array([lens[r] + step - 1 for r in range(R)])
+                    ds = rows[np.arange(R), p // BLOCK_SIZE] * BLOCK_SIZE + p % BLOCK_SIZE
+                    meta = build_meta(R, R, mb_, p, ds, np.arange(R), np.arange(R + 1), p + 1,
+                                      np.arange(R), rows)
+                    last = torch.arange(R, dtype=torch.int32, device=self.device)
+                self.meta_dev[: meta.size].copy_(torch.from_numpy(meta))
+                torch.cuda.synchronize(self.device)
+                if step == 0:
+                    self.forward(slot, T, R, False, max(lens), max(lens))
+                else:
+                    self.forward(slot, R, R, True, 1, max(lens) + step, last_token=last_token)
+                self.stream.synchronize()
+                out = self.out_ids[slot][:R].clone()
+                last_token.copy_(out)
+                hn = ops.rmsnorm(self.hidden[slot], self.final_norm, self.spec.eps, row_idx=last)
+                ids_out.append(out.cpu())
+                hn_out.append(hn.cpu())
+        return torch.stack(ids_out, 1).numpy(), torch.stack(hn_out)
+
     # ------------------------------------------------------------- probe
     def probe(self, layer: int) -> None:
         N.call("pl_stage_probe", self.handle, layer)
 
     def probe_read(self, cap: int = 65536) -> tuple[np.ndarray, np.ndarray]:
+        """(ms [n, 5], meta [n, 3] = (phase, T, kind)); see pl_stage_probe_read."""
         ms = np.zeros(cap * 5, dtype=np.float32)
-        meta = np.zeros(cap * 2, dtype=np.int32)
+        meta = np.zeros(cap * 3, dtype=np.int32)
         n = C.c_int32()
         N.call("pl_stage_probe_read", self.handle, ms.ctypes.data_as(C.POINTER(C.c_float)),
                meta.ctypes.data_as(C.POINTER(C.c_int32)), cap, C.byref(n))
         k = n.value
-        return ms[: k * 5].reshape(k, 5), meta[: k * 2].reshape(k, 2)
+        return ms[: k * 5].reshape(k, 5), meta[: k * 3].reshape(k, 3)
 
     def weight_bytes(self) -> int:
         n = sum(t.numel() * t.element_size() for L in self.layers for k, t in L.items()

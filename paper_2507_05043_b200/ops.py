@@ -157,13 +157,19 @@ def attn_prefill(qkv: torch.Tensor, cu_seqlens: torch.Tensor, max_seqlen: int, H
 
 def attn_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
                 block_table: torch.Tensor, ctx_len: torch.Tensor, max_ctx: int, Hq: int, Hkv: int,
-                hd: int, out: torch.Tensor | None = None, block_size: int = 64) -> torch.Tensor:
-    """q: [R, >= Hq*hd] rows (e.g. the q part of the fused qkv buffer)."""
+                hd: int, out: torch.Tensor | None = None, block_size: int = 64,
+                ws: torch.Tensor | None = None) -> torch.Tensor:
+    """q: [R, >= Hq*hd] rows (e.g. the q part of the fused qkv buffer).  `ws`: a zero-
+    initialised uint8 workspace reused across calls (sized for the largest call with
+    pl_attn_decode_workspace_bytes); default a fresh one per call."""
     _need_cuda(q, k_cache, v_cache, block_table, ctx_len)
     R = ctx_len.numel()
     out = out if out is not None else torch.empty(R, Hq * hd, dtype=BF16, device=q.device)
-    ws_bytes = N.lib().pl_attn_decode_workspace_bytes(R, Hq, max_ctx, hd)
-    ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)  # split counters start at 0
+    if ws is None:
+        ws_bytes = N.lib().pl_attn_decode_workspace_bytes(R, Hq, max_ctx, hd)
+        ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)  # split counters start at 0
+    else:
+        ws_bytes = ws.numel()
     N.call("pl_attn_decode", _ptr(q), q.stride(0), _ptr(k_cache), _ptr(v_cache), k_cache.shape[0],
            block_size,
            _ptr(block_table), block_table.shape[1], _ptr(ctx_len), R, max_ctx, Hq, Hkv, hd,

@@ -35,20 +35,9 @@ from paper_2507_05043_b200.spec import TINY, LLAMA3_8B
 
 
 def result_key(res):
-    return {
-        "events": [(e.time_ns, int(e.kind), e.subject, e.stage) for e in res.events],
-        "links": [(e.time_ns, e.link, e.payload_id, e.chunk_index, e.size_bytes, e.phase_class.value,
-                   e.event) for e in res.link_events],
-        "decisions": [(i, d.n_microbatches, d.token_budget_per_microbatch, d.predicted_bubble_fraction)
-                      for i, d in res.decisions],
-        "busy": res.stage_busy_ns,
-        "emissions": res.token_emissions,
-        "first": sorted(res.first_compute_ns.items()),
-        "end": res.end_ns,
-        "done": res.all_finished,
-        "reqs": [(r.id, r.state.value, r.tokens_emitted, r.first_token_time, r.finish_time,
-                  r.arrival_time) for r in res.requests],
-    }
+    from paper_2507_05043_b200.engine import schedule_key
+
+    return schedule_key(res)
 
 
 def assert_same(cfg, cluster, profiles, trace, horizon=None):

@@ -87,8 +87,7 @@ def test_rmsnorm_row_gather(ops):
 GEMM_SHAPES = [  # (T, N, K)
     (1, 512, 256), (5, 640, 256), (16, 6144, 4096), (17, 384, 768), (64, 4096, 4096),
     (100, 1024, 512), (256, 512, 256), (300, 512, 256), (1000, 1536, 256), (2048, 768, 1024),
-    # 148 < N/128 < 296 weight tiles: data-parallel + stream-K hybrid (fix-up of shared tiles,
-    # up to ~12 pieces per tile at K=1024)
+    # more weight tiles than SMs (148 < N/128 < 296): two waves of persistent CTAs
     (64, 28672, 4096), (7, 20480, 1024), (130, 19200, 512),
 ]
 
@@ -225,6 +224,46 @@ def test_attn_decode_paged(ops, ctx, Hq, Hkv):
     close_bf16(out, torch.cat(refs), rel=2.0 ** -6, atol=4e-3)
 
 
+def _paged_case(ctx, Hq, Hkv, seed, hd=128, bs=64):
+    R = len(ctx)
+    g = torch.Generator().manual_seed(seed)
+    max_blocks = max((c + bs - 1) // bs for c in ctx)
+    num_blocks = R * max_blocks + 3
+    perm = torch.randperm(num_blocks, generator=g)
+    bt = perm[: R * max_blocks].reshape(R, max_blocks).to(torch.int32)
+    kc = torch.randn(num_blocks, Hkv, bs, hd, generator=g).to(BF16)
+    vc = torch.randn(num_blocks, Hkv, bs, hd, generator=g).to(BF16)
+    q = torch.randn(R, Hq * hd, generator=g).to(BF16)
+    refs = []
+    for r in range(R):
+        pages = bt[r, : (ctx[r] + bs - 1) // bs].long()
+        k = kc[pages].permute(0, 2, 1, 3).reshape(-1, Hkv, hd)[: ctx[r]]
+        v = vc[pages].permute(0, 2, 1, 3).reshape(-1, Hkv, hd)[: ctx[r]]
+        refs.append(OD.attention_ref(q[r].reshape(1, Hq, hd), k, v, None))
+    return q, kc, vc, bt, torch.tensor(ctx, dtype=torch.int32), torch.cat(refs)
+
+
+def test_split_decode_shared_workspace_across_shapes(ops):
+    """One workspace (sized for the largest launch, as a stage sizes it) serves split
+    launches of different R and context: R=1 at a long context, then R=16, then R=1
+    again.  The arrival counters sit at fixed addresses at the end of the workspace, so
+    no launch's partials land on another launch's counters (attention.cu)."""
+    Hq, Hkv, hd = 32, 8, 128
+    from paper_2507_05043_b200 import _native as NN
+
+    ws_bytes = NN.lib().pl_attn_decode_workspace_bytes(16, Hq, 4096, hd)
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev())
+    cases = [[4000], [1100 + 37 * i for i in range(16)], [3000], [1500] * 16]
+    for i, ctx in enumerate(cases):
+        q, kc, vc, bt, ctx_t, ref = _paged_case(ctx, Hq, Hkv, seed=100 + i)
+        out = ops.attn_decode(q.to(dev()), kc.to(dev()), vc.to(dev()), bt.to(dev()), ctx_t.to(dev()),
+                              max(ctx), Hq, Hkv, hd, ws=ws).cpu()
+        close_bf16(out, ref, rel=2.0 ** -6, atol=4e-3)
+    # every counter is back to zero
+    tail = ws[ws_bytes - 16 * Hkv * 4:].view(torch.int32)
+    assert int(tail.abs().sum()) == 0
+
+
 _PAIR_SCRIPT = r"""
 import sys, torch
 sys.path.insert(0, {root!r})
@@ -325,3 +364,41 @@ def test_gemm_packed_bit_identical(ops, T, N, K, epi):
     if a.dtype == BF16:
         a, c = a.view(torch.int16), c.view(torch.int16)
     assert torch.equal(a.cpu(), c.cpu())
+
+
+_PPS_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+from test_kernels_gpu import _paged_case
+from paper_2507_05043_b200 import ops
+d = torch.device("cuda:0")
+outs = []
+for i, (ctx, Hq, Hkv) in enumerate({cases!r}):
+    q, kc, vc, bt, ctx_t, ref = _paged_case(ctx, Hq, Hkv, seed=7 + i)
+    out = ops.attn_decode(q.to(d), kc.to(d), vc.to(d), bt.to(d), ctx_t.to(d), max(ctx), Hq, Hkv, 128).cpu()
+    outs.append((out, ref))
+torch.save(outs, sys.argv[1])
+"""
+
+
+@pytest.mark.parametrize("pps", ["1", "3", "32"])
+def test_attn_decode_pages_per_split_override(tmp_path, pps):
+    """PL_ATTN_PPS (pages per decode-attention split; default 16) at its extremes: one page
+    per split (up to 47 splits merged by the last arriver), an odd split, and 32 (every
+    block-table entry of a split travels in one warp-wide load)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    cases = [([3000], 32, 8), ([65, 640, 1300, 2047], 8, 2), ([129] * 8, 64, 8)]
+    script = tmp_path / "pps.py"
+    script.write_text(_PPS_SCRIPT.format(root=str(root), tests=str(root / "tests"), cases=cases))
+    out = tmp_path / "pps.pt"
+    p = subprocess.run([sys.executable, str(script), str(out)], env=dict(os.environ, PL_ATTN_PPS=pps),
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-3000:]
+    for got, ref in torch.load(out):
+        close_bf16(got, ref, rel=2.0 ** -6, atol=4e-3)

@@ -6,10 +6,14 @@
   ("peaked") init, on config 1 (tiny, S=2) and on a truncated Llama-3-8B-shape
   model; under the standard init every GPU token lies inside the oracle's tie
   band (teacher forced) and >= 90% match exactly;
-* logits: the GPU stack's fp32 logits are within |dlogit| <= 0.02 + 2% of the
-  logit range of the oracle's (bf16 rounding points identical, fp32 summation
-  order differs).
+* logits: the GPU stack's fp32 logits are within |dlogit| <= tol of the oracle's
+  (bf16 rounding points identical, fp32 summation order differs); tol = 4x the
+  drift between two CPU oracles that differ only in summation order
+  (tests/golden/logit_tolerance.json, oracle/calibrate_tolerance.py).
 """
+
+import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -25,6 +29,14 @@ from paper_2507_05043_b200.spec import prompt_tokens
 from test_driver_parity import result_key
 
 pytestmark = pytest.mark.gpu
+
+_TOL = json.loads((Path(__file__).resolve().parent / "golden" / "logit_tolerance.json").read_text())
+
+
+def tol_of(spec) -> float:
+    """Calibrated logits tolerance of a test model (see the module docstring)."""
+    key = "tiny" if spec.d == 256 else "tiny-d1024" if spec.d == 1024 else None
+    return _TOL[key]["tol"]
 
 
 def synth_profiles(plan, per_token=1e-6, overhead=2e-5):
@@ -86,8 +98,7 @@ def test_config1_standard_init_tie_band():
         logits = model.teacher_forced(p, gen)          # [out_len, V]
         best = logits.max(-1).values
         chosen = logits.gather(1, gen[:, None]).squeeze(1)
-        span = (logits.max() - logits.min()).item()
-        tol = 0.02 + 0.02 * span
+        tol = tol_of(spec)
         gap = (best - chosen).max().item()
         assert (chosen >= best - tol).all(), f"request {r.id}: token {gap:.4f} below the max (band {tol:.4f})"
         exact += (logits.argmax(-1) == gen).sum().item()
@@ -152,30 +163,34 @@ def test_stage_logits_within_tolerance():
     hidden = exe.hidden[0][:T].clone()
     last = torch.tensor(cu[1:] - 1, dtype=torch.int32, device=hidden.device)
     hn = ops.rmsnorm(hidden, exe.final_norm, spec.eps, row_idx=last)
-    logits = ops.gemm(hn, exe.lm_head).float().cpu()   # bf16 logits (store epilogue)
     ids_gpu = exe.out_ids[0][:R].cpu()
 
     model = OD.OracleModel(OD.OracleSpec.from_spec(spec), seed=0, max_pos=256)
     toks = [torch.from_numpy(ids[cu[i]:cu[i + 1]]) for i in range(R)]
     ref = model.forward(toks, [torch.arange(n) for n in lens], model.new_cache(R))
-    span = (ref.max() - ref.min()).item()
+    # GPU logits from the GPU's final-normed rows in fp32 (the lm_head GEMM's bf16 store
+    # epilogue would add a rounding the argmax path never sees)
+    logits = OD.linear_acc(hn.cpu(), exe.lm_head.cpu())
     err = (logits - ref).abs().max().item()
-    assert err <= 0.02 + 0.02 * span, f"max |dlogit| {err:.4f} (span {span:.3f})"
+    tol = tol_of(spec)
+    assert err <= tol, f"max |dlogit| {err:.4f} (tol {tol:.4f})"
     top2 = ref.topk(2, -1).values
-    clear = (top2[:, 0] - top2[:, 1]) > 0.02 + 0.02 * span
+    clear = (top2[:, 0] - top2[:, 1]) > tol
     assert torch.equal(ids_gpu[clear], ref.argmax(-1)[clear])
     exe.close()
 
 
+@pytest.mark.parametrize("pack", [False, True], ids=["per-projection", "chain"])
 @pytest.mark.parametrize("spec", [TINY, TINY.with_(Hq=8, Hkv=2, d=1024, ffn=1536, vocab=2048)])
-def test_decode_logits_within_tolerance(spec):
-    """Prefill then teacher-forced decode steps through the paged decode path
-    (split-K GEMMs at small T, tensor-core decode attention): logits vs the oracle."""
+def test_decode_logits_within_tolerance(spec, pack):
+    """Prefill then teacher-forced decode steps through the paged decode path: logits vs
+    the oracle.  Row-major weights run one GEMM per projection (split-K + reduce kernels);
+    packed weights run the persistent decode-layer chain kernel (chain.cu)."""
     lens = [100, 37, 64]
     R, T = len(lens), sum(lens)
     steps = 5
     exe = StageExecutor(spec, 0, (0, spec.num_layers), True, True, torch.device("cuda", 0), seed=0,
-                        pack_weights=False,
+                        pack_weights=pack,
                         max_tokens=T, max_reqs=R, max_ctx=256, num_blocks=3 * 4, n_slots=1)
     mb_ = exe.max_blocks
     rows = np.arange(R * mb_, dtype=np.int32).reshape(R, -1)
@@ -208,12 +223,12 @@ def test_decode_logits_within_tolerance(spec):
         exe.forward(0, R, R, True, 1, int(p.max()) + 1, last_token=last_token)
         exe.stream.synchronize()
         hn = ops.rmsnorm(exe.hidden[0][:R].clone(), exe.final_norm, spec.eps)
-        got = ops.gemm(hn, exe.lm_head).float().cpu()
+        got = OD.linear_acc(hn.cpu(), model.lm_head)
         ref = model.forward([nxt[i:i + 1] for i in range(R)], [torch.tensor([p[i]]) for i in range(R)], caches)
-        span = (ref.max() - ref.min()).item()
         err = (got - ref).abs().max().item()
-        worst = max(worst, err / (0.02 + 0.02 * span))
-        assert err <= 0.02 + 0.02 * span, f"step {k}: max |dlogit| {err:.4f} (span {span:.3f})"
+        tol = tol_of(spec)
+        worst = max(worst, err / tol)
+        assert err <= tol, f"step {k}: max |dlogit| {err:.4f} (tol {tol:.4f})"
     exe.close()
 
 
@@ -379,3 +394,43 @@ def test_realized_link_log_matches_virtual_chunks():
         assert sizes == virt_sizes
     assert any(e.chunk_index > 0 for e in real), "prefill payloads were not chunked"
     eng.close()
+
+
+def test_decode_rows_batch_invariant():
+    """A decode request's result never depends on the decode micro-batch it rides in:
+    every decode GEMM picks its split-K from the weight shape (N, K) only and the
+    attention splits from the request's own context, so request 0's hidden row and
+    greedy id are bit-identical at R = 1, 7, 64 and 200 (prefill micro-batches above 256
+    tokens use the token-row orientation instead -- same bf16 rounding points, a
+    different fp32 summation order -- so the claim is about decode)."""
+    spec = LLAMA3_8B.with_(num_layers=2)
+    R, L = 200, 24
+    exe = StageExecutor(spec, 0, (0, 2), True, True, torch.device("cuda", 0), seed=0,
+                        max_tokens=R * L, max_reqs=R, max_ctx=64, num_blocks=R, n_slots=1)
+    rows = np.arange(R, dtype=np.int32)[:, None]
+    lens = [L] * R
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    pos = np.concatenate([np.arange(n) for n in lens])
+    req_of = np.repeat(np.arange(R), lens)
+    slots = rows[req_of, 0] * 64 + pos
+    meta = build_meta(R * L, R, 1, pos, slots, req_of, cu, lens, cu[1:] - 1, rows)
+    ids = np.concatenate([prompt_tokens(0, i, L, spec.vocab) for i in range(R)])
+    exe.meta_dev[: meta.size].copy_(torch.from_numpy(meta))
+    exe.ids_dev[: R * L].copy_(torch.from_numpy(ids))
+    torch.cuda.synchronize()
+    exe.forward(0, R * L, R, False, L, L)
+    exe.stream.synchronize()
+    last = exe.out_ids[0][:R].clone()
+    outs = []
+    for n in (1, 7, 64, 200):
+        p = np.full(n, L)
+        meta = build_meta(n, n, 1, p, rows[:n, 0] * 64 + L, np.arange(n), np.arange(n + 1), p + 1,
+                          np.arange(n), rows[:n])
+        exe.meta_dev[: meta.size].copy_(torch.from_numpy(meta))
+        torch.cuda.synchronize()
+        exe.forward(0, n, n, True, 1, L + 1, last_token=last)
+        exe.stream.synchronize()
+        outs.append((exe.hidden[0][0].clone().view(torch.int16).cpu(), int(exe.out_ids[0][0])))
+    for h, t in outs[1:]:
+        assert torch.equal(h, outs[0][0]) and t == outs[0][1]
+    exe.close()
