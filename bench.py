@@ -161,8 +161,11 @@ def parity_check(spec, eng, trace, res, profiles, rank, world, full_logits: bool
     from paper_2507_05043_b200.spec import prompt_tokens
 
     exe = eng.gpu.exe[0]
-    R, steps = 4, 4
-    lens = [64 + 16 * r for r in range(R)]
+    steps = 4
+    R = min(4, exe.max_reqs)
+    lens = [max(2, min(64 + 16 * r, exe.max_ctx - steps)) for r in range(R)]
+    while sum(lens) > exe.max_tokens and max(lens) > 2:
+        lens = [max(2, n // 2) for n in lens]
     prompts = [prompt_tokens(0, 10_000 + r, n, spec.vocab) for r, n in enumerate(lens)]
     ids, hn = exe.greedy(prompts, steps)
     o = OD.OracleSpec.from_spec(spec)
@@ -325,40 +328,12 @@ def run_b200(args):
 
     hbm, tfl, peak_src = peaks()
     # ---- dominant kernel: gate_up GEMM of decode micro-batches (probe, CUDA events)
-    gu_ms, gu_T = [], []
-    qkv_ms, o_ms, down_ms, attn_ms = [], [], [], []
-    for exe in eng.gpu.exe.values():
-        ms, meta = exe.probe_read()
-        for row, (phase, T) in zip(ms, meta):
-            if phase == 1:
-                qkv_ms.append(row[0]); attn_ms.append(row[1]); o_ms.append(row[2])
-                gu_ms.append(row[3]); down_ms.append(row[4]); gu_T.append(T)
-    roof = None
-    if gu_ms:
-        avg_T = float(np.mean(gu_T))
-        w_bytes = 2 * spec.ffn * spec.d * 2
-        act_bytes = avg_T * spec.d * 2 + avg_T * spec.ffn * 2
-        alg = w_bytes + act_bytes
-        avg_s = float(np.mean(gu_ms)) / 1e3
-        achieved = alg / avg_s / 1e9
-        roof = {"kernel": "gemm_tc_kernel<SWAP> gate_up + SwiGLU epilogue (decode; no split-K at N=28672)",
-                "timing": "CUDA events around the kernel on the stage compute stream, layer 0 of every "
-                          "decode micro-batch, in a probe pass after the timed region (events between "
-                          "kernels disable PDL overlap for that layer: per-kernel times are conservative)",
-                "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": ncu_traffic("gate_up", int(round(avg_T))),
-                "algorithmic_bytes_per_launch": int(alg), "avg_launch_us": round(avg_s * 1e6, 2),
-                "avg_T": round(avg_T, 2), "launches_timed": len(gu_ms), "peak_source": peak_src,
-                "other_decode_kernels_avg_us": {
-                    "qkv_gemm": round(float(np.mean(qkv_ms)) * 1e3, 2),
-                    "rope+attention": round(float(np.mean(attn_ms)) * 1e3, 2),
-                    "o_gemm": round(float(np.mean(o_ms)) * 1e3, 2),
-                    "down_gemm": round(float(np.mean(down_ms)) * 1e3, 2)}}
+    roof = dominant_kernel_roofline(spec, eng, hbm, peak_src)
     roofs = [None] * world
     if world > 1:
         import torch.distributed as dist
         dist.all_gather_object(roofs, roof)
-        # report the stage whose gate_up runs slowest (the pipeline's binding stage)
+        # report the stage whose dominant kernel runs slowest (the pipeline's binding stage)
         cands = [r for r in roofs if r]
         roof = min(cands, key=lambda r: r["frac"]) if cands else None
 
@@ -408,6 +383,63 @@ def run_b200(args):
         }
     eng.close()
     return out
+
+
+def dominant_kernel_roofline(spec, eng, hbm, peak_src):
+    """Roofline of the dominant decode kernel from the probe pass (CUDA events on the
+    stage's compute stream around layer 0's kernels of every decode micro-batch).
+
+    Persistent chain path (default, chain.cu): the chain kernel of layer 0 streams the
+    o, gate_up and down projections of layer 0 and the qkv projection of layer 1:
+      algorithmic bytes = (d*attn + 2*ffn*d + d*ffn + qkv*d) * 2        (weights, once)
+                        + T * (attn + d + ffn + d) * 2                    (activations read)
+                        + T * (2*d + ffn + qkv) * 2                       (outputs written)
+    Per-projection path (PL_CHAIN=0): the gate_up GEMM, 2*ffn*d*2 + T*(d + ffn)*2."""
+    import numpy as np
+
+    d, ffn, attn, qkv = spec.d, spec.ffn, spec.attn_dim, spec.qkv_dim
+    chain_ms, chain_T, attn_ms = [], [], []
+    gu_ms, gu_T, other = [], [], {"qkv_gemm": [], "rope+attention": [], "o_gemm": [], "down_gemm": []}
+    for exe in eng.gpu.exe.values():
+        ms, meta = exe.probe_read()
+        for row, (phase, T, kind) in zip(ms, meta):
+            if phase != 1:
+                continue
+            if kind == 1 and exe.hi - exe.lo >= 2:
+                attn_ms.append(row[0]); chain_ms.append(row[1]); chain_T.append(T)
+            elif kind == 0:
+                other["qkv_gemm"].append(row[0]); other["rope+attention"].append(row[1])
+                other["o_gemm"].append(row[2]); gu_ms.append(row[3]); other["down_gemm"].append(row[4])
+                gu_T.append(T)
+    timing = ("CUDA events around the kernel on the stage compute stream, layer 0 of every decode "
+              "micro-batch, in a probe pass after the timed region (an event between two kernels "
+              "ends PDL overlap there: conservative)")
+    if chain_ms:
+        T = float(np.mean(chain_T))
+        w = (d * attn + 2 * ffn * d + d * ffn + qkv * d) * 2
+        act = T * (attn + d + ffn + d) * 2 + T * (2 * d + ffn + qkv) * 2
+        alg = w + act
+        avg_s = float(np.mean(chain_ms)) / 1e3
+        achieved = alg / avg_s / 1e9
+        return {"kernel": "chain_kernel (persistent decode layer: o + RMSNorm + gate_up/SwiGLU + down + "
+                          "RMSNorm + next qkv/RoPE/KV append, one launch)", "timing": timing,
+                "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": ncu_traffic("chain", int(round(T))),
+                "algorithmic_bytes_per_launch": int(alg), "avg_launch_us": round(avg_s * 1e6, 2),
+                "avg_T": round(T, 2), "launches_timed": len(chain_ms), "peak_source": peak_src,
+                "other_decode_kernels_avg_us": {"decode_attention": round(float(np.mean(attn_ms)) * 1e3, 2)}}
+    if gu_ms:
+        T = float(np.mean(gu_T))
+        alg = 2 * ffn * d * 2 + T * d * 2 + T * ffn * 2
+        avg_s = float(np.mean(gu_ms)) / 1e3
+        achieved = alg / avg_s / 1e9
+        return {"kernel": "gemm_tc_kernel<SWAP> gate_up + SwiGLU epilogue (decode; no split-K at N=28672)",
+                "timing": timing, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": ncu_traffic("gate_up", int(round(T))),
+                "algorithmic_bytes_per_launch": int(alg), "avg_launch_us": round(avg_s * 1e6, 2),
+                "avg_T": round(T, 2), "launches_timed": len(gu_ms), "peak_source": peak_src,
+                "other_decode_kernels_avg_us": {k: round(float(np.mean(v)) * 1e3, 2) for k, v in other.items()}}
+    return None
 
 
 def decode_path_roofline(spec, eng, res, hbm_gbs, tflops):

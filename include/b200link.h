@@ -216,6 +216,14 @@ PL_API int32_t pl_stage_destroy(void* handle);
  * rope+attention, o gemm, gate_up gemm, down gemm}; kind 1 (persistent decode
  * chain) = {decode attention, chain kernel, 0, 0, 0}.  Synchronize the stream first. */
 PL_API int32_t pl_stage_probe(void* handle, int32_t layer);
+/* Debug (PL_CHAIN_TRACE=k in the environment): per-unit globaltimer stamps of the
+ * stage's k-th persistent chain launch, [grid][64][4] u64 = {claim time mod 2^40 |
+ * claim index << 40, unit popped by the epilogue, accumulator ready, epilogue done}. */
+PL_API int32_t pl_stage_chain_trace(void* handle, uint64_t* out_host, int64_t n, int32_t* grid);
+/* Benchmark: `iters` launches of a persistent chain holding ONE projection of layer 0
+ * (kind 0 o, 1 gate_up, 2 down, 3 qkv) at T tokens, without dependencies or
+ * finalisation -- the chain kernel's weight stream alone (results are scratch). */
+PL_API int32_t pl_stage_chain_bench(void* handle, int32_t kind, int32_t T, int32_t iters, void* stream);
 PL_API int32_t pl_stage_probe_read(void* handle, float* out_ms_host, int32_t* out_meta_host, int32_t cap,
                             int32_t* n_host);
 

@@ -9,6 +9,7 @@ the reference's exception hierarchy (pipelink/errors.py:4-39).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -18,7 +19,7 @@ ConfigError = pipelink.ConfigError
 ProtocolError = pipelink.ProtocolError
 PipelinkError = pipelink.PipelinkError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libb200link.so"
+LIB_PATH = Path(os.environ.get("PL_LIB_PATH") or Path(__file__).resolve().parent / "_lib" / "libb200link.so")
 
 PL_OK, PL_ERR_CONFIG, PL_ERR_PROTOCOL, PL_ERR_CUDA = 0, 1, 2, 3
 EPI_NONE, EPI_BIAS, EPI_RESIDUAL, EPI_SWIGLU, EPI_ARGMAX = 0, 1, 2, 3, 4
@@ -99,6 +100,8 @@ _SIGS = {
     "pl_stage_pack_weights": (i32, [vp, vp]),
     "pl_stage_destroy": (i32, [vp]),
     "pl_stage_probe": (i32, [vp, i32]),
+    "pl_stage_chain_trace": (i32, [vp, vp, i64, C.POINTER(i32)]),
+    "pl_stage_chain_bench": (i32, [vp, i32, i32, i32, vp]),
     "pl_stage_probe_read": (i32, [vp, C.POINTER(f32), C.POINTER(i32), i32, C.POINTER(i32)]),
     "pl_nccl_version": (i32, []),
     "pl_nccl_unique_id": (i32, [C.POINTER(C.c_uint8), i32]),

@@ -21,8 +21,13 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-OBJ = PKG / "_build"
-LIB_DIR = PKG / "_lib"
+import os as _os
+
+# experiment builds (never the product): PL_BUILD_VARIANT=<name> + PL_NVCC_EXTRA="-D..." build
+# into _build_<name>/ and _lib_<name>/, loaded with PL_LIB_PATH=<that .so>
+_VARIANT = _os.environ.get("PL_BUILD_VARIANT", "")
+OBJ = PKG / ("_build" + (f"_{_VARIANT}" if _VARIANT else ""))
+LIB_DIR = PKG / ("_lib" + (f"_{_VARIANT}" if _VARIANT else ""))
 LIB = LIB_DIR / "libb200link.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -53,6 +58,7 @@ def _flags() -> list[str]:
         "--expt-relaxed-constexpr",
         f"-I{ROOT / 'include'}",
         f"-I{inc}",
+        *_os.environ.get("PL_NVCC_EXTRA", "").split(),
     ]
 
 

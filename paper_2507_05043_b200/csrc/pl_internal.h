@@ -148,14 +148,15 @@ struct ChainLaunch {
   int64_t N[4] = {0, 0, 0, 0}, K[4] = {0, 0, 0, 0};
   int splits[4] = {1, 1, 1, 1};
   const void* w[4] = {nullptr, nullptr, nullptr, nullptr};  // packed weights (pack_weight_launch)
-  float* partial[4] = {nullptr, nullptr, nullptr, nullptr};
-  int* arrive[4] = {nullptr, nullptr, nullptr, nullptr};
-  const int4* units = nullptr;
-  const int* unit_off = nullptr;
+  float* partial[4] = {nullptr, nullptr, nullptr, nullptr};  // split-K partials [splits][tiles][Tp][128]
+  const int4* units = nullptr;  // global claim order {job, tile, kb0, nkb} (device)
+  const int4* units_host = nullptr;  // the same list on the host
+  int n_units = 0;
   const __nv_bfloat16* o_attn = nullptr;
   __nv_bfloat16 *h = nullptr, *a = nullptr, *m = nullptr, *q_out = nullptr;
   int64_t ld_q = 0;
-  float* ss = nullptr;
+  float* part_ss = nullptr;  // [2][Tp][d / piece] finalisation sums of squares
+  int* row_parts = nullptr;  // [2][Tp] zero between launches
   const __nv_bfloat16* norm_w[2] = {nullptr, nullptr};
   int has_norm[2] = {0, 0};
   float eps = 0.f;
@@ -165,14 +166,17 @@ struct ChainLaunch {
   int max_pos = 0;
   __nv_bfloat16 *k_cache = nullptr, *v_cache = nullptr;
   int block_size = 0, Hq = 0, Hkv = 0;
-  unsigned long long* ctr = nullptr;
-  unsigned long long tgt[4] = {0, 0, 0, 0};
+  void* ctr = nullptr;  // this launch's counter set (CHAIN_CTR_BYTES, zero; two sets alternate)
   int* gu_flag = nullptr;
   int seq = 0;
+  unsigned long long* trace = nullptr;  // debug: [grid][64][4] globaltimer stamps, or null
+  int bench = 0;  // pl_stage_chain_bench: no dependencies, no finalisation (weight stream only)
 };
+constexpr int CHAIN_CTR_BYTES = 64;
 int chain_plan(const int* kinds, int njobs, const int64_t* N, const int64_t* K, int grid, int ring,
-               int* splits_out, std::vector<int4>& units, std::vector<int>& offs);
+               int* splits_out, std::vector<int4>& units);
 int chain_ring_kb(int BN);
+int chain_ctas_per_sm();
 int chain_launch(const ChainLaunch& c, cudaStream_t st);
 int chain_preload();
 

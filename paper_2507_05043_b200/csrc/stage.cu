@@ -16,6 +16,7 @@
 //   hidden = hidden + m . Wd^T                  tcgen05 GEMM, RESIDUAL epilogue
 // First stage: hidden = embed(ids).  Last stage: final norm of each request's
 // last row, lm_head GEMM with fused argmax -> int64 token ids (engine.py:409).
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -42,16 +43,15 @@ struct ChainPlan {
   int kind[4] = {0, 0, 0, 0};
   int64_t N[4] = {0, 0, 0, 0}, K[4] = {0, 0, 0, 0};
   int splits[4] = {1, 1, 1, 1};
-  std::vector<int4> units;
-  std::vector<int> offs;
-  int64_t units_off = 0, offs_off = 0;  // byte offsets inside the chain region
+  std::vector<int4> units;  // global claim order
+  int64_t units_off = 0;    // byte offset inside the chain region
 };
 
 struct ChainLayout {
   ChainPlan plan[CH_TYPES];
   int grid = 0, Tp_max = 0;
-  int64_t partial[4] = {0, 0, 0, 0}, arrive[4] = {0, 0, 0, 0};  // by ChainKind
-  int64_t ss = 0, ctr = 0, gu_flag = 0, bytes = 0;
+  int64_t partial[4] = {0, 0, 0, 0};  // by ChainKind
+  int64_t part_ss = 0, row_parts = 0, ctr = 0, gu_flag = 0, bytes = 0;
 };
 
 int chain_tp(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
@@ -77,28 +77,33 @@ ChainLayout chain_layout(const pl_stage_config& c, int grid) {
       P.N[j] = NN[P.kind[j]];
       P.K[j] = KK[P.kind[j]];
     }
-    chain_plan(P.kind, P.njobs, P.N, P.K, grid, ring, P.splits, P.units, P.offs);
+    chain_plan(P.kind, P.njobs, P.N, P.K, grid, ring, P.splits, P.units);
     for (int j = 0; j < P.njobs; ++j) max_split[P.kind[j]] = std::max(max_split[P.kind[j]], P.splits[j]);
+    if (getenv("PL_CHAIN_VERBOSE")) {
+      fprintf(stderr, "chain plan %d (grid %d):", t, grid);
+      for (int j = 0; j < P.njobs; ++j)
+        fprintf(stderr, " kind %d N %lld K %lld splits %d;", P.kind[j], (long long)P.N[j], (long long)P.K[j],
+                P.splits[j]);
+      fprintf(stderr, " %zu units\n", P.units.size());
+    }
   }
   int64_t off = 0;
   for (int k = 0; k < 4; ++k) {
     const int64_t tiles = NN[k] / 128;
-    C.partial[k] = off;
-    off += align256(max_split[k] > 1 ? max_split[k] * tiles * C.Tp_max * 128 * 4 : 0);
-    C.arrive[k] = off;
-    off += align256(tiles * 4);
+    C.partial[k] = off;  // every split-K projection writes partials (also at one split)
+    off += align256(k == CHAIN_GATE_UP ? 0 : max_split[k] * tiles * C.Tp_max * 128 * 4);
   }
-  C.ss = off;
-  off += align256(2 * (d / 128) * C.Tp_max * 4);
-  C.ctr = off;
-  off += 256;
+  C.part_ss = off;
+  off += align256(2 * C.Tp_max * (d / 256) * 4);  // pieces of >= 256 features
+  C.row_parts = off;
+  off += align256(2 * C.Tp_max * 4);
+  C.ctr = off;  // two counter sets (launch parity)
+  off += align256(2 * CHAIN_CTR_BYTES);
   C.gu_flag = off;
   off += align256(ffn / 64 * 4);
   for (int t = 0; t < CH_TYPES; ++t) {
     C.plan[t].units_off = off;
     off += align256(static_cast<int64_t>(C.plan[t].units.size()) * 16);
-    C.plan[t].offs_off = off;
-    off += align256(static_cast<int64_t>(C.plan[t].offs.size()) * 4);
   }
   C.bytes = off;
   return C;
@@ -148,7 +153,7 @@ Layout stage_layout(const pl_stage_config& c) {
   L.attn_ws = off;
   off += align256(attn_decode_workspace_bytes(static_cast<int>(R), c.Hq, c.max_ctx, c.hd));
   L.chain = off;
-  if (chain_shapes_ok(c)) off += align256(chain_layout(c, device_sms()).bytes);
+  if (chain_shapes_ok(c)) off += align256(chain_layout(c, device_sms() * chain_ctas_per_sm()).bytes);
   L.total = off;
   return L;
 }
@@ -173,29 +178,101 @@ struct Stage {
   // persistent decode-layer kernels
   bool chain_ok = false;
   ChainLayout CL;
-  unsigned long long ch_exp[4] = {0, 0, 0, 0};  // counter values after the last chain launch
-  int ch_seq = 0;
+  int ch_seq = 0;  // chain launches so far (gate_up tile flags hold the finishing launch's number)
+  // debug: PL_CHAIN_TRACE=k records per-unit globaltimer stamps of the k-th chain launch
+  unsigned long long* ch_trace = nullptr;
+  int ch_trace_seq = 0;
 
   int init_chain() {
     chain_ok = false;
     if (!chain_shapes_ok(cfg)) return PL_OK;
-    CL = chain_layout(cfg, device_sms());
+    CL = chain_layout(cfg, device_sms() * chain_ctas_per_sm());
     if (CL.bytes == 0) return PL_OK;
     for (int t = 0; t < CH_TYPES; ++t) {
       const ChainPlan& P = CL.plan[t];
       cudaError_t e = cudaMemcpy(ws + L.chain + P.units_off, P.units.data(), P.units.size() * sizeof(int4),
                                  cudaMemcpyHostToDevice);
-      if (e == cudaSuccess)
-        e = cudaMemcpy(ws + L.chain + P.offs_off, P.offs.data(), P.offs.size() * sizeof(int),
-                       cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return set_cuda_error(e, "chain unit tables");
     }
     return PL_OK;
   }
 
+  // Opt-in (PL_CHAIN=1): measured slower than one kernel per projection on B200 at
+  // every decode T (profiles/r2/chain_*.log) -- its software dependency
+  // tracking (two global norm barriers, split finalisation, the qkv tail) costs more
+  // than the fill/drain it removes between kernels
   bool use_chain(int T) const {
-    static const bool on = [] { const char* v = getenv("PL_CHAIN"); return !(v && v[0] == '0'); }();
+    static const bool on = [] { const char* v = getenv("PL_CHAIN"); return v && v[0] == '1'; }();
     return on && CL.bytes > 0 && pk_qkv && pk_o && pk_gu && pk_down && T <= CL.Tp_max && T <= 256;
+  }
+
+  // pl_stage_chain_bench: a chain of ONE projection of layer 0 (kind: 0 o, 1 gate_up, 2
+  // down, 3 qkv) with no dependencies and no finalisation -- the weight stream alone
+  std::vector<ChainPlan> bench_plans;
+  int bench_chain(int kind, int T, cudaStream_t st) {
+    if (CL.bytes == 0 || kind < 0 || kind > 3 || T <= 0 || T > CL.Tp_max)
+      return set_error(PL_ERR_CONFIG, "chain_bench: unavailable (kind %d, T %d)", kind, T);
+    if (bench_plans.empty()) bench_plans.resize(4);
+    ChainPlan& P = bench_plans[kind];
+    const pl_stage_config& c = cfg;
+    const int64_t d = c.d, qkv_dim = static_cast<int64_t>(c.Hq + 2 * c.Hkv) * c.hd;
+    const int64_t NN[4] = {d, 2 * static_cast<int64_t>(c.ffn), d, qkv_dim};
+    const int64_t KK[4] = {static_cast<int64_t>(c.Hq) * c.hd, d, c.ffn, d};
+    if (P.njobs == 0) {
+      P.njobs = 1;
+      P.kind[0] = kind;
+      P.N[0] = NN[kind];
+      P.K[0] = KK[kind];
+      // the splits the full chain uses for this projection
+      const ChainPlan& F = CL.plan[CH_FULL];
+      for (int j = 0; j < F.njobs; ++j)
+        if (F.kind[j] == kind) P.splits[0] = F.splits[j];
+      const int per = static_cast<int>((KK[kind] / 64 + P.splits[0] - 1) / P.splits[0]);
+      for (int sp = 0; sp < P.splits[0]; ++sp)
+        for (int tl = 0; tl < static_cast<int>(NN[kind] / 128); ++tl) {
+          const int k0 = sp * per, n = std::min(static_cast<int>(KK[kind] / 64), k0 + per) - k0;
+          if (n > 0) P.units.push_back(make_int4(0, tl, k0, n));
+        }
+      // unit table in the chain region's tail (the full plan's table is the largest)
+      P.units_off = CL.plan[CH_FULL].units_off;
+    }
+    uint8_t* base = ws + L.chain;
+    cudaError_t e = cudaMemcpyAsync(base + P.units_off, P.units.data(), P.units.size() * sizeof(int4),
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return set_cuda_error(e, "chain_bench units");
+    const pl_layer_weights& w = layers[0];
+    const void* wts[4] = {w.w_o, w.w_gate_up, w.w_down, w.w_qkv};
+    ChainLaunch k;
+    k.T = T;
+    k.Tp = chain_tp(T);
+    k.njobs = 1;
+    k.d = c.d;
+    k.ffn = c.ffn;
+    k.attn_dim = c.Hq * c.hd;
+    k.grid = CL.grid;
+    k.kind[0] = kind;
+    k.N[0] = P.N[0];
+    k.K[0] = P.K[0];
+    k.splits[0] = P.splits[0];
+    k.w[0] = wts[kind];
+    k.partial[0] = reinterpret_cast<float*>(base + CL.partial[kind]);
+    k.units = reinterpret_cast<const int4*>(base + P.units_off);
+    k.units_host = P.units.data();
+    k.n_units = static_cast<int>(P.units.size());
+    k.o_attn = buf(L.o);
+    k.h = buf(L.a);  // scratch: nothing is finalised
+    k.a = buf(L.a);
+    k.m = buf(L.m);
+    k.q_out = buf(L.qkv);
+    k.ld_q = qkv_dim;
+    k.part_ss = reinterpret_cast<float*>(base + CL.part_ss);
+    k.row_parts = reinterpret_cast<int*>(base + CL.row_parts);
+    k.eps = c.eps;
+    k.seq = ++ch_seq;
+    k.ctr = base + CL.ctr + (k.seq & 1) * CHAIN_CTR_BYTES;
+    k.gu_flag = reinterpret_cast<int*>(base + CL.gu_flag);
+    k.bench = 1;
+    return chain_launch(k, st);
   }
 
   // one chain launch of type `t` for layer l (CH_QKV_ONLY: layer l's qkv; CH_FULL: layer
@@ -224,17 +301,18 @@ struct Stage {
       k.splits[j] = P.splits[j];
       k.w[j] = wts[kd];
       k.partial[j] = reinterpret_cast<float*>(base + CL.partial[kd]);
-      k.arrive[j] = reinterpret_cast<int*>(base + CL.arrive[kd]);
     }
     k.units = reinterpret_cast<const int4*>(base + P.units_off);
-    k.unit_off = reinterpret_cast<const int*>(base + P.offs_off);
+    k.units_host = P.units.data();
+    k.n_units = static_cast<int>(P.units.size());
     k.o_attn = buf(L.o);
     k.h = hid;
     k.a = buf(L.a);
     k.m = buf(L.m);
     k.q_out = buf(L.qkv);
     k.ld_q = static_cast<int64_t>(c.Hq + 2 * c.Hkv) * c.hd;
-    k.ss = reinterpret_cast<float*>(base + CL.ss);
+    k.part_ss = reinterpret_cast<float*>(base + CL.part_ss);
+    k.row_parts = reinterpret_cast<int*>(base + CL.row_parts);
     k.has_norm[0] = t != CH_QKV_ONLY;
     k.has_norm[1] = t == CH_FULL;
     k.norm_w[0] = static_cast<const __nv_bfloat16*>(w.mlp_norm);
@@ -250,17 +328,18 @@ struct Stage {
     k.block_size = c.block_size;
     k.Hq = c.Hq;
     k.Hkv = c.Hkv;
-    k.ctr = reinterpret_cast<unsigned long long*>(base + CL.ctr);
-    k.gu_flag = reinterpret_cast<int*>(base + CL.gu_flag);
-    const bool has_o = t != CH_QKV_ONLY;
-    unsigned long long tgt[4] = {ch_exp[0] + (has_o ? c.d / 128 : 0), ch_exp[1] + (k.has_norm[0] ? CL.grid : 0),
-                                 ch_exp[2] + (has_o ? c.d / 128 : 0), ch_exp[3] + (k.has_norm[1] ? CL.grid : 0)};
-    for (int i = 0; i < 4; ++i) k.tgt[i] = tgt[i];
     k.seq = ++ch_seq;
-    const int rc = chain_launch(k, st);
-    if (rc) return rc;
-    for (int i = 0; i < 4; ++i) ch_exp[i] = tgt[i];
-    return PL_OK;
+    k.ctr = base + CL.ctr + (k.seq & 1) * CHAIN_CTR_BYTES;
+    if (ch_trace_seq == 0) {
+      const char* v = getenv("PL_CHAIN_TRACE");
+      ch_trace_seq = v ? atoi(v) : -1;
+      if (ch_trace_seq > 0 && cudaMalloc(&ch_trace, static_cast<size_t>(CL.grid) * 64 * 4 * 8) != cudaSuccess)
+        ch_trace = nullptr;
+      if (ch_trace) cudaMemset(ch_trace, 0, static_cast<size_t>(CL.grid) * 64 * 4 * 8);
+    }
+    k.trace = (ch_trace && k.seq == ch_trace_seq) ? ch_trace : nullptr;
+    k.gu_flag = reinterpret_cast<int*>(base + CL.gu_flag);
+    return chain_launch(k, st);
   }
 
   int pack(cudaStream_t st) {
@@ -574,9 +653,38 @@ int32_t pl_stage_pack_weights(void* handle, void* stream) {
   return static_cast<Stage*>(handle)->pack(static_cast<cudaStream_t>(stream));
 }
 
+// Debug: copy the per-unit stamps of the traced chain launch (PL_CHAIN_TRACE=k) to the
+// host: [grid][64][4] u64 = {claim time mod 2^40 | claim index << 40, unit popped by the
+// epilogue, accumulator ready, epilogue done}; returns the grid size in *grid.
+int32_t pl_stage_chain_trace(void* handle, uint64_t* out_host, int64_t n, int32_t* grid) {
+  Stage* s = static_cast<Stage*>(handle);
+  if (!s || !out_host || !grid) return set_error(PL_ERR_CONFIG, "chain_trace: null argument");
+  *grid = s->CL.grid;
+  if (!s->ch_trace) return set_error(PL_ERR_CONFIG, "chain_trace: set PL_CHAIN_TRACE=<launch number>");
+  const int64_t total = static_cast<int64_t>(s->CL.grid) * 64 * 4;
+  cudaError_t e = cudaMemcpy(out_host, s->ch_trace, std::min(n, total) * 8, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? PL_OK : set_cuda_error(e, "chain_trace copy");
+}
+
+// Benchmark of the persistent chain kernel's weight stream: `iters` launches of a chain
+// holding ONE projection of layer 0 (kind 0 o, 1 gate_up, 2 down, 3 qkv) at T tokens,
+// without dependencies or finalisation.  Results are scratch.
+int32_t pl_stage_chain_bench(void* handle, int32_t kind, int32_t T, int32_t iters, void* stream) {
+  Stage* s = static_cast<Stage*>(handle);
+  if (!s) return set_error(PL_ERR_CONFIG, "chain_bench: null handle");
+  if (!s->pk_qkv || !s->pk_o || !s->pk_gu || !s->pk_down)
+    return set_error(PL_ERR_CONFIG, "chain_bench: weights are not packed");
+  for (int i = 0; i < iters; ++i) {
+    const int rc = s->bench_chain(kind, T, static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+  }
+  return PL_OK;
+}
+
 int32_t pl_stage_destroy(void* handle) {
   Stage* s = static_cast<Stage*>(handle);
   if (!s) return PL_OK;
+  if (s->ch_trace) cudaFree(s->ch_trace);
   for (auto& r : s->probes)
     for (auto& e : r.ev) cudaEventDestroy(e);
   delete s;

@@ -16,7 +16,10 @@ depth) end to end on the GPU against the layer-streamed CPU oracle:
   that differ only in fp32 summation order, through the same model and
   workload (tests/golden/logit_tolerance.json, oracle/calibrate_tolerance.py).
 * greedy ids: every GPU id lies inside the oracle's tie band (its oracle logit
-  is within tol of the row max); exact matches are reported.
+  is within tol of the row max); exact matches are reported (two CPU oracles that
+  differ only in summation order already disagree on 4/32 (L3) and 8/32 (Q2)
+  argmaxes of this workload at standard init -- logit_tolerance.json -- so exact
+  identity is asserted only under the margin-engineered init, below).
 """
 
 import json
@@ -71,7 +74,7 @@ def test_llama3_8b_full_depth_standard_init():
     err, tol, gap, exact, n = full_model_check(LLAMA3_8B, "l3-32")
     assert err <= tol, f"max |dlogit| {err:.5f} > tol {tol:.5f}"
     assert gap <= tol, f"a GPU token sits {gap:.5f} below the oracle max (band {tol:.5f})"
-    assert exact >= n - 2
+    assert exact >= n // 2
 
 
 def test_qwen2_72b_ten_layer_slice_standard_init():
@@ -80,4 +83,17 @@ def test_qwen2_72b_ten_layer_slice_standard_init():
     err, tol, gap, exact, n = full_model_check(QWEN2_72B.with_(num_layers=10), "q2-10")
     assert err <= tol, f"max |dlogit| {err:.5f} > tol {tol:.5f}"
     assert gap <= tol, f"a GPU token sits {gap:.5f} below the oracle max (band {tol:.5f})"
-    assert exact >= n - 2
+    assert exact >= n // 2
+
+
+@pytest.mark.parametrize("name", ["l3-32", "q2-10"])
+def test_full_depth_peaked_greedy_identical(name):
+    """Margin-engineered init (embed U(+-8), lm_head[v] = 4 embed[v+1]):
+    the benched depths produce greedy ids IDENTICAL to the oracle's -- the oracle's
+    teacher-forced argmax equals the GPU's id at every step, i.e. the oracle's own
+    greedy sequence is the GPU's."""
+    from paper_2507_05043_b200 import LLAMA3_8B, QWEN2_72B
+
+    spec = (LLAMA3_8B if name == "l3-32" else QWEN2_72B.with_(num_layers=10)).with_(peaked=True)
+    err, tol, gap, exact, n = full_model_check(spec, name)
+    assert exact == n, f"{n - exact} of {n} greedy ids differ from the oracle"

@@ -180,12 +180,12 @@ def test_stage_logits_within_tolerance():
     exe.close()
 
 
-@pytest.mark.parametrize("pack", [False, True], ids=["per-projection", "chain"])
+@pytest.mark.parametrize("pack", [False, True], ids=["rowmajor", "chain"])
 @pytest.mark.parametrize("spec", [TINY, TINY.with_(Hq=8, Hkv=2, d=1024, ffn=1536, vocab=2048)])
 def test_decode_logits_within_tolerance(spec, pack):
     """Prefill then teacher-forced decode steps through the paged decode path: logits vs
-    the oracle.  Row-major weights run one GEMM per projection (split-K + reduce kernels);
-    packed weights run the persistent decode-layer chain kernel (chain.cu)."""
+    the oracle.  Row-major weights (TMA boxes) and packed weights (bulk copies of
+    pre-swizzled tiles; with PL_CHAIN=1 the persistent chain kernel, tests/test_chain_gpu.py)."""
     lens = [100, 37, 64]
     R, T = len(lens), sum(lens)
     steps = 5
