@@ -147,7 +147,9 @@ def parity_check(spec, eng, trace, res, profiles, rank, world, full_logits: bool
 
     from paper_2507_05043_b200.engine import schedule_key
 
-    ref = PL.PipelineEngine(eng.cfg, eng.cluster, profiles).run(trace)
+    refe = PL.PipelineEngine(eng.cfg, eng.cluster, profiles)
+    refe.link_profiles = list(eng.link_profiles)  # the measured links the timed run used
+    ref = refe.run(trace)
     a, b = schedule_key(ref), schedule_key(res)
     out = {"schedule_equal": all(a[k] == b[k] for k in a),
            "schedule_fields": sorted(k for k in a if a[k] != b[k]) or "all equal"}
@@ -278,6 +280,13 @@ def run_b200(args):
     local_prof = {s: profile_stage(exe, ctx=args.prompt) for s, exe in eng.gpu.exe.items()}
     profiles = gather_profiles(local_prof, S)
     eng.set_stage_profiles(profiles)
+    links = None
+    if S > 1:  # measured NVLink hops (LinkProfile, profiles.py:75-92) for the controller
+        from paper_2507_05043_b200.profiler import measure_links
+
+        eng.run(PL.Trace(requests=[PL.Request(0, 0.0, 16, 2)]))  # NCCL connections first
+        links = measure_links(eng)
+        eng.set_link_profiles(links)
     t_setup = time.time() - t_setup
 
     for _ in range(args.warmup):
@@ -376,6 +385,9 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "parity": parity,
+            "measured_links": [{"name": lp.name, "latency_us": round(lp.latency_s * 1e6, 2),
+                                "bandwidth_GBps": round(lp.bandwidth_bps / 1e9, 1)} for lp in links]
+            if links else None,
             "clocks": clk.summary,
             "setup_s": round(t_setup, 1),
             "schedule": {"decisions": len(runs[-1][0].decisions),

@@ -243,6 +243,9 @@ PL_API int32_t pl_gate_until_ns(const uint64_t* t0, uint64_t offset_ns, void* st
 
 /* Host<->device plumbing without a Python round trip. */
 PL_API int32_t pl_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* Single-process multi-GPU placement: enable NVLink peer access between every pair of
+ * the listed devices, so same-process hops are direct peer copies. */
+PL_API int32_t pl_enable_peer_access(int32_t ndev, const int32_t* devs);
 
 /* ------------------------------------------------------------ scheduler --- */
 

@@ -112,6 +112,7 @@ _SIGS = {
     "pl_record_globaltimer": (i32, [vp, vp]),
     "pl_gate_until_ns": (i32, [vp, u64, vp]),
     "pl_memcpy_async": (i32, [vp, vp, i64, vp]),
+    "pl_enable_peer_access": (i32, [i32, vp]),
     "pl_sched_create": (i32, [C.POINTER(SchedConfig), C.POINTER(vp)]),
     "pl_sched_destroy": (i32, [vp]),
     "pl_sched_choose_n": (i32, [vp, i64, i32, C.POINTER(i32), C.POINTER(i64), C.POINTER(f64)]),

@@ -188,6 +188,29 @@ int32_t pl_token_scatter(const int64_t* ids, const int32_t* req_slot, const int3
                               S(stream));
 }
 
+int32_t pl_enable_peer_access(int32_t ndev, const int32_t* devs) {
+  if (ndev < 0 || (ndev > 0 && !devs)) return set_error(PL_ERR_CONFIG, "enable_peer_access: bad arguments");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (int i = 0; i < ndev; ++i)
+    for (int j = 0; j < ndev; ++j) {
+      if (devs[i] == devs[j]) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devs[i], devs[j]);
+      if (!can) continue;
+      cudaSetDevice(devs[i]);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devs[j], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        cudaSetDevice(prev);
+        return set_cuda_error(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  cudaSetDevice(prev);
+  return PL_OK;
+}
+
 int32_t pl_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
   if (bytes <= 0) return PL_OK;
   cudaError_t e = cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault, S(stream));

@@ -149,6 +149,10 @@ class B200PipelineEngine(PipelineDriver):
         if torch.distributed.is_available() and torch.distributed.is_initialized():
             world, rank = torch.distributed.get_world_size(), torch.distributed.get_rank()
         self.placement = Placement(S, world, rank, devices)
+        local = sorted({d.index for d in self.placement.stage_device if d is not None and d.index is not None})
+        if len(local) > 1:  # same-process hops between GPUs: direct NVLink peer copies
+            arr = (C.c_int32 * len(local))(*local)
+            N.call("pl_enable_peer_access", len(local), arr)
         comms = create_link_comms(self.placement) if world > 1 else {}
         self.gpu = GpuBackend(decoder, cfg, self.placement, seed=seed, prompts=prompts, comms=comms,
                               throttle=throttle)

@@ -152,7 +152,7 @@ def measure_links(engine, small: int = 4096, large: int = 16 << 20, reps: int = 
             sbuf = torch.empty(large, dtype=torch.uint8, device=dev) if src_local else None
             dbuf = (torch.empty(large, dtype=torch.uint8, device=g.exe[dst].device)
                     if dst_local else None)
-            st = g.send_stream[src] if src_local else g.recv_stream[dst]
+            st = torch.cuda.Stream(dev)  # a private link stream (the runtime's are C++-owned)
 
             def once(nbytes):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -4,8 +4,12 @@
 
 Every rank builds the same B200PipelineEngine; stages are split over the ranks
 and hops between ranks are NCCL P2P.  Rank 0 (the head) checks that the greedy
-ids equal the CPU oracle's and that the schedule equals pipelink's.  Exit code
-0 = parity holds.
+ids equal the CPU oracle's and that the schedule equals pipelink's.  Every rank
+measures its links (profiler.measure_links: NCCL send timing, fed to the
+controller), records the realized per-chunk NCCL log of the links it sends on
+(CUDA events around each ncclSend) and checks it against the virtual LinkQueue
+log (tests/link_checks.py, after pkg/tests/test_transport.py:136-211).  One JSON
+summary line on rank 0.  Exit code 0 = parity holds.
 """
 
 import argparse
@@ -14,6 +18,7 @@ import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tests"))
 
 
 def main():
@@ -55,13 +60,32 @@ def main():
     trace = deploy.uniform_trace(a.requests, a.prompt, a.decode)
     profiles = [PL.synth_profile(hi - lo, 1e-6, 2e-5, stage_id=i) for i, (_, (lo, hi)) in enumerate(plan.stages)]
     eng = B200PipelineEngine(cfg, cluster, profiles, decoder=spec)
+    eng.run(PL.Trace(requests=[PL.Request(0, 0.0, 16, 2)]))  # NCCL connections, first launches
+    from paper_2507_05043_b200.profiler import measure_links
+    from link_checks import check_realized_link
+
+    links = measure_links(eng)
+    eng.set_link_profiles(links)
+    eng.gpu.record_links = True
     res = eng.run(trace)
     ok = True
-    ref = PL.PipelineEngine(cfg, cluster, profiles).run(trace)
+    refe = PL.PipelineEngine(cfg, cluster, profiles)
+    refe.link_profiles = list(links)
+    ref = refe.run(trace)
     if [(e.time_ns, e.kind, e.subject, e.stage) for e in res.events] != \
        [(e.time_ns, e.kind, e.subject, e.stage) for e in ref.events]:
         print(f"rank {rank}: schedule differs from pipelink", flush=True)
         ok = False
+    link_report, link_err = {}, None
+    try:
+        for lp in links:
+            if any(e.link == lp.name for e in eng.gpu.realized_links):
+                link_report[lp.name] = check_realized_link(eng.gpu.realized_links, res.link_events, lp.name)
+    except AssertionError as e:
+        link_err = f"rank {rank}: {e}"
+        ok = False
+    parts = [None] * world
+    dist.all_gather_object(parts, {"links": link_report, "err": link_err})
     if rank == 0:
         from oracle import decoder as OD
 
@@ -72,6 +96,18 @@ def main():
                if not np.array_equal(res.b200.tokens[r.id], want[i].numpy())]
         print(f"world {world}, {S} stages: {len(trace.requests) - len(bad)}/{len(trace.requests)} requests "
               f"identical to the CPU oracle; device {res.b200.run_time_s * 1e3:.1f} ms", flush=True)
+        import json
+
+        realized = {}
+        for p in parts:
+            realized.update(p["links"])
+        print(json.dumps({"world": world, "stages": S, "model": a.model, "tokens_identical": not bad,
+                          "schedule_equal": ok, "nccl_max_nchannels": os.environ.get("NCCL_MAX_NCHANNELS"),
+                          "measured_links": [{"name": lp.name, "latency_us": round(lp.latency_s * 1e6, 2),
+                                              "bandwidth_GBps": round(lp.bandwidth_bps / 1e9, 1)} for lp in links],
+                          "realized_nccl_links": realized,
+                          "link_errors": [p["err"] for p in parts if p["err"]],
+                          "device_run_ms": round(res.b200.run_time_s * 1e3, 2)}), flush=True)
         ok = ok and not bad
     t = torch.tensor([0 if ok else 1])
     dist.all_reduce(t)
