@@ -195,6 +195,10 @@ typedef struct pl_microbatch {
                                 output (non-last), updated in place           */
   int64_t* out_ids;          /* last stage: [R] greedy tokens                 */
   int32_t n_decode;          /* mixed: decode requests leading the batch      */
+  void* peer_hidden;         /* decode, non-last stage, or NULL: the last residual
+                                epilogue also stores the output rows here -- the
+                                next stage's receive buffer, possibly on a peer
+                                GPU (fused transport: no link copy)           */
 } pl_microbatch;
 
 PL_API int64_t pl_stage_workspace_bytes(const pl_stage_config* cfg);
@@ -328,6 +332,10 @@ typedef struct pl_pipeline_config {
   void* const* out_ids;  /* [n_stages * n_slots] int64 tokens (last stage) */
   void* const* comm;     /* [n_stages] NCCL communicators or NULL */
   int64_t* const* ids_recv; /* head: [n_slots] return-hop landing buffers */
+  int32_t fuse_transport;   /* decode payloads between stages of THIS process: the
+                               producer's last residual epilogue stores straight into
+                               the next stage's buffer (peer memory over NVLink); the
+                               link issues no copy (prefill chunks still copy) */
 } pl_pipeline_config;
 
 PL_API int32_t pl_pipeline_create(const pl_pipeline_config* cfg, void** handle);

@@ -48,7 +48,7 @@ class MicroBatch(C.Structure):
     _fields_ = [
         ("T", i32), ("R", i32), ("phase", i32), ("max_seqlen", i32), ("max_ctx", i32),
         ("meta", vp), ("token_ids", vp), ("last_token", vp), ("hidden", vp), ("out_ids", vp),
-        ("n_decode", i32),
+        ("n_decode", i32), ("peer_hidden", vp),
     ]
 
 
@@ -71,6 +71,7 @@ class PipelineConfig(C.Structure):
         ("num_blocks", i64), ("max_tokens", i32), ("max_reqs", i32), ("d", i32), ("throttle", i32),
         ("record_links", i32), ("stage", vp), ("stream", vp), ("device", vp), ("meta_dev", vp),
         ("ids_dev", vp), ("hidden", vp), ("out_ids", vp), ("comm", vp), ("ids_recv", vp),
+        ("fuse_transport", i32),
     ]
 
 

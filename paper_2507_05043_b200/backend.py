@@ -125,6 +125,9 @@ class GpuBackend(Backend):
         self.comms = comms or {}
         self.throttle = throttle
         self.record_links = False   # per-chunk CUDA events -> realized link log (device clock)
+        # native runtime: decode payloads between stages of this process are stored by the
+        # producer's last residual epilogue straight into the next stage's buffer
+        self.fuse_transport = True
         self.S = placement.n_stages
         self.layer_ranges = [rng for _, rng in cfg.partition.stages]
         self.n_slots = cfg.controller.effective_n_max(self.S)
@@ -551,7 +554,7 @@ class GpuBackend(Backend):
         return h
 
     def _native_handle(self, record_links: bool):
-        key = (self._built_for, bool(record_links), bool(self.throttle))
+        key = (self._built_for, bool(record_links), bool(self.throttle), bool(self.fuse_transport))
         if getattr(self, "_native", None) is not None and self._native[0] == key:
             return self._native[1]
         self._native_close()
@@ -585,6 +588,7 @@ class GpuBackend(Backend):
         c.n_stages, c.n_slots, c.max_blocks, c.block_size = S, K, self.max_blocks, BLOCK_SIZE
         c.num_blocks, c.max_tokens, c.max_reqs, c.d = self.num_blocks, self.max_tokens, self.max_reqs, self.spec.d
         c.throttle, c.record_links = int(self.throttle), int(record_links)
+        c.fuse_transport = int(self.fuse_transport)
         c.stage, c.stream, c.device = C.cast(stage, C.c_void_p), C.cast(stream, C.c_void_p), C.cast(dev, C.c_void_p)
         c.meta_dev, c.ids_dev = C.cast(meta, C.c_void_p), C.cast(ids, C.c_void_p)
         c.hidden, c.out_ids = C.cast(hidden, C.c_void_p), C.cast(out_ids, C.c_void_p)

@@ -66,6 +66,7 @@ struct GemmArgs {
   const __nv_bfloat16* bias;
   const __nv_bfloat16* residual;
   int64_t ldr;
+  __nv_bfloat16* C2;  // fused transport: a second copy of every final output row (ldc), or null
   float* partial;     // split-K partials, fp32: pmode 0 [splits][N][Tp], pmode 1 [splits][T][N]
   int Tp;             // T rounded up to the BN tile
   int pmode;
@@ -180,12 +181,15 @@ PL_DEV void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // Final (non-partial) epilogue for one accumulator element.
 PL_DEV void store_out(const GemmArgs& a, int epi, int t, int n, float acc) {
+  __nv_bfloat16 v;
   if (epi == EPI_RESIDUAL)
-    a.C[(int64_t)t * a.ldc + n] = f2bf(rbf(acc) + bf2f(a.residual[(int64_t)t * a.ldr + n]));
+    v = f2bf(rbf(acc) + bf2f(a.residual[(int64_t)t * a.ldr + n]));
   else if (epi == EPI_BIAS)
-    a.C[(int64_t)t * a.ldc + n] = f2bf(acc + bf2f(a.bias[n]));
+    v = f2bf(acc + bf2f(a.bias[n]));
   else
-    a.C[(int64_t)t * a.ldc + n] = f2bf(acc);
+    v = f2bf(acc);
+  a.C[(int64_t)t * a.ldc + n] = v;
+  if (a.C2) a.C2[(int64_t)t * a.ldc + n] = v;  // the next stage's receive buffer (peer memory)
 }
 
 // Cluster split-K reduction (SWAP, one weight tile per cluster, cluster rank = split):
@@ -887,7 +891,8 @@ __global__ void __launch_bounds__(256)
     gemm_splitk_reduce_kernel(const float* partial, int splits, int T, int Tp, int N,
                               int epi, __nv_bfloat16* __restrict__ C, int64_t ldc,
                               const __nv_bfloat16* __restrict__ bias,
-                              const __nv_bfloat16* __restrict__ residual, int64_t ldr, int swiglu_il) {
+                              const __nv_bfloat16* __restrict__ residual, int64_t ldr, int swiglu_il,
+                              __nv_bfloat16* __restrict__ C2) {
   pdl_trigger();
   pdl_wait();
   const int n_out = (epi == EPI_SWIGLU) ? N / 2 : N;
@@ -919,14 +924,17 @@ __global__ void __launch_bounds__(256)
       const int t = t0 + k;
       if (t >= T) break;
       const int64_t o = static_cast<int64_t>(t) * ldc + j;
+      __nv_bfloat16 v;
       if (epi == EPI_SWIGLU)
-        C[o] = f2bf(rbf(silu_f(rbf(av[k]))) * rbf(uv[k]));
+        v = f2bf(rbf(silu_f(rbf(av[k]))) * rbf(uv[k]));
       else if (epi == EPI_RESIDUAL)
-        C[o] = f2bf(rbf(av[k]) + bf2f(residual[static_cast<int64_t>(t) * ldr + j]));
+        v = f2bf(rbf(av[k]) + bf2f(residual[static_cast<int64_t>(t) * ldr + j]));
       else if (epi == EPI_BIAS)
-        C[o] = f2bf(av[k] + bf2f(bias[j]));
+        v = f2bf(av[k] + bf2f(bias[j]));
       else
-        C[o] = f2bf(av[k]);
+        v = f2bf(av[k]);
+      C[o] = v;
+      if (C2) C2[o] = v;  // fused transport into the next stage's buffer
     }
   }
 }
@@ -1421,6 +1429,8 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   a.bias = bias;
   a.residual = residual;
   a.ldr = ldr;
+  a.C2 = fuse ? fuse->mirror : nullptr;
+  if (a.C2 && !swap) return set_error(PL_ERR_CONFIG, "gemm: a mirrored output needs the decode (SWAP) path");
   a.splits = epi == EPI_ARGMAX ? 1 : gemm_num_splits(N, K, swap);
   a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
   const int bn = swap ? swap_bn(T) : 256;
@@ -1562,7 +1572,8 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     const int64_t total = n_out * ((T + 3) / 4);
     const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
     return launch_k("gemm_splitk_reduce_kernel", gemm_splitk_reduce_kernel, dim3(blocks), dim3(256), 0,
-                    st, a.partial, a.splits, a.T, a.Tp, a.N, epi, C, ldc, bias, residual, ldr, a.swiglu_il);
+                    st, a.partial, a.splits, a.T, a.Tp, a.N, epi, C, ldc, bias, residual, ldr, a.swiglu_il,
+                    a.C2);
   }
   return PL_OK;
 }

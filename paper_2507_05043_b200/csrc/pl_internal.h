@@ -91,6 +91,9 @@ int64_t gemm_workspace_bytes(int64_t T, int64_t N, int64_t K, int epi);
 enum FuseKind : int { FUSE_NONE = 0, FUSE_RESIDUAL_NORM = 1, FUSE_QKV_ROPE = 2 };
 struct FusedEpi {
   int kind = FUSE_NONE;
+  // fused transport (any kind): every final output row also stored here (ldc), e.g. the
+  // next pipeline stage's receive buffer on a peer GPU (decode / SWAP GEMMs only)
+  __nv_bfloat16* mirror = nullptr;
   // FUSE_RESIDUAL_NORM: C (= residual) updated in place, then norm_out = rmsnorm(C) * norm_w
   const __nv_bfloat16* norm_w = nullptr;
   float eps = 0.f;

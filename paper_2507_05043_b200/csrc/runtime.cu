@@ -93,7 +93,7 @@ struct Pipeline : sched::Hooks {
   // configuration
   int S = 1, n_slots = 1, max_blocks = 1, block_size = 64, max_tokens = 1, max_reqs = 1, d = 0;
   int64_t num_blocks = 0;
-  bool throttle = false, record_links = false;
+  bool throttle = false, record_links = false, fuse = false;
   std::vector<StageRt> st;
   std::vector<void*> comm;  // per link
   int64_t* last_token = nullptr;
@@ -159,7 +159,7 @@ struct Pipeline : sched::Hooks {
   int init(const pl_pipeline_config& c) {
     S = c.n_stages, n_slots = c.n_slots, max_blocks = c.max_blocks, block_size = c.block_size;
     max_tokens = c.max_tokens, max_reqs = c.max_reqs, d = c.d, num_blocks = c.num_blocks;
-    throttle = c.throttle != 0, record_links = c.record_links != 0;
+    throttle = c.throttle != 0, record_links = c.record_links != 0, fuse = c.fuse_transport != 0;
     if (S < 1 || n_slots < 1 || max_blocks < 1 || block_size < 1 || max_tokens < 1 || max_reqs < 1 || d < 1)
       return set_error(PL_ERR_CONFIG, "pipeline_create: bad sizes");
     st.resize(S);
@@ -444,6 +444,15 @@ struct Pipeline : sched::Hooks {
     if (r.n_fwd >= RUN_AHEAD && !cu(cudaEventSynchronize(ahead), "run-ahead")) return;  // run-ahead cap
     if (r.has_send[k]) cudaStreamWaitEvent(r.comp, r.ev_send[k], 0);
     if (s > 0 && r.recv_ev[k]) cudaStreamWaitEvent(r.comp, r.recv_ev[k], 0);
+    // fused transport: a decode payload for a stage of this process is stored by this
+    // forward's last residual epilogue straight into the next stage's slot buffer --
+    // once that slot's previous occupant has left it
+    void* peer = nullptr;
+    if (fused_hop(s, rec)) {
+      StageRt& rd = st[s + 1];
+      if (rd.has_send[k]) cudaStreamWaitEvent(r.comp, rd.ev_send[k], 0);
+      peer = rd.hidden[k];
+    }
     if (s == 0 && rec.decode != 0 && last_fb) {  // decode rows read the latest token scatter
       cudaStreamWaitEvent(r.comp, last_fb, 0);
       if (!first_decode) {
@@ -471,6 +480,7 @@ struct Pipeline : sched::Hooks {
     m.last_token = (s == 0 && rec.decode != 0) ? last_token : nullptr;
     m.hidden = r.hidden[k];
     m.out_ids = s == S - 1 ? r.out_ids[k] : nullptr;
+    m.peer_hidden = peer;
     if (!ok(pl_stage_forward(r.stage, &m, r.comp))) return;
     cudaEventRecord(b, r.comp);
     cudaEventRecord(r.ev_comp[k], r.comp);
@@ -478,6 +488,12 @@ struct Pipeline : sched::Hooks {
     cudaEventRecord(ahead, r.comp);
     r.n_fwd++;
     if (S == 1) scatter(rec, mb.id, r.out_ids[k], r.comp);
+  }
+
+  // decode payloads between two stages of this process travel inside the producer's
+  // epilogue (pl_microbatch.peer_hidden) when fused transport is on
+  bool fused_hop(int s, const MbRec& rec) const {
+    return fuse && rec.decode == 1 && s + 1 < S && st[s].local && st[s + 1].local;
   }
 
   void emit(int link, const sched::Payload& p, const sched::Chunk& ch, int64_t offset, int64_t now) override {
@@ -502,6 +518,20 @@ struct Pipeline : sched::Hooks {
     cudaEvent_t t_emit = nullptr;
     if (rs.local && record_links) {
       t_emit = pool(rs.dev).take();
+    }
+    if (!is_ret && fused_hop(src, rec)) {
+      // the bytes already landed in dst's slot at the end of the producing forward: the
+      // chunk is that forward's completion (a zero-length realized chunk)
+      cudaSetDevice(rs.dev);
+      cudaStreamWaitEvent(rs.send, rs.ev_comp[k], 0);
+      if (t_emit) cudaEventRecord(t_emit, rs.send);
+      if (t_emit) note_chunk(link, src, k, p, ch, t_emit, rs.send);
+      cudaEventRecord(rs.ev_send[k], rs.send);
+      rs.has_send[k] = 1;
+      cudaEvent_t e = pool(rs.dev).take();
+      cudaEventRecord(e, rs.send);
+      recv_done(dst, rec, p.mb, e, is_ret, deliver);
+      return;
     }
     if (rs.local && rd.local) {
       if (first && rd.has_send[k]) cudaStreamWaitEvent(rs.send, rd.ev_send[k], 0);

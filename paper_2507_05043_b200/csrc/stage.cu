@@ -457,7 +457,7 @@ struct Stage {
       }
     }
 
-    if (decode && use_chain(T)) {
+    if (decode && use_chain(T) && !mb.peer_hidden) {
       // persistent chain kernels: per layer one attention launch and one chain launch
       for (int l = 0; l < c.num_layers; ++l) {
         const pl_layer_weights& w = layers[l];
@@ -565,8 +565,15 @@ struct Stage {
                             nullptr, pk_gu)))
         return rc;
       mark(5);
-      // the next layer's input norm rides on this residual reduction (not across stages)
+      // the next layer's input norm rides on this residual reduction (not across stages);
+      // the stage's last residual write also lands in the next stage's buffer (fused
+      // transport, pl_microbatch.peer_hidden)
       FusedEpi df = norm_fuse(l + 1 < c.num_layers ? layers[l + 1].attn_norm : nullptr);
+      if (l + 1 == c.num_layers && mb.peer_hidden) {
+        if (!decode || c.is_last)
+          return set_error(PL_ERR_CONFIG, "stage_forward: peer_hidden is for decode micro-batches of non-last stages");
+        df.mirror = static_cast<__nv_bfloat16*>(mb.peer_hidden);
+      }
       if ((rc = gemm_launch(m, ffn, static_cast<const __nv_bfloat16*>(w.w_down), ffn, nullptr, hid, d,
                             hid, d, T, d, ffn, EPI_RESIDUAL, gws, gws_bytes, nullptr, st, &df,
                             &a_ready, pk_down)))

@@ -20,7 +20,10 @@ in C++ (csrc/runtime.cu); ``native=False`` runs the Python twin
 (driver.PipelineDriver + backend.GpuBackend).  Both give the identical
 schedule and tokens.  Extra keywords: ``throttle=True`` replays the virtual
 link timing on the GPU clock; ``prompts={rid: ids}`` overrides the synthetic
-prompts; ``devices=[...]`` spreads stages over local GPUs without torchrun.
+prompts; ``devices=[...]`` spreads stages over local GPUs without torchrun;
+``fuse_transport`` (default on, native runtime) stores decode payloads between
+stages of this process from the producer's last residual epilogue straight into
+the next stage's buffer over NVLink peer memory instead of a link copy.
 """
 
 from __future__ import annotations
@@ -138,7 +141,7 @@ class B200PipelineEngine(PipelineDriver):
 
     def __init__(self, cfg, cluster, stage_profiles, *, decoder: DecoderSpec, seed: int = 0,
                  devices: list | None = None, prompts: dict | None = None, throttle: bool = False,
-                 native: bool = True):
+                 native: bool = True, fuse_transport: bool = True):
         if cfg.model.hidden_dim != decoder.d or cfg.model.dtype_bytes != 2:
             raise pipelink.ConfigError("cfg.model must describe the decoder's bf16 residual stream "
                                        "(use DecoderSpec.model_spec())")
@@ -156,6 +159,7 @@ class B200PipelineEngine(PipelineDriver):
         comms = create_link_comms(self.placement) if world > 1 else {}
         self.gpu = GpuBackend(decoder, cfg, self.placement, seed=seed, prompts=prompts, comms=comms,
                               throttle=throttle)
+        self.gpu.fuse_transport = fuse_transport
         super().__init__(cfg, cluster, stage_profiles, backend=self.gpu)
         self._comms = comms
         self.native = native

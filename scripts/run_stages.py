@@ -64,14 +64,15 @@ def main():
     ap.add_argument("--prompt", type=int, default=512)
     ap.add_argument("--decode", type=int, default=256)
     ap.add_argument("--no-links", action="store_true", help="skip the realized link log")
+    ap.add_argument("--no-fuse", action="store_true", help="copy decode payloads on the link streams")
     a = ap.parse_args()
 
     import torch
 
+    from paper_2507_05043_b200 import PRESETS, deploy  # locates the reference pipelink first
     import bench as B
     import pipelink as PL
     from link_checks import check_realized_link
-    from paper_2507_05043_b200 import PRESETS, deploy
     from paper_2507_05043_b200.engine import B200PipelineEngine, schedule_key
     from paper_2507_05043_b200.profiler import measure_links, profile_stage
 
@@ -87,7 +88,8 @@ def main():
     trace = deploy.uniform_trace(a.batch, a.prompt, a.decode)
     placeholder = [PL.synth_profile(hi - lo, 1e-6, 1e-4, stage_id=i) for i, (_, (lo, hi)) in enumerate(plan.stages)]
     t0 = time.time()
-    eng = B200PipelineEngine(cfg, cluster, placeholder, decoder=spec, devices=devices)
+    eng = B200PipelineEngine(cfg, cluster, placeholder, decoder=spec, devices=devices,
+                             fuse_transport=not a.no_fuse)
     eng.prepare(trace)
     eng.set_stage_profiles([profile_stage(eng.gpu.exe[s], ctx=a.prompt) for s in range(S)])
     warm = PL.Trace(requests=[PL.Request(r.id, 0.0, min(r.input_len, 256), 2) for r in trace.requests[:4]])
@@ -118,7 +120,8 @@ def main():
     bubbles = [round(PL.measure_bubble(st.real, s, 0.0, st.real.end_ns / 1e9), 4) for s in range(S)]
     out = {"workload": f"{spec.name} {S}-stage pipeline on {G} GPU(s), one process, {a.batch} requests "
                        f"{a.prompt}/{a.decode}",
-           "stage_gpu": stage_gpu, "device_tok_s": round(st.throughput_tok_s, 1),
+           "stage_gpu": stage_gpu, "fused_transport": not a.no_fuse,
+           "device_tok_s": round(st.throughput_tok_s, 1),
            "decode_window_tok_s": round(window, 1) if window else None,
            "tpot_p50_ms": round(1e3 * (st.tpot_p50_s() or 0), 3), "ttft_p50_ms": round(1e3 * (st.ttft_p50_s() or 0), 2),
            "roofline": roof,

@@ -434,3 +434,30 @@ def test_decode_rows_batch_invariant():
     for h, t in outs[1:]:
         assert torch.equal(h, outs[0][0]) and t == outs[0][1]
     exe.close()
+
+
+def test_fused_transport_same_tokens_and_link_log():
+    """Fused transport (§8(f)3): decode payloads between stages of one process are stored
+    by the producer's last residual epilogue straight into the next stage's buffer (no
+    link copy).  Same schedule, same tokens as the copying transport and the oracle; the
+    realized link log still follows the LinkQueue (tests/link_checks.py), decode chunks
+    now zero-length at the producer's completion."""
+    from link_checks import check_realized_link
+
+    spec = TINY.with_(peaked=True, num_layers=4)
+    cfg, cluster, plan, trace = config1(spec, S=4, n_req=6, in_len=90, out_len=7, mbt=256, chunk=4096)
+    profiles = synth_profiles(plan)
+    outs = {}
+    for fuse in (False, True):
+        eng = B200PipelineEngine(cfg, cluster, profiles, decoder=spec, fuse_transport=fuse)
+        eng.gpu.record_links = True
+        res = eng.run(trace)
+        assert result_key(res) == result_key(pipelink.PipelineEngine(cfg, cluster, profiles).run(trace))
+        for lp in eng.link_profiles:
+            check_realized_link(eng.gpu.realized_links, res.link_events, lp.name)
+        outs[fuse] = res.b200.tokens
+        eng.close()
+    _, _, want = oracle_greedy(spec, trace)
+    for i, r in enumerate(trace.requests):
+        assert np.array_equal(outs[True][r.id], outs[False][r.id])
+        assert np.array_equal(outs[True][r.id], want[i].numpy())
