@@ -209,14 +209,8 @@ def dist_setup():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
-        if os.environ.get("PL_OVERSUBSCRIBE_GPUS"):
-            # two ranks per GPU (testing): torch's own collectives stay on gloo -- an NCCL
-            # world communicator rejects duplicate GPUs; the hop links are b200link's
-            # two-rank NCCL communicators
-            dist.init_process_group(backend="gloo", world_size=world, rank=rank)
-        else:
-            dist.init_process_group(backend="cuda:nccl,cpu:gloo", world_size=world, rank=rank,
-                                    device_id=torch.device("cuda", local))
+        dist.init_process_group(backend="cuda:nccl,cpu:gloo", world_size=world, rank=rank,
+                                device_id=torch.device("cuda", local))
     return world, rank, local
 
 

@@ -63,12 +63,8 @@ class _MbRec:
 
 
 def local_device_index(default: int = 0) -> int:
-    """This process's GPU: LOCAL_RANK, folded onto PL_OVERSUBSCRIBE_GPUS devices when that
-    is set (testing only: e.g. an 8-rank, 8-stage pipeline on a 4-GPU box, two ranks per
-    GPU; every hop communicator still joins two distinct GPUs)."""
-    local = int(os.environ.get("LOCAL_RANK", default))
-    mod = int(os.environ.get("PL_OVERSUBSCRIBE_GPUS", "0") or 0)
-    return local % mod if mod > 0 else local
+    """This process's GPU: LOCAL_RANK (one process per GPU)."""
+    return int(os.environ.get("LOCAL_RANK", default))
 
 
 class Placement:

@@ -1,6 +1,8 @@
 // extern "C" entry points of libb200link (declared in include/b200link.h) and
 // the thread-local error channel.
 #include <atomic>
+#include <mutex>
+#include <set>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -26,6 +28,19 @@ int set_error(int code, const char* fmt, ...) {
 
 int set_cuda_error(cudaError_t e, const char* what) {
   return set_error(PL_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+int ensure_smem_attr(const void* func, int bytes, const char* what) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({dev, func})) return PL_OK;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return set_cuda_error(e, what);
+  done.insert({dev, func});
+  return PL_OK;
 }
 
 bool pdl_enabled() {

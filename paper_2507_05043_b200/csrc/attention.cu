@@ -258,12 +258,9 @@ int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* 
     return set_error(PL_ERR_CONFIG, "attention prefill: GQA group %d unsupported (1, 2, 4, 8)", G);
   if (ldqkv % 8 || ldo % 8) return set_error(PL_ERR_CONFIG, "attention: leading dims % 8");
   constexpr int smem = 32768 * 3;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_prefill_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "attn_prefill smem attribute");
-    attr = true;
+  {
+    const int rc0 = ensure_smem_attr(reinterpret_cast<const void*>(attn_prefill_kernel), smem, "attn_prefill smem attribute");
+    if (rc0) return rc0;
   }
   const int QT = PF_ROWS / G;
   dim3 grid((max_seqlen + QT - 1) / QT, Hkv, R);
@@ -776,13 +773,9 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
 #define PL_DECODE_CASE(GG)                                                                      \
   case GG: {                                                                                    \
     constexpr int smem = DecodeSmem<GG>::TOTAL;                                                 \
-    static bool attr = false;                                                                   \
-    if (!attr) {                                                                                \
-      cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<GG>,                              \
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);  \
-      if (e != cudaSuccess) return set_cuda_error(e, "attn_decode smem attribute");             \
-      attr = true;                                                                              \
-    }                                                                                           \
+    if ((rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_decode_kernel<GG>), smem,          \
+                               "attn_decode smem attribute")))                                  \
+      return rc;                                                                                \
     rc = launch_k("attn_decode_kernel", attn_decode_kernel<GG>, grid, dim3(DEC_THREADS), smem,  \
                   st, mk, mv, da);                                                              \
     break;                                                                                      \

@@ -830,12 +830,8 @@ template <int BN>
 static int chain_launch_bn(const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                            const ChainArgs& a, int grid, cudaStream_t st) {
   constexpr int smem = ChainSmem<BN>::TOTAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(chain_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "chain smem attribute");
-    attr = true;
-  }
+  const int rc = ensure_smem_attr(reinterpret_cast<const void*>(chain_kernel<BN>), smem, "chain smem attribute");
+  if (rc) return rc;
   return launch_k("chain_kernel", chain_kernel<BN>, dim3(grid), dim3(CH_THREADS), smem, st, m0, m1, m2, a);
 }
 

@@ -1287,13 +1287,9 @@ int make_packed_map(CUtensorMap* out, const void* ptr, int64_t tiles) {
 
 template <int S>
 int launch_pair_s(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         PairSmem<S>::TOTAL);
-    if (e != cudaSuccess) return set_cuda_error(e, "gemm pair smem attribute");
-    attr_set = true;
-  }
+  const int rc = ensure_smem_attr(reinterpret_cast<const void*>(gemm_pair_kernel<S>), PairSmem<S>::TOTAL,
+                                  "gemm pair smem attribute");
+  if (rc) return rc;
   return launch_k("gemm_pair_kernel", gemm_pair_kernel<S>, dim3(grid), dim3(GEMM_THREADS), PairSmem<S>::TOTAL, st, ma, mb,
                   a);
 }
@@ -1306,13 +1302,9 @@ template <int BN, bool SWAP, int CTAS = (BN <= 128 ? 2 : 1)>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, int grid,
               cudaStream_t st, int cluster = 0) {
   constexpr int smem = GemmSmem<BN, SWAP, CTAS>::TOTAL;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, SWAP, CTAS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
-    attr_set = true;
-  }
+  const int rc = ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel<BN, SWAP, CTAS>), smem,
+                                  "gemm smem attribute");
+  if (rc) return rc;
   return launch_kc("gemm_tc_kernel", gemm_tc_kernel<BN, SWAP, CTAS>, dim3(grid), dim3(GEMM_THREADS), smem, st, cluster,
                    ma, mb, a);
 }

@@ -31,6 +31,11 @@ int check_launch(const char* what);
 // PDL on/off (env PL_PDL=0 disables programmatic dependent launch)
 bool pdl_enabled();
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the CURRENT device, set once
+// per (device, function): the attribute is per device, and one process may drive
+// stages on several GPUs
+int ensure_smem_attr(const void* func, int bytes, const char* what);
+
 // Launch with programmatic stream serialization so the kernel may start while its
 // predecessor in the stream drains (see pdl_wait / pdl_trigger in common.cuh).
 // cluster_x > 0: launch as clusters of cluster_x consecutive CTAs.

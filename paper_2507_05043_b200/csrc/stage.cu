@@ -165,7 +165,22 @@ struct ProbeRec {
   int phase, T, kind;  // kind 0: per-projection kernels, 1: attention + chain kernel
 };
 
+// Makes the stage's GPU current for the duration of a call (one process may drive
+// stages on several GPUs; kernels must launch on the device that owns the stream).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 struct Stage {
+  int dev = 0;  // the CUDA device the stage was created on
   pl_stage_config cfg;
   std::vector<pl_layer_weights> layers;
   uint8_t* ws;
@@ -637,6 +652,7 @@ int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* laye
   cudaError_t e = cudaMemset(workspace, 0, static_cast<size_t>(L.total));
   if (e != cudaSuccess) return set_cuda_error(e, "stage workspace memset");
   Stage* s = new Stage();
+  cudaGetDevice(&s->dev);
   s->cfg = *cfg;
   s->layers.assign(layers, layers + cfg->num_layers);
   s->ws = static_cast<uint8_t*>(workspace);
@@ -652,12 +668,16 @@ int32_t pl_stage_create(const pl_stage_config* cfg, const pl_layer_weights* laye
 
 int32_t pl_stage_forward(void* handle, const pl_microbatch* mb, void* stream) {
   if (!handle || !mb) return set_error(PL_ERR_CONFIG, "stage_forward: null argument");
-  return static_cast<Stage*>(handle)->forward(*mb, static_cast<cudaStream_t>(stream));
+  Stage* s = static_cast<Stage*>(handle);
+  DeviceGuard g(s->dev);
+  return s->forward(*mb, static_cast<cudaStream_t>(stream));
 }
 
 int32_t pl_stage_pack_weights(void* handle, void* stream) {
   if (!handle) return set_error(PL_ERR_CONFIG, "stage_pack_weights: null handle");
-  return static_cast<Stage*>(handle)->pack(static_cast<cudaStream_t>(stream));
+  Stage* s = static_cast<Stage*>(handle);
+  DeviceGuard g(s->dev);
+  return s->pack(static_cast<cudaStream_t>(stream));
 }
 
 // Debug: copy the per-unit stamps of the traced chain launch (PL_CHAIN_TRACE=k) to the
@@ -681,6 +701,7 @@ int32_t pl_stage_chain_bench(void* handle, int32_t kind, int32_t T, int32_t iter
   if (!s) return set_error(PL_ERR_CONFIG, "chain_bench: null handle");
   if (!s->pk_qkv || !s->pk_o || !s->pk_gu || !s->pk_down)
     return set_error(PL_ERR_CONFIG, "chain_bench: weights are not packed");
+  DeviceGuard g(s->dev);
   for (int i = 0; i < iters; ++i) {
     const int rc = s->bench_chain(kind, T, static_cast<cudaStream_t>(stream));
     if (rc) return rc;

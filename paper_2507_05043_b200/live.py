@@ -16,6 +16,14 @@ prefixes a 4-byte request count, demo.py:161-163).
     result = run_device_demo(cfg, cluster, stage_profiles, trace, decoder=TINY)
     result.tokens_by_request   # {rid: count}   (rank 0)
     result.tokens              # {rid: ids}     (rank 0)
+
+Runtime monitoring: every stage writes the device-clock duration
+of its last completed forward (phase, tokens, ms) into its slot of the frame header;
+the tail returns all stages' reports after the token ids (the reference returns only
+the 8-byte ids, demo.py:32-49).  The head feeds them, and each micro-batch's
+dispatch-to-feedback time, to a ``RuntimeMonitor`` (monitor.py) that rebuilds the
+StageProfiles / LinkProfiles ``choose_n`` plans with every ``monitor_epoch``
+micro-batches (``monitor_epoch=0`` keeps the startup profiles).
 """
 
 from __future__ import annotations
@@ -38,7 +46,40 @@ BatchPhase = pipelink.engine.BatchPhase
 RequestState = pipelink.RequestState
 PayloadClass = pipelink.PayloadClass
 Phase = pipelink.Phase
-HDR = 8  # int32 words: T, R, phase, max_seqlen, max_ctx, slot, meta_len, reserved
+HDR0 = 8  # int32 words: T, R, phase, max_seqlen, max_ctx, slot, meta_len, reserved
+# then 3 words per stage: the stage's last completed forward (phase, tokens, ms as f32 bits)
+
+
+def hdr_words(S: int) -> int:
+    return HDR0 + 3 * S
+
+
+class _FwdClock:
+    """CUDA events around a stage's forwards; reports the latest completed one."""
+
+    def __init__(self):
+        self.q = deque()
+        self.last = (0, 0, 0.0)
+
+    def start(self, stream):
+        a = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        return a
+
+    def stop(self, a, stream, phase: int, T: int):
+        b = torch.cuda.Event(enable_timing=True)
+        b.record(stream)
+        self.q.append((phase, T, a, b))
+
+    def report(self) -> tuple[int, int, float]:
+        while self.q and self.q[0][3].query():
+            phase, T, a, b = self.q.popleft()
+            self.last = (phase, T, a.elapsed_time(b))
+        return self.last
+
+
+def _report_words(rep) -> np.ndarray:
+    return np.array([rep[0], rep[1], np.float32(rep[2]).view(np.int32)], dtype=np.int32)
 
 
 @dataclass
@@ -47,6 +88,9 @@ class LiveResult:
     tokens: dict
     wall_s: float
     microbatches: int
+    monitor_updates: int = 0
+    stage_profiles: list | None = None   # the monitor's latest estimates
+    link_profiles: list | None = None
 
 
 class _Requests:
@@ -94,7 +138,7 @@ def _hop_comms(S: int) -> dict:
 
 
 def run_device_demo(cfg, cluster, stage_profiles, trace, *, decoder, seed: int = 0,
-                    timeout_s: float = 120.0) -> LiveResult | None:
+                    timeout_s: float = 120.0, monitor_epoch: int = 32) -> LiveResult | None:
     import torch.distributed as dist
 
     S = len(cfg.partition.stages)
@@ -116,21 +160,22 @@ def run_device_demo(cfg, cluster, stage_profiles, trace, *, decoder, seed: int =
     comms = _hop_comms(S)
     comm_ret = comms.get(S - 1)  # the return hop: tail and head only
     if rank == S - 1:
-        _tail(be, exe, comms[S - 2], comm_ret, cfg, policy, timeout_s)
+        _tail(be, exe, comms[S - 2], comm_ret, cfg, policy, timeout_s, S)
         return None
     if rank > 0:
-        _middle(exe, comms[rank - 1], comms[rank], cfg, policy, timeout_s)
+        _middle(exe, comms[rank - 1], comms[rank], cfg, policy, timeout_s, S, rank)
         return None
     return _head(be, exe, comms[0], comm_ret, cfg, policy, requests, trace, stage_profiles,
-                 link_profiles, bytes_per_token, timeout_s, dev)
+                 link_profiles, bytes_per_token, timeout_s, dev, S, monitor_epoch)
 
 
-def _tail(be, exe, comm_fwd, comm_ret, cfg, policy, timeout_s):
+def _tail(be, exe, comm_fwd, comm_ret, cfg, policy, timeout_s, S):
     # return link: this rank created it, so it is comm-rank 0 and the head is peer 1
     ret = DeviceLinkSender(comm_ret, 1, cfg.chunk_size, policy, "ret-sender", exe.device)
     ret.start()
     stream = exe.stream
-    d = exe.spec.d
+    HDR = hdr_words(S)
+    clock = _FwdClock()
 
     def on_payload(p):
         hdr = p.body[: HDR * 4].view(torch.int32).cpu().numpy()
@@ -141,13 +186,20 @@ def _tail(be, exe, comm_fwd, comm_ret, cfg, policy, timeout_s):
             stream.wait_stream(torch.cuda.current_stream())
             exe.meta_dev[:meta_len].view(torch.uint8).copy_(meta_b)
             exe.hidden[slot][:T].view(torch.uint8).reshape(-1).copy_(hid_b)
+        a = clock.start(stream)
         exe.forward(slot, T, R, phase == 1, max_seqlen, max_ctx)
+        clock.stop(a, stream, phase, T)
+        # [ids | every stage's report]: the head's monitor reads the trailer
+        reports = hdr[HDR0:HDR].copy()
+        reports[3 * (S - 1): 3 * S] = _report_words(clock.report())
+        trailer = torch.from_numpy(reports.view(np.int64) if reports.size % 2 == 0 else
+                                   np.concatenate([reports, np.zeros(1, np.int32)]).view(np.int64))
         with torch.cuda.stream(stream):
-            ids = exe.out_ids[slot][:R].clone()  # the slot's out_ids are reused later
+            ids = torch.cat([exe.out_ids[slot][:R], trailer.to(exe.device, non_blocking=False)])
         ev = torch.cuda.Event()
         ev.record(stream)
         fb = pipelink.Payload(id=p.payload_id, phase_class=PayloadClass.DECODE,
-                              size_bytes=8 * R, micro_batch_id=p.payload_id, enqueue_time=0)
+                              size_bytes=ids.numel() * 8, micro_batch_id=p.payload_id, enqueue_time=0)
         ret.send(fb, ids, ready=ev)
 
     recv = DeviceLinkReceiver(comm_fwd, 0, on_payload, "tail-recv", exe.device)
@@ -158,12 +210,14 @@ def _tail(be, exe, comm_fwd, comm_ret, cfg, policy, timeout_s):
         raise pipelink.ProtocolError(f"tail receiver failed: {recv.error!r}")
 
 
-def _middle(exe, comm_in, comm_out, cfg, policy, timeout_s):
+def _middle(exe, comm_in, comm_out, cfg, policy, timeout_s, S, rank):
     """A stage between head and tail: receive [header | metadata | residual stream],
     run the stage forward in place, pass the same framing on to the next rank."""
     nxt = DeviceLinkSender(comm_out, 1, cfg.chunk_size, policy, "mid-sender", exe.device)
     nxt.start()
     stream = exe.stream
+    HDR = hdr_words(S)
+    clock = _FwdClock()
 
     def on_payload(p):
         hdr = p.body[: HDR * 4].view(torch.int32).cpu().numpy()
@@ -173,9 +227,14 @@ def _middle(exe, comm_in, comm_out, cfg, policy, timeout_s):
             stream.wait_stream(torch.cuda.current_stream())
             exe.meta_dev[:meta_len].view(torch.uint8).copy_(p.body[HDR * 4: off])
             exe.hidden[slot][:T].view(torch.uint8).reshape(-1).copy_(p.body[off:])
+        a = clock.start(stream)
         exe.forward(slot, T, R, phase == 1, max_seqlen, max_ctx)
+        clock.stop(a, stream, phase, T)
+        rep_w = torch.from_numpy(_report_words(clock.report()).view(np.uint8))
         with torch.cuda.stream(stream):
             p.body[off:].copy_(exe.hidden[slot][:T].view(torch.uint8).reshape(-1))  # reuse the frame
+            o = (HDR0 + 3 * rank) * 4
+            p.body[o: o + 12].copy_(rep_w.to(exe.device))
         ev = torch.cuda.Event()
         ev.record(stream)
         out = pipelink.Payload(id=p.payload_id, phase_class=p.phase_class, size_bytes=p.body.numel(),
@@ -191,7 +250,13 @@ def _middle(exe, comm_in, comm_out, cfg, policy, timeout_s):
 
 
 def _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profiles, link_profiles,
-          bytes_per_token, timeout_s, dev):
+          bytes_per_token, timeout_s, dev, S, monitor_epoch):
+    from .monitor import RuntimeMonitor
+
+    monitor = RuntimeMonitor(stage_profiles, link_profiles, epoch=max(1, monitor_epoch))
+    HDR = hdr_words(S)
+    clock = _FwdClock()
+    sent_at: dict = {}
     fwd = DeviceLinkSender(comm_fwd, 1, cfg.chunk_size, policy, "fwd-sender", dev)
     feedback: queue.Queue = queue.Queue()
     head_recv = DeviceLinkReceiver(comm_ret, 0, feedback.put, "head-recv", dev)  # tail = comm-rank 0
@@ -208,11 +273,24 @@ def _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profi
     scatter_stream = torch.cuda.Stream(dev)
 
     def apply_feedback(p) -> int:
+        nonlocal stage_profiles, link_profiles
         mb = payload_mb.pop(p.payload_id)
         in_flight.pop(mb.id)
         rec = be.mbs[mb.id]
-        ids = p.body.view(torch.int64)
+        ids = p.body.view(torch.int64)[: rec.R]
         be._scatter(rec, ids, scatter_stream)
+        if monitor_epoch > 0:
+            rtt = time.perf_counter() - sent_at.pop(mb.id)
+            words = p.body.view(torch.int64)[rec.R:].cpu().numpy().view(np.int32)[: 3 * S]
+            compute = 0.0
+            for s in range(S):
+                ph, T, ms = int(words[3 * s]), int(words[3 * s + 1]), float(words[3 * s + 2:3 * s + 3].view(np.float32)[0])
+                if T > 0:
+                    monitor.stage_sample(s, Phase.DECODE if ph == 1 else Phase.PREFILL, T, ms / 1e3)
+                    compute += ms / 1e3
+            monitor.round_trip(rec.T * bytes_per_token, rtt, compute)
+            if monitor.tick():
+                stage_profiles, link_profiles = monitor.stage_profiles, monitor.link_profiles
         done = 0
         for rid in mb.request_ids:
             r = requests[rid]
@@ -254,9 +332,12 @@ def _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profi
                                 requests[rid].state = RequestState.PREFILL
                         in_flight[mb.id] = mb
                         be.admit(mb, 0)
+                        a = clock.start(exe.stream)
                         be.compute(0, mb, 0)
                         rec = be.mbs[mb.id]
-                        body = _forward_body(exe, rec, dev)
+                        clock.stop(a, exe.stream, 1 if rec.decode else 0, rec.T)
+                        body = _forward_body(exe, rec, dev, HDR, clock.report())
+                        sent_at[mb.id] = time.perf_counter()
                         pclass = PayloadClass.DECODE if mb.phase is BatchPhase.DECODE else PayloadClass.PREFILL
                         payload = pipelink.Payload(id=next_payload, phase_class=pclass,
                                                    size_bytes=body.numel(), micro_batch_id=mb.id,
@@ -278,14 +359,18 @@ def _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profi
     gen = be.gen_tokens.cpu().numpy()
     toks = {rid: gen[be.rid_index[rid], : r.tokens_emitted].copy() for rid, r in requests.items()}
     return LiveResult(tokens_by_request={rid: requests[rid].tokens_emitted for rid in sorted(requests)},
-                      tokens=toks, wall_s=time.perf_counter() - t0, microbatches=n_mbs)
+                      tokens=toks, wall_s=time.perf_counter() - t0, microbatches=n_mbs,
+                      monitor_updates=monitor.updates, stage_profiles=monitor.stage_profiles,
+                      link_profiles=monitor.link_profiles)
 
 
-def _forward_body(exe, rec, dev) -> torch.Tensor:
-    """[int32 header | int32 metadata | bf16 residual stream] of one micro-batch (device)."""
+def _forward_body(exe, rec, dev, HDR, report) -> torch.Tensor:
+    """[int32 header (+ per-stage reports) | int32 metadata | bf16 residual stream] of one
+    micro-batch (device); the head's own report goes into stage slot 0."""
     meta = rec.meta
-    hdr = np.array([rec.T, rec.R, 1 if rec.decode else 0, rec.max_seqlen, rec.max_ctx, rec.slot,
-                    meta.size, 0], dtype=np.int32)
+    hdr = np.zeros(HDR, dtype=np.int32)
+    hdr[:HDR0] = [rec.T, rec.R, 1 if rec.decode else 0, rec.max_seqlen, rec.max_ctx, rec.slot, meta.size, 0]
+    hdr[HDR0:HDR0 + 3] = _report_words(report)
     prefix = np.concatenate([hdr, meta]).view(np.uint8)
     hid_bytes = rec.T * exe.spec.d * 2
     body = torch.empty(prefix.size + hid_bytes, dtype=torch.uint8, device=dev)

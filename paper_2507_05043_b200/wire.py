@@ -210,3 +210,78 @@ class DeviceLinkReceiver(threading.Thread):
                 self._stream.synchronize()
                 phase = PayloadClass.DECODE if flags & FLAG_DECODE else PayloadClass.PREFILL
                 self._on_payload(ReceivedDevicePayload(pid, phase, body))
+
+
+# ------------------------------------------------------------ cross-host hops
+# A pipeline spanning boxes (the paper's deployment: consumer GPUs over the Internet,
+# PAPER.md:50) crosses hosts on TCP.  These wrap the reference's own socket backend
+# unchanged -- its framing (u32 length + <QII> payload id / chunk index / flags header +
+# body, wire.py:3-15, 28-65), LinkQueue draining and reassembly (wire.py:75-185) --
+# and add only the device staging at both ends: one device-to-pinned-host copy when
+# the producing forward is done, one host-to-device copy of the reassembled payload.
+
+def _ref_wire():
+    import importlib
+
+    return importlib.import_module("pipelink.wire")
+
+
+class HostBridgeLinkSender:
+    """``SocketLinkSender`` for a device payload (same contract: start / send / close /
+    join; ``send`` raises ProtocolError on a size mismatch or while closing)."""
+
+    def __init__(self, sock, chunk_size, policy=LinkPolicy.DECODE_PRIORITY, name: str = "host-link-sender"):
+        self._inner = _ref_wire().SocketLinkSender(sock, chunk_size, policy, name)
+
+    def start(self) -> None:
+        self._inner.start()
+
+    def send(self, payload, body: torch.Tensor, ready: torch.cuda.Event | None = None) -> None:
+        if body.numel() * body.element_size() != payload.size_bytes:
+            raise ProtocolError(f"payload {payload.id}: body is {body.numel() * body.element_size()} bytes, "
+                                f"declared {payload.size_bytes}")
+        flat = body.reshape(-1).view(torch.uint8)
+        if flat.is_cuda:
+            host = torch.empty(flat.numel(), dtype=torch.uint8, pin_memory=True)
+            st = torch.cuda.current_stream(flat.device)
+            if ready is not None:
+                st.wait_event(ready)
+            host.copy_(flat, non_blocking=True)
+            st.synchronize()
+        else:
+            host = flat
+        self._inner.send(payload, host.numpy().tobytes())
+
+    def close(self) -> None:
+        self._inner.close()
+
+    def join(self, timeout: float | None = None) -> None:
+        self._inner.join(timeout)
+
+
+class HostBridgeLinkReceiver:
+    """``SocketLinkReceiver`` delivering ``ReceivedDevicePayload`` (body on `device`)."""
+
+    def __init__(self, sock, on_payload, name: str = "host-link-receiver", device=None):
+        self.device = torch.device(device) if device is not None else torch.device("cpu")
+
+        def deliver(p):
+            body = torch.frombuffer(bytearray(p.body), dtype=torch.uint8)
+            if self.device.type == "cuda":
+                body = body.pin_memory().to(self.device, non_blocking=False)
+            on_payload(ReceivedDevicePayload(p.payload_id, p.phase_class, body))
+
+        self._inner = _ref_wire().SocketLinkReceiver(sock, deliver, name)
+
+    @property
+    def failed(self) -> bool:
+        return self._inner.failed
+
+    def start(self) -> None:
+        self._inner.start()
+
+    def run(self) -> None:
+        self._inner.run()
+
+    def join(self, timeout: float | None = None) -> None:
+        self._inner.join(timeout)

@@ -4,7 +4,9 @@
 
 Criterion-11 analog (test_acceptance.py:367-381): per-request token counts of the
 live run equal the virtual run's; additionally the generated ids equal the CPU
-oracle's (margin-engineered init).  Exit code 0 = parity holds.
+oracle's (margin-engineered init).  The head's RuntimeMonitor rebuilds the stage /
+link profiles every 8 micro-batches from measured forwards and round trips; the
+profiles it ended with are printed.  Exit code 0 = parity holds.
 """
 
 import os
@@ -37,7 +39,7 @@ def main():
                                chunk_size=4096)
     trace = PL.Trace(requests=[PL.Request(i, 0.0, 40 + 7 * i, 6 + (i % 5)) for i in range(20)])
     profiles = [PL.synth_profile(hi - lo, 1e-6, 2e-5, stage_id=i) for i, (_, (lo, hi)) in enumerate(plan.stages)]
-    res = run_device_demo(cfg, cluster, profiles, trace, decoder=spec)
+    res = run_device_demo(cfg, cluster, profiles, trace, decoder=spec, monitor_epoch=8)
     ok = True
     if dist.get_rank() == 0:
         virtual = PL.PipelineEngine(cfg, cluster, profiles).run(trace)
@@ -53,6 +55,12 @@ def main():
         print(f"live {S}-stage NVLink run: {res.microbatches} micro-batches in {res.wall_s:.2f} s; "
               f"token counts {'==' if counts_ok else '!='} virtual; "
               f"{len(trace.requests) - bad}/{len(trace.requests)} requests identical to the oracle", flush=True)
+        # runtime monitoring: the profiles the head ended with (measured on the device clock)
+        dec = {s: [(t, round(sec * 1e6, 1)) for t, sec in p.points(PL.Phase.DECODE)]
+               for s, p in enumerate(res.stage_profiles)}
+        links = [(lp.name, round(lp.latency_s * 1e6, 1), round(lp.bandwidth_bps / 1e9, 1)) for lp in res.link_profiles]
+        print(f"monitor: {res.monitor_updates} profile updates; decode points (tokens, us) {dec}; "
+              f"links (us, GB/s) {links}", flush=True)
         ok = counts_ok and bad == 0
     t = torch.tensor([0 if ok else 1])
     dist.all_reduce(t)

@@ -40,9 +40,7 @@ def main():
     from paper_2507_05043_b200.backend import local_device_index
 
     torch.cuda.set_device(local_device_index())
-    # PL_OVERSUBSCRIBE_GPUS (two ranks per GPU): torch collectives on gloo only, since an
-    # NCCL world communicator rejects duplicate GPUs (the hop links are two-rank comms)
-    dist.init_process_group(backend="gloo" if os.environ.get("PL_OVERSUBSCRIBE_GPUS") else "cuda:nccl,cpu:gloo")
+    dist.init_process_group(backend="cuda:nccl,cpu:gloo")
 
     from paper_2507_05043_b200 import LLAMA3_8B, TINY, deploy
     from paper_2507_05043_b200.engine import B200PipelineEngine
