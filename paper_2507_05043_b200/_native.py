@@ -90,6 +90,7 @@ _SIGS = {
     "pl_gemm_packed": (i32, [vp, i64, vp, vp, vp, i64, vp, i64, i64, i64, i64, i32, vp, i64, vp, vp]),
     "pl_rope_kv_write": (i32, [vp, i64, vp, vp, vp, i32, vp, vp, i32, i64, i32, i32, i32, vp]),
     "pl_attn_prefill": (i32, [vp, i64, vp, i32, i32, i32, i32, i32, f32, vp, i64, vp]),
+    "pl_attn_prefill_ex": (i32, [vp, i64, i64, vp, i32, i32, i32, i32, i32, f32, vp, i64, i32, vp]),
     "pl_attn_decode_workspace_bytes": (i64, [i32, i32, i32, i32]),
     "pl_attn_decode": (i32, [vp, i64, vp, vp, i64, i32, vp, i32, vp, i32, i32, i32, i32, i32, f32, vp, i64, vp, i64, vp]),
     "pl_lmhead_workspace_bytes": (i64, [i32, i64]),

@@ -123,7 +123,7 @@ class GpuBackend(Backend):
         self.record_links = False   # per-chunk CUDA events -> realized link log (device clock)
         # native runtime: decode payloads between stages of this process are stored by the
         # producer's last residual epilogue straight into the next stage's buffer
-        self.fuse_transport = True
+        self.fuse_transport = False  # opt-in: measured slower across GPUs
         self.S = placement.n_stages
         self.layer_ranges = [rng for _, rng in cfg.partition.stages]
         self.n_slots = cfg.controller.effective_n_max(self.S)

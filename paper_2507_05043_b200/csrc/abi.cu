@@ -78,6 +78,7 @@ int32_t pl_preload_kernels(void) {
   if (!rc) rc = kernels_preload();
   if (!rc) rc = transport_preload();
   if (!rc) rc = chain_preload();
+  if (!rc) rc = attn_tc_preload();
   return rc;
 }
 
@@ -164,6 +165,15 @@ int32_t pl_attn_prefill(const void* qkv, int64_t ldqkv, const int32_t* cu_seqlen
   if (!qkv || !cu_seqlens || !out) return set_error(PL_ERR_CONFIG, "attn_prefill: null argument");
   return attn_prefill_launch(B(qkv), ldqkv, cu_seqlens, R, max_seqlen, Hq, Hkv, hd, scale, BM_(out),
                              ldo, S(stream));
+}
+
+int32_t pl_attn_prefill_ex(const void* qkv, int64_t ldqkv, int64_t rows, const int32_t* cu_seqlens, int32_t R,
+                           int32_t max_seqlen, int32_t Hq, int32_t Hkv, int32_t hd, float scale, void* out,
+                           int64_t ldo, int32_t impl, void* stream) {
+  if (!qkv || !cu_seqlens || !out) return set_error(PL_ERR_CONFIG, "attn_prefill: null argument");
+  if (impl < 0 || impl > 2) return set_error(PL_ERR_CONFIG, "attn_prefill: impl must be 0, 1 or 2");
+  return attn_prefill_launch(B(qkv), ldqkv, cu_seqlens, R, max_seqlen, Hq, Hkv, hd, scale, BM_(out),
+                             ldo, S(stream), rows, impl);
 }
 
 int64_t pl_attn_decode_workspace_bytes(int32_t R, int32_t Hq, int32_t max_ctx, int32_t hd) {

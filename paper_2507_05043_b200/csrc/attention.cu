@@ -247,12 +247,25 @@ __global__ void __launch_bounds__(PF_THREADS, 2)
   }
 }
 
+// Which prefill kernel: 1 = mma.sync (this file), 2 = tcgen05 (attn_tc.cu), 0 = by
+// PL_ATTN_TC (0 / 1); tcgen05 needs the qkv row count (its TMA maps).
+int attn_prefill_impl(int impl, int64_t rows) {
+  static const int env = [] { const char* v = getenv("PL_ATTN_TC"); return v ? atoi(v) : -1; }();
+  if (impl == 0) impl = env == 1 ? 2 : 1;
+  return impl == 2 && rows > 0 ? 2 : 1;
+}
+
 int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* cu_seqlens, int R,
                         int max_seqlen, int Hq, int Hkv, int hd, float scale, __nv_bfloat16* out,
-                        int64_t ldo, cudaStream_t st) {
+                        int64_t ldo, cudaStream_t st, int64_t rows, int impl) {
   if (R <= 0 || max_seqlen <= 0) return PL_OK;
   if (hd != HD) return set_error(PL_ERR_CONFIG, "attention: head_dim must be 128 (got %d)", hd);
   if (Hkv <= 0 || Hq % Hkv) return set_error(PL_ERR_CONFIG, "attention: Hq must be a multiple of Hkv");
+  if (attn_prefill_impl(impl, rows) == 2) {
+    if (ldqkv % 8 || ldo % 8) return set_error(PL_ERR_CONFIG, "attention: leading dims % 8");
+    return attn_prefill_tc_launch(qkv, ldqkv, rows, cu_seqlens, R, max_seqlen, Hq, Hkv, scale * LOG2E, out,
+                                  ldo, st);
+  }
   const int G = Hq / Hkv;
   if (G > 8 || PF_ROWS % (16 * G))
     return set_error(PL_ERR_CONFIG, "attention prefill: GQA group %d unsupported (1, 2, 4, 8)", G);

@@ -189,9 +189,16 @@ int chain_launch(const ChainLaunch& c, cudaStream_t st);
 int chain_preload();
 
 // attention.cu
+// rows = qkv rows (> 0 enables the tcgen05 kernel, whose TMA maps need the extent);
+// impl 0 auto, 1 mma.sync, 2 tcgen05
 int attn_prefill_launch(const __nv_bfloat16* qkv, int64_t ldqkv, const int32_t* cu_seqlens, int R,
                         int max_seqlen, int Hq, int Hkv, int hd, float scale, __nv_bfloat16* out,
-                        int64_t ldo, cudaStream_t st);
+                        int64_t ldo, cudaStream_t st, int64_t rows = 0, int impl = 0);
+// attn_tc.cu
+int attn_prefill_tc_launch(const __nv_bfloat16* qkv, int64_t ldqkv, int64_t rows, const int32_t* cu_seqlens,
+                           int R, int max_seqlen, int Hq, int Hkv, float scale_log2, __nv_bfloat16* out,
+                           int64_t ldo, cudaStream_t st);
+int attn_tc_preload();
 int64_t attn_decode_workspace_bytes(int R, int Hq, int max_ctx, int hd);
 int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16* k_cache,
                        const __nv_bfloat16* v_cache, int64_t num_blocks, int block_size,

@@ -548,7 +548,7 @@ struct Stage {
       }
       if (Rp > 0) {  // causal attention over the prompt rows (cu_seqlens are absolute rows)
         rc = attn_prefill_launch(qkv, qkv_dim, cu + Rd, Rp, mb.max_seqlen, c.Hq, c.Hkv, c.hd, scale, o,
-                                 attn_dim, st);
+                                 attn_dim, st, T);
         if (rc) return rc;
       }
       mark(2);

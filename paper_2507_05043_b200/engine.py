@@ -21,9 +21,10 @@ in C++ (csrc/runtime.cu); ``native=False`` runs the Python twin
 schedule and tokens.  Extra keywords: ``throttle=True`` replays the virtual
 link timing on the GPU clock; ``prompts={rid: ids}`` overrides the synthetic
 prompts; ``devices=[...]`` spreads stages over local GPUs without torchrun;
-``fuse_transport`` (default on, native runtime) stores decode payloads between
+``fuse_transport`` (opt-in, native runtime) stores decode payloads between
 stages of this process from the producer's last residual epilogue straight into
-the next stage's buffer over NVLink peer memory instead of a link copy.
+the next stage's buffer over NVLink peer memory instead of a link copy (measured
+slower across GPUs: the producer then waits on the consumer's slot).
 """
 
 from __future__ import annotations
@@ -141,7 +142,7 @@ class B200PipelineEngine(PipelineDriver):
 
     def __init__(self, cfg, cluster, stage_profiles, *, decoder: DecoderSpec, seed: int = 0,
                  devices: list | None = None, prompts: dict | None = None, throttle: bool = False,
-                 native: bool = True, fuse_transport: bool = True):
+                 native: bool = True, fuse_transport: bool = False):
         if cfg.model.hidden_dim != decoder.d or cfg.model.dtype_bytes != 2:
             raise pipelink.ConfigError("cfg.model must describe the decoder's bf16 residual stream "
                                        "(use DecoderSpec.model_spec())")
@@ -209,14 +210,16 @@ class B200PipelineEngine(PipelineDriver):
         """The run re-expressed on the device clock as a reference RunResult, so the
         unchanged summarize() / measure_bubble() (metrics.py:78-117, engine.py:130-144)
         report measured TTFT/TPOT/throughput/bubbles.  Stage intervals cover this
-        rank's stages; token times exist on the head rank."""
+        rank's stages; token times exist on the head rank.  The device replay does not
+        pace arrivals, so a request "arrives" on the device clock when its first
+        micro-batch starts on stage 0: device TTFT is dispatch to first token."""
         g = self.gpu
         S = len(self.stage_profiles)
         busy = [[(a, b) for _, a, b in g.busy_real_ns.get(s, [])] for s in range(S)]
         first_compute = {}
         for mb_id, a, _ in g.busy_real_ns.get(0, []):
             for rid in g.mb_requests.get(mb_id, ()):
-                first_compute.setdefault(rid, a)
+                first_compute[rid] = min(a, first_compute.get(rid, a))
         emissions = []
         reqs = []
         times = {}
@@ -227,7 +230,7 @@ class B200PipelineEngine(PipelineDriver):
                     times.setdefault(rid, []).append(t)
         for r in virtual.requests:
             c = r.fresh_copy()
-            c.arrival_time = r.arrival_time
+            c.arrival_time = first_compute[r.id] / 1e9 if r.id in first_compute else r.arrival_time
             c.state, c.tokens_emitted = r.state, r.tokens_emitted
             ts = times.get(r.id)
             if ts:

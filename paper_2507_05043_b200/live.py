@@ -281,7 +281,8 @@ def _head(be, exe, comm_fwd, comm_ret, cfg, policy, requests, trace, stage_profi
         be._scatter(rec, ids, scatter_stream)
         if monitor_epoch > 0:
             rtt = time.perf_counter() - sent_at.pop(mb.id)
-            words = p.body.view(torch.int64)[rec.R:].cpu().numpy().view(np.int32)[: 3 * S]
+            with torch.cuda.stream(scatter_stream):  # never the legacy default stream
+                words = p.body.view(torch.int64)[rec.R:].cpu().numpy().view(np.int32)[: 3 * S]
             compute = 0.0
             for s in range(S):
                 ph, T, ms = int(words[3 * s]), int(words[3 * s + 1]), float(words[3 * s + 2:3 * s + 3].view(np.float32)[0])

@@ -145,13 +145,14 @@ def rope_kv_write(qkv: torch.Tensor, pos: torch.Tensor, slot: torch.Tensor | Non
 
 
 def attn_prefill(qkv: torch.Tensor, cu_seqlens: torch.Tensor, max_seqlen: int, Hq: int, Hkv: int,
-                 hd: int, out: torch.Tensor | None = None) -> torch.Tensor:
+                 hd: int, out: torch.Tensor | None = None, impl: int = 0) -> torch.Tensor:
+    """impl: 0 default (tcgen05), 1 mma.sync, 2 tcgen05."""
     _need_cuda(qkv, cu_seqlens)
     T = qkv.shape[0]
     out = out if out is not None else torch.empty(T, Hq * hd, dtype=BF16, device=qkv.device)
     R = cu_seqlens.numel() - 1
-    N.call("pl_attn_prefill", _ptr(qkv), qkv.stride(0), _ptr(cu_seqlens), R, max_seqlen, Hq, Hkv,
-           hd, float(hd ** -0.5), _ptr(out), out.stride(0), _stream())
+    N.call("pl_attn_prefill_ex", _ptr(qkv), qkv.stride(0), T, _ptr(cu_seqlens), R, max_seqlen, Hq, Hkv,
+           hd, float(hd ** -0.5), _ptr(out), out.stride(0), impl, _stream())
     return out
 
 

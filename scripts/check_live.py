@@ -23,7 +23,7 @@ def main():
 
     import faulthandler
 
-    faulthandler.dump_traceback_later(150, exit=True)  # a hang prints every thread's stack
+    faulthandler.dump_traceback_later(150, exit=True, file=sys.stdout)  # a hang prints every thread's stack
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     dist.init_process_group(backend="cuda:nccl,cpu:gloo")
     from paper_2507_05043_b200 import TINY, deploy

@@ -64,7 +64,7 @@ def main():
     ap.add_argument("--prompt", type=int, default=512)
     ap.add_argument("--decode", type=int, default=256)
     ap.add_argument("--no-links", action="store_true", help="skip the realized link log")
-    ap.add_argument("--no-fuse", action="store_true", help="copy decode payloads on the link streams")
+    ap.add_argument("--fuse", action="store_true", help="store decode payloads from the producer's epilogue")
     a = ap.parse_args()
 
     import torch
@@ -89,7 +89,7 @@ def main():
     placeholder = [PL.synth_profile(hi - lo, 1e-6, 1e-4, stage_id=i) for i, (_, (lo, hi)) in enumerate(plan.stages)]
     t0 = time.time()
     eng = B200PipelineEngine(cfg, cluster, placeholder, decoder=spec, devices=devices,
-                             fuse_transport=not a.no_fuse)
+                             fuse_transport=a.fuse)
     eng.prepare(trace)
     eng.set_stage_profiles([profile_stage(eng.gpu.exe[s], ctx=a.prompt) for s in range(S)])
     warm = PL.Trace(requests=[PL.Request(r.id, 0.0, min(r.input_len, 256), 2) for r in trace.requests[:4]])
@@ -120,7 +120,7 @@ def main():
     bubbles = [round(PL.measure_bubble(st.real, s, 0.0, st.real.end_ns / 1e9), 4) for s in range(S)]
     out = {"workload": f"{spec.name} {S}-stage pipeline on {G} GPU(s), one process, {a.batch} requests "
                        f"{a.prompt}/{a.decode}",
-           "stage_gpu": stage_gpu, "fused_transport": not a.no_fuse,
+           "stage_gpu": stage_gpu, "fused_transport": a.fuse,
            "device_tok_s": round(st.throughput_tok_s, 1),
            "decode_window_tok_s": round(window, 1) if window else None,
            "tpot_p50_ms": round(1e3 * (st.tpot_p50_s() or 0), 3), "ttft_p50_ms": round(1e3 * (st.ttft_p50_s() or 0), 2),

@@ -181,15 +181,17 @@ def test_rope_kv_bit_exact(ops):
         assert torch.equal(vc[b, :, o], x[t, Hq + Hkv:])
 
 
+@pytest.mark.parametrize("impl", [1, 2], ids=["mma_sync", "tcgen05"])
 @pytest.mark.parametrize("lens,Hq,Hkv", [([128] * 8, 2, 1), ([1, 63, 64, 65, 200], 4, 2),
-                                         ([512, 512], 32, 8), ([2048], 8, 1)])
-def test_attn_prefill(ops, lens, Hq, Hkv):
+                                         ([512, 512], 32, 8), ([2048], 8, 1), ([300, 1, 129, 700], 8, 8),
+                                         ([1000, 24], 64, 8)])
+def test_attn_prefill(ops, lens, Hq, Hkv, impl):
     hd = 128
     T = sum(lens)
     g = torch.Generator().manual_seed(sum(lens) + Hq)
     qkv = torch.randn(T, (Hq + 2 * Hkv) * hd, generator=g).to(BF16)
     cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
-    out = ops.attn_prefill(qkv.to(dev()), cu.to(dev()), max(lens), Hq, Hkv, hd).cpu()
+    out = ops.attn_prefill(qkv.to(dev()), cu.to(dev()), max(lens), Hq, Hkv, hd, impl=impl).cpu()
     x = qkv.reshape(T, Hq + 2 * Hkv, hd)
     refs = []
     for r, n in enumerate(lens):

@@ -39,7 +39,7 @@ def torchrun(script, *args, nproc=2, timeout=600, gpus=None, env=None):
            *args]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout,
                        env={**os.environ, "PYTHONPATH": str(ROOT), **(env or {})})
-    assert p.returncode == 0, p.stdout[-6000:] + p.stderr[-2000:]
+    assert p.returncode == 0, p.stdout[-20000:] + p.stderr[-4000:]
     return p.stdout
 
 
