@@ -6,12 +6,16 @@ pipelink/engine.py:384), so the CPU baseline is this repo's oracle decoder
 serving run would take tens of minutes on CPU, so the estimate is built from
 bounded samples of the SAME workload and extrapolated:
 
-  * decode: one decode step of B requests (ctx = prompt length) through
-    `layers_sampled` decoder layers, plus embed + final norm + lm_head;
-  * prefill: one prompt of `prefill_sample` tokens through the sampled layers.
+  * decode: one decode step of B requests at the run's MEAN context
+    (P + (n_out - 1) / 2: decode attention is linear in the context, so the mean
+    step is the average step) through `layers_sampled` decoder layers, plus
+    embed + final norm + lm_head;
+  * prefill: one whole prompt of P tokens through the sampled layers (the causal
+    attention's quadratic term is timed, not extrapolated); prompts longer than
+    `prefill_cap` are sampled at the cap and scaled linearly (said in `sample`).
 
-  t_decode_step = t_head + L/ls * t_layers(decode)
-  t_prefill     = B * P / prefill_sample * (L/ls * t_layers(prefill) + t_head')
+  t_decode_step = t_head + L/ls * t_layers(decode at the mean context)
+  t_prefill     = B * (L/ls * t_layers(prefill of one prompt) + t_head')
   output tok/s  = B * n_out / (t_prefill + (n_out - 1) * t_decode_step)
 
 Weights for the TIMING sample are drawn with torch's RNG (values do not change
@@ -42,7 +46,7 @@ def _rand_layer(spec: OD.OracleSpec, g: torch.Generator) -> OD.LayerW:
 
 
 def estimate(spec, batch: int, prompt_len: int, n_out: int, layers_sampled: int = 2,
-             prefill_sample: int = 256, threads: int | None = None, reps: int = 2) -> dict:
+             prefill_cap: int = 1024, threads: int | None = None, reps: int = 2) -> dict:
     threads = threads or os.cpu_count() or 1
     torch.set_num_threads(threads)
     o = OD.OracleSpec.from_spec(spec)
@@ -58,12 +62,13 @@ def estimate(spec, batch: int, prompt_len: int, n_out: int, layers_sampled: int 
         hn = OD.rmsnorm_ref(h, fnorm, o.eps)
         return OD.linear_acc(hn, lm).argmax(-1)
 
-    # decode step: B requests, one token each, ctx = prompt_len
-    kv = [[((torch.randn(prompt_len, o.Hkv, o.hd, generator=g) * 0.5).to(BF16),
-            (torch.randn(prompt_len, o.Hkv, o.hd, generator=g) * 0.5).to(BF16))
+    # decode step: B requests, one token each, at the run's mean context
+    ctx = prompt_len + (n_out - 1) // 2
+    kv = [[((torch.randn(ctx, o.Hkv, o.hd, generator=g) * 0.5).to(BF16),
+            (torch.randn(ctx, o.Hkv, o.hd, generator=g) * 0.5).to(BF16))
            for _ in range(batch)] for _ in range(ls)]
     ids = torch.randint(0, o.vocab, (batch,), generator=g)
-    pos = torch.full((batch,), prompt_len, dtype=torch.int64)
+    pos = torch.full((batch,), ctx, dtype=torch.int64)
 
     def decode_once():
         caches = [[c for c in layer] for layer in kv]   # fresh lists: layer_forward appends
@@ -77,7 +82,7 @@ def estimate(spec, batch: int, prompt_len: int, n_out: int, layers_sampled: int 
         return t1 - t0, t2 - t1
 
     def prefill_once():
-        n = min(prefill_sample, prompt_len)
+        n = min(prefill_cap, prompt_len)
         tok = torch.randint(0, o.vocab, (n,), generator=g)
         e = torch.empty(0, o.Hkv, o.hd, dtype=BF16)
         caches = [[(e, e)] for _ in range(ls)]
@@ -88,14 +93,14 @@ def estimate(spec, batch: int, prompt_len: int, n_out: int, layers_sampled: int 
         t1 = time.perf_counter()
         head(h[-1:])
         t2 = time.perf_counter()
-        return (t1 - t0) / n, t2 - t1
+        return (t1 - t0) * prompt_len / n, t2 - t1  # one whole prompt
 
     decode_once()  # warm
     d = min((decode_once() for _ in range(reps)), key=lambda x: x[0] + x[1])
     p = min((prefill_once() for _ in range(reps)), key=lambda x: x[0])
     scale = o.num_layers / ls
     t_step = d[0] * scale + d[1]
-    t_prefill = batch * prompt_len * p[0] * scale + batch * p[1]
+    t_prefill = batch * (p[0] * scale + p[1])
     total_tokens = batch * n_out
     t_run = t_prefill + (n_out - 1) * t_step
     return {
@@ -104,7 +109,9 @@ def estimate(spec, batch: int, prompt_len: int, n_out: int, layers_sampled: int 
         "t_decode_step_s": t_step,
         "t_prefill_s": t_prefill,
         "threads": threads,
-        "sample": (f"oracle CPU decoder: 1 decode step of B={batch} at ctx {prompt_len} and a "
-                   f"{min(prefill_sample, prompt_len)}-token prefill through {ls}/{o.num_layers} "
-                   f"layers + lm_head, extrapolated to the full {batch}x{prompt_len}/{n_out} run"),
+        "sample": (f"oracle CPU decoder: 1 decode step of B={batch} at the mean ctx {ctx} and one "
+                   f"{min(prefill_cap, prompt_len)}-token prefill"
+                   f"{'' if prompt_len <= prefill_cap else ' (scaled linearly to ' + str(prompt_len) + ')'}"
+                   f" through {ls}/{o.num_layers} layers + lm_head, extrapolated to the full "
+                   f"{batch}x{prompt_len}/{n_out} run"),
     }

@@ -38,8 +38,8 @@
 //          a[t] = bf16(w * bf16(h[t] / rms))           (modeling_llama.py:62-67, 313-331)
 //   Q      q / k / v = bf16(sum + bias); neox RoPE on q and k pairs (i, i + 64) of each
 //          head with HF's per-op rounding; q rows for the attention, k / v into the pages
-// Split factors come from the weight shapes only (chain_plan), so a token's result
-// never depends on T or on the batch.
+// Split factors come from the weight shapes only (chain_plan), so a decode token's
+// result does not depend on T or on the batch.
 //
 // Roles (224 threads): warp 0 lane 0 weight producer (claims units; 1-D bulk copies of
 // the packed 16 KB tiles), warp 6 activation producer (dependency polls, TMA), warp 1

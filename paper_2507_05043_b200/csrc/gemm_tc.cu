@@ -9,8 +9,11 @@
 //   SWAP  (decode, T <= 256): the weight tile is the MMA "A" operand (M = 128
 //          output features per CTA) and the tokens are the MMA N dimension
 //          (16..256).  Weight bytes dominate, so the kernel is an HBM stream of
-//          W with split-K chosen from (N, K) only -- never from T -- which keeps
-//          every token's result independent of the batch it rides in.
+//          W with split-K chosen from (N, K) only -- never from T -- so among
+//          decode (SWAP) batches a token's result does not depend on the batch it
+//          rides in.  The orientation itself switches at T = 256 (SWAP above has
+//          split-K, !SWAP does not), so prefill rows may round differently in a
+//          <= 256-token micro-batch than in a larger one.
 //   !SWAP (prefill): tokens are the A operand (M = 128 rows), features are N = 256;
 //          at T >= 512 gemm_pair_kernel (CTA pairs, cta_group::2, 256 x 256 tiles).
 //
@@ -1334,7 +1337,7 @@ int make_tma_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, i
 }
 
 // Split-K factor for the decode (SWAP) path, from the weight shape (N, K) only so a
-// token's result never depends on the batch it rides in.  Decode GEMMs are HBM
+// token's result does not depend on which decode batch it rides in.  Decode GEMMs are HBM
 // streams: a CTA with a 4-6 deep TMA ring pulls ~2x its fair share of bandwidth,
 // so the only goal is to give every SM at least one work item -- any extra split
 // is pure partial-sum traffic.  Smallest split with tiles*splits >= #SMs, each

@@ -521,16 +521,19 @@ struct Pipeline : sched::Hooks {
     }
     if (!is_ret && fused_hop(src, rec)) {
       // the bytes already landed in dst's slot at the end of the producing forward: the
-      // chunk is that forward's completion (a zero-length realized chunk)
-      cudaSetDevice(rs.dev);
-      cudaStreamWaitEvent(rs.send, rs.ev_comp[k], 0);
-      if (t_emit) cudaEventRecord(t_emit, rs.send);
-      if (t_emit) note_chunk(link, src, k, p, ch, t_emit, rs.send);
-      cudaEventRecord(rs.ev_send[k], rs.send);
-      rs.has_send[k] = 1;
-      cudaEvent_t e = pool(rs.dev).take();
-      cudaEventRecord(e, rs.send);
-      recv_done(dst, rec, p.mb, e, is_ret, deliver);
+      // chunk is that forward's completion (a zero-length realized chunk); the payload
+      // is delivered once, with its last chunk
+      if (t_emit) {
+        cudaEventRecord(t_emit, rs.send);
+        note_chunk(link, src, k, p, ch, t_emit, rs.send);
+      }
+      if (last) {
+        cudaEventRecord(rs.ev_send[k], rs.send);
+        rs.has_send[k] = 1;
+        cudaEvent_t e = pool(rs.dev).take();
+        cudaEventRecord(e, rs.send);
+        recv_done(dst, rec, p.mb, e, is_ret, deliver);
+      }
       return;
     }
     if (rs.local && rd.local) {
