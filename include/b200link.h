@@ -125,7 +125,7 @@ PL_API int32_t pl_attn_prefill(const void* qkv, int64_t ldqkv, const int32_t* cu
                         int32_t max_seqlen, int32_t Hq, int32_t Hkv, int32_t hd, float scale,
                         void* out, int64_t ldo, void* stream);
 /* Same, with the qkv row count (the tcgen05 kernel's TMA maps need it) and the kernel:
- * impl 0 = default (PL_ATTN_TC=1 selects tcgen05), 1 = mma.sync FA2, 2 = tcgen05
+ * impl 0 = default (tcgen05; PL_ATTN_TC=0 selects mma.sync), 1 = mma.sync FA2, 2 = tcgen05
  * (FA4-style: S and O in TMEM, TMA-fed K / V ring; GQA groups 1, 2, 4, 8). */
 PL_API int32_t pl_attn_prefill_ex(const void* qkv, int64_t ldqkv, int64_t rows, const int32_t* cu_seqlens,
                            int32_t R, int32_t max_seqlen, int32_t Hq, int32_t Hkv, int32_t hd, float scale,

@@ -13,7 +13,7 @@
 //   the whole GQA group, so each KV page is read from HBM exactly once.  Pages
 //   arrive by TMA into 128-byte-swizzled shared memory (persistent CTAs, one TMA
 //   producer warp, four tensor-core consumer warps); a request's context is cut
-//   into ceil(pages/8) even splits, so the reduction order depends on its own
+//   into ceil(pages/16) even splits, so the reduction order depends on its own
 //   context length only, never on the batch.
 #include "common.cuh"
 #include "pl_internal.h"
@@ -248,10 +248,11 @@ __global__ void __launch_bounds__(PF_THREADS, 2)
 }
 
 // Which prefill kernel: 1 = mma.sync (this file), 2 = tcgen05 (attn_tc.cu), 0 = by
-// PL_ATTN_TC (0 / 1); tcgen05 needs the qkv row count (its TMA maps).
+// PL_ATTN_TC (default tcgen05; 0 selects mma.sync); tcgen05 needs the qkv row count
+// (its TMA maps), so a launch without it takes the mma.sync kernel.
 int attn_prefill_impl(int impl, int64_t rows) {
   static const int env = [] { const char* v = getenv("PL_ATTN_TC"); return v ? atoi(v) : -1; }();
-  if (impl == 0) impl = env == 1 ? 2 : 1;
+  if (impl == 0) impl = env == 0 ? 1 : 2;
   return impl == 2 && rows > 0 ? 2 : 1;
 }
 

@@ -1355,8 +1355,8 @@ int gemm_num_splits(int64_t N, int64_t K, bool swap) {
     if (tiles * best >= sms) break;
   }
   // Long-K projections (the down GEMMs, K >= 12288): round the split count up to a
-  // multiple of 4.  The residual+norm reduce loads partials in groups of 4, so this adds
-  // no reduction round, and the smaller per-CTA streams even out the SMs that carry two
+  // multiple of 4.  The residual+norm reduce loads partials in groups of 8 (VPT = 1) or 4,
+  // so this adds no reduction round, and the smaller per-CTA streams even out the SMs that carry two
   // CTAs (L3 down: 5 -> 8 splits, 160 -> 256 CTAs; 4-layer decode forward -1.0 % at
   // T = 64, -1.5 % at T = 32, neutral at T = 16: profiles/r1/split_sweep.log).
   if (kb >= 192 && best > 1 && best % 4) {
