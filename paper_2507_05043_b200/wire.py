@@ -92,20 +92,20 @@ class DeviceLinkSender(threading.Thread):
             self._cond.notify()
 
     def close(self) -> None:
-        """Flush queued payloads, then send the shutdown frame and stop."""
+        """Stop accepting payloads; the sender thread drains what is queued, posts the
+        end-of-stream frame and exits (wire.py:107-111 semantics)."""
         with self._cond:
             self._closing = True
-            self._cond.notify()
+            self._cond.notify_all()
 
     def _next_chunk(self):
+        """Block until the LinkQueue yields a chunk; False once closed and drained."""
         with self._cond:
-            while True:
-                chunk = self._queue.next_chunk()
-                if chunk is not None:
-                    return chunk
-                if self._closing:
-                    return False
+            chunk = self._queue.next_chunk()
+            while chunk is None and not self._closing:
                 self._cond.wait()
+                chunk = self._queue.next_chunk()
+            return chunk if chunk is not None else False
 
     def _frame(self, payload_id: int, index: int, flags: int, piece: torch.Tensor | None,
                total: int = 0) -> None:
