@@ -1,6 +1,6 @@
 #!/bin/bash
 # chain kernel ring experiments: bigger shared-memory budget, ring splits
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 python -m paper_2507_05043_b200.build > gpurun_out/build.log 2>&1
 declare -A V

@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 python -m paper_2507_05043_b200.build > gpurun_out/build.log 2>&1
 B220="-DCH_BUDGET_KB=220 -DCH_BS16=8 -DCH_BS32=8 -DCH_BS64=6 -DCH_BS128=4 -DCH_BS256=2"

@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 python -m paper_2507_05043_b200.build > gpurun_out/build.log 2>&1
 PL_CHAIN_VERBOSE=1 PL_CHAIN_TRACE=8 timeout 300 python scripts/chain_trace.py gpurun_out/trace_8.npz > gpurun_out/trace_8.log 2>&1
