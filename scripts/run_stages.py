@@ -63,6 +63,7 @@ def main():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--prompt", type=int, default=512)
     ap.add_argument("--decode", type=int, default=256)
+    ap.add_argument("--max-batched", type=int, default=32768, help="controller max_batched_tokens")
     ap.add_argument("--no-links", action="store_true", help="skip the realized link log")
     ap.add_argument("--fuse", action="store_true", help="store decode payloads from the producer's epilogue")
     a = ap.parse_args()
@@ -83,7 +84,7 @@ def main():
     devices = [torch.device("cuda", g) for g in range(G)]
     cluster = deploy.b200_cluster(S)
     plan = deploy.plan(cluster, spec, S)
-    ctrl = PL.ControllerConfig(max_batched_tokens=32768, max_batch_size=a.batch)
+    ctrl = PL.ControllerConfig(max_batched_tokens=a.max_batched, max_batch_size=a.batch)
     cfg = deploy.engine_config(plan, spec, ctrl)
     trace = deploy.uniform_trace(a.batch, a.prompt, a.decode)
     placeholder = [PL.synth_profile(hi - lo, 1e-6, 1e-4, stage_id=i) for i, (_, (lo, hi)) in enumerate(plan.stages)]
