@@ -37,9 +37,9 @@ def _meta_for(exe: StageExecutor, T: int, decode: bool, ctx: int):
         del nb
         return meta, R, 1, ctx
     L = min(T, 512, exe.max_blocks * BLOCK_SIZE)  # prompts must fit the stage's block tables
-    R = max(1, T // L)
-    lens = np.full(R, T // R, dtype=np.int64)
-    lens[-1] += T - lens.sum()
+    R = -(-T // L)  # prompts of L tokens, the last one shorter
+    lens = np.full(R, L, dtype=np.int64)
+    lens[-1] = T - L * (R - 1)
     cu = np.concatenate([[0], np.cumsum(lens)])
     pos = np.arange(T) - np.repeat(cu[:-1], lens)
     rows = (np.arange(R * exe.max_blocks, dtype=np.int64) % max(1, exe.num_blocks)).reshape(R, -1)
@@ -83,7 +83,7 @@ def profile_stage(exe: StageExecutor, decode_points=DECODE_POINTS, prefill_point
             entries[(Phase.DECODE, T)] = round(time_forward(exe, T, True, ctx), 7)
     for T in prefill_points:
         L = min(T, 512, exe.max_blocks * BLOCK_SIZE)
-        if T <= exe.max_tokens and max(1, T // L) <= exe.max_reqs:
+        if T <= exe.max_tokens and -(-T // L) <= exe.max_reqs:
             entries[(Phase.PREFILL, T)] = round(time_forward(exe, T, False, ctx), 7)
     # the reference requires >= 2 monotone points per phase (profiles.py:38-64)
     for ph in (Phase.DECODE, Phase.PREFILL):
