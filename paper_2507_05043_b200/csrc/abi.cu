@@ -243,4 +243,13 @@ int32_t pl_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream)
   return PL_OK;
 }
 
+#ifdef PL_TIMELINE
+// experiment builds only: kernel timeline sink (buf: 2 x u64 per record, count: u32)
+PL_API int32_t pl_timeline_set(void* buf, void* count, uint32_t cap) {
+  int rc = tl_set_gemm(buf, count, cap);
+  if (!rc) rc = tl_set_attn(buf, count, cap);
+  return rc;
+}
+#endif
+
 }  // extern "C"

@@ -407,6 +407,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
   int* last_flag = reinterpret_cast<int*>(smem + L::FLAG);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = args.R * args.Hkv * args.nsplit;
+  if (threadIdx.x == 0) PL_TL(3u << 24, 0);
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmK);
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
       }
       if (lane == 0) {
         pdl_wait();
+        PL_TL(3u << 24, 2);  // predecessor complete
         issue_q(cur);
       }
     }
@@ -554,6 +556,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
 
     for (int i = 0; i < np; ++i) {
       mbar_wait(&full[stage], phase);
+#ifdef PL_TIMELINE
+      if (ct == 0 && i == np - 1 && it + static_cast<int>(gridDim.x) >= n_items) PL_TL(3u << 24, 3);  // last page in
+#endif
       const uint32_t kb = smem_u32(smem + stage * PAGE_BYTES);
       const uint32_t vb = kb + 2 * HALF_TILE;
       float s[4] = {0.f, 0.f, 0.f, 0.f};  // tokens g8, g8+8 x heads 2 t4, 2 t4 + 1
@@ -713,6 +718,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 2)
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");  // red_* reused by the next item
   }
+  if (ct == 0) PL_TL(3u << 24, 1);  // after the final consumer barrier
 }
 
 // Workspace: [o partials | (m, l) partials | ... free ... | arrival counters].  The
@@ -806,6 +812,13 @@ int attn_decode_launch(const __nv_bfloat16* q, int64_t ldq, const __nv_bfloat16*
   return rc;
 }
 
+
+#ifdef PL_TIMELINE
+int tl_set_attn(void* buf, void* count, unsigned cap) {
+  TimelineSink t{static_cast<unsigned long long*>(buf), static_cast<unsigned*>(count), cap};
+  return cudaMemcpyToSymbol(g_tl, &t, sizeof(t)) == cudaSuccess ? PL_OK : PL_ERR_CUDA;
+}
+#endif
 
 // Load every kernel of this file into the context now (lazy module loading would
 // otherwise load it at first launch, which can wait on a spinning NCCL kernel).

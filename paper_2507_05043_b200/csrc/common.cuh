@@ -102,6 +102,33 @@ PL_DEV uint64_t globaltimer_ns() {
   return t;
 }
 
+// Kernel timeline (experiment builds only, -DPL_TIMELINE; scripts/timeline.py): CTAs
+// append (tag | block | event 0 start, 1 end, 2-7 kernel phases; %globaltimer) records to a sink set by
+// pl_timeline_set.  Each translation unit has its own copy of the sink.
+#ifdef PL_TIMELINE
+struct TimelineSink {
+  unsigned long long* buf;
+  unsigned int* count;
+  unsigned int cap;
+};
+static __device__ TimelineSink g_tl;
+PL_DEV void tl_rec(uint32_t tag, uint32_t end) {
+  if (!g_tl.buf) return;
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const unsigned i = atomicAdd(g_tl.count, 1u);
+  if (i < g_tl.cap) {
+    g_tl.buf[2 * i] = (static_cast<uint64_t>(tag) << 32) | (static_cast<uint64_t>(blockIdx.x) << 3) | end;
+    g_tl.buf[2 * i + 1] = t;
+  }
+}
+#define PL_TL(tag, end) ::pl::tl_rec((tag), (end))
+#else
+#define PL_TL(tag, end) \
+  do {                  \
+  } while (0)
+#endif
+
 // Bounded wait: a protocol bug must surface as a launch failure within a few
 // seconds instead of hanging the GPU.
 PL_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {

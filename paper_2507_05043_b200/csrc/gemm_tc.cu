@@ -233,30 +233,70 @@ PL_DEV void csk_reduce(const GemmArgs& args, const uint8_t* smem, int ep, int BN
   const float b1 = args.bias ? bf2f(args.bias[n1]) : 0.f;
   const float b2 = args.bias ? bf2f(args.bias[n2]) : 0.f;
   const bool roped = hh < args.Hq + args.Hkv;
-  for (int c = c_begin + (ep >> 6); c < c_end; c += 2) {
-    const int t = c;
-    const float v1 = rbf(sum_at(c, i) + b1), v2 = rbf(sum_at(c, i + HALF) + b2);
-    float o1 = v1, o2 = v2;
-    if (roped) {
-      int pp = args.pos[t];
-      pp = pp < 0 ? 0 : (pp >= args.max_pos ? args.max_pos - 1 : pp);
-      const float cs = bf2f(args.cos_sin[static_cast<int64_t>(pp) * HDIM + i]);
-      const float sn = bf2f(args.cos_sin[static_cast<int64_t>(pp) * HDIM + HALF + i]);
-      o1 = rbf(rbf(v1 * cs) + rbf(-v2 * sn));
-      o2 = rbf(rbf(v2 * cs) + rbf(v1 * sn));
+  // Columns (tokens) in batches of CB: every global (pos, slot, RoPE table) and DSMEM
+  // load of a batch is issued before the first use, so a batch costs one L2 round trip
+  // instead of two dependent ones per token (at T = 64 the per-token loop kept the qkv
+  // epilogue at ~8 us).
+  constexpr int CB = 4;
+  for (int cb = c_begin + (ep >> 6); cb < c_end; cb += 2 * CB) {
+    int pp[CB], sl[CB];
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      const int c = min(cb + 2 * u, c_end - 1);  // clamped: duplicates are never stored
+#ifdef PL_XP_NOMETA  // timing experiment only (wrong results)
+      pp[u] = c;
+      sl[u] = -1;
+#else
+      pp[u] = roped ? args.pos[c] : 0;
+      sl[u] = args.slot ? args.slot[c] : -1;
+#endif
     }
-    __nv_bfloat16* row = args.C + static_cast<int64_t>(t) * args.ldc;
-    row[n1] = f2bf(o1);
-    row[n2] = f2bf(o2);
-    const int sl = args.slot ? args.slot[t] : -1;
-    if (hh >= args.Hq && sl >= 0) {
-      const bool is_k = roped;
-      const int kh = is_k ? hh - args.Hq : hh - args.Hq - args.Hkv;
-      __nv_bfloat16* cache = is_k ? args.k_cache : args.v_cache;
-      __nv_bfloat16* dst = cache + ((static_cast<int64_t>(sl / args.block_size) * args.Hkv + kh) * args.block_size +
-                                    sl % args.block_size) * HDIM;
-      dst[i] = f2bf(o1);
-      dst[i + HALF] = f2bf(o2);
+    float cs[CB], sn[CB];
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      const int p = pp[u] < 0 ? 0 : (pp[u] >= args.max_pos ? args.max_pos - 1 : pp[u]);
+#ifdef PL_XP_NOMETA
+      cs[u] = 1.f + p;
+      sn[u] = 0.f;
+#else
+      cs[u] = roped ? bf2f(args.cos_sin[static_cast<int64_t>(p) * HDIM + i]) : 0.f;
+      sn[u] = roped ? bf2f(args.cos_sin[static_cast<int64_t>(p) * HDIM + HALF + i]) : 0.f;
+#endif
+    }
+    float x1[CB], x2[CB];
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      const int c = min(cb + 2 * u, c_end - 1);
+#ifdef PL_XP_NODSMEM  // timing experiment only (wrong results)
+      x1[u] = reinterpret_cast<const float*>(smem)[c * BM + i];
+      x2[u] = reinterpret_cast<const float*>(smem)[c * BM + i + HALF];
+#else
+      x1[u] = sum_at(c, i);
+      x2[u] = sum_at(c, i + HALF);
+#endif
+    }
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      const int t = cb + 2 * u;
+      if (t >= c_end) break;
+      const float v1 = rbf(x1[u] + b1), v2 = rbf(x2[u] + b2);
+      float o1 = v1, o2 = v2;
+      if (roped) {
+        o1 = rbf(rbf(v1 * cs[u]) + rbf(-v2 * sn[u]));
+        o2 = rbf(rbf(v2 * cs[u]) + rbf(v1 * sn[u]));
+      }
+      __nv_bfloat16* row = args.C + static_cast<int64_t>(t) * args.ldc;
+      row[n1] = f2bf(o1);
+      row[n2] = f2bf(o2);
+      if (hh >= args.Hq && sl[u] >= 0) {
+        const bool is_k = roped;
+        const int kh = is_k ? hh - args.Hq : hh - args.Hq - args.Hkv;
+        __nv_bfloat16* cache = is_k ? args.k_cache : args.v_cache;
+        __nv_bfloat16* dst = cache + ((static_cast<int64_t>(sl[u] / args.block_size) * args.Hkv + kh) *
+                                          args.block_size + sl[u] % args.block_size) * HDIM;
+        dst[i] = f2bf(o1);
+        dst[i + HALF] = f2bf(o2);
+      }
     }
   }
 }
@@ -363,6 +403,8 @@ __global__ void __launch_bounds__(224, CTAS)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t tl_tag = (1u << 24) | ((static_cast<uint32_t>(args.N) / 128u) << 12) | static_cast<uint32_t>(args.num_kb);
+  if (threadIdx.x == 0) PL_TL(tl_tag, 0);
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
@@ -492,6 +534,7 @@ __global__ void __launch_bounds__(224, CTAS)
       PieceWalk walk;
       walk.init(args);
       Piece pc;
+      bool tl_first = true;
       while (walk.next(args, pc)) {
         const int nkb = pc.nkb;
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -500,6 +543,10 @@ __global__ void __launch_bounds__(224, CTAS)
         for (int i = 0; i < nkb; ++i) {
           mbar_wait(&fullA[sa], pa);
           mbar_wait(&fullB[sb], pb);
+          if (tl_first) {  // first k-block of weights and activations in shared memory
+            PL_TL(tl_tag, 2);
+            tl_first = false;
+          }
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(smem_u32(smem + sa * A_TILE_BYTES));
           const uint64_t db = umma_desc_sw128(smem_u32(smem + L::B_OFFSET + sb * L::B_TILE_BYTES));
@@ -540,6 +587,7 @@ __global__ void __launch_bounds__(224, CTAS)
     while (walk.next(args, pc)) {
       const int m_tile = pc.m_tile, n_tile = pc.n_tile, split = pc.split;
       mbar_wait(&tfull[acc], aphase);
+      if (warp == 2 && lane == 0) PL_TL(tl_tag, 3);  // accumulator complete
       tc_fence_after();
       const uint32_t tcol = tmem + lane_base + acc * BN;
       auto release_tmem = [&]() {  // accumulator drained: hand the TMEM buffer back
@@ -559,17 +607,23 @@ __global__ void __launch_bounds__(224, CTAS)
         // the tile's final epilogue, accumulator values from `fetch(c0, v[16])`
         auto final_epi = [&](auto fetch) {
           if (epi == EPI_SWIGLU && args.swiglu_il) {
-            // interleaved rows: lane pairs (gate_j, up_j) meet by one shuffle, no smem
+            // interleaved rows: lane pairs (gate_j, up_j) meet by one shuffle, no smem;
+            // the pair splits each 16-token chunk (even lane tokens 0-7, odd lane 8-15)
+            // so both lanes evaluate SiLU (the epilogue is instruction-bound: at T = 64 one
+            // lane per pair doing all 64 tokens took ~9 us)
             const int j = m_tile * 64 + (row >> 1);
+            const bool odd = row & 1;
             for (int c0 = 0; c0 < BN; c0 += 16) {
-              float v[16];
+              float v[16], other[16];
               fetch(c0, v);
 #pragma unroll
-              for (int c = 0; c < 16; ++c) {
-                const float other = __shfl_xor_sync(0xffffffffu, v[c], 1);
-                const int t = t_base + c0 + c;
-                if (!(row & 1) && t < args.T)
-                  args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(rbf(v[c]))) * rbf(other));
+              for (int c = 0; c < 16; ++c) other[c] = __shfl_xor_sync(0xffffffffu, v[c], 1);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const float g = odd ? other[k + 8] : v[k];
+                const float u = odd ? v[k + 8] : other[k];
+                const int t = t_base + c0 + k + (odd ? 8 : 0);
+                if (t < args.T) args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(rbf(g))) * rbf(u));
               }
             }
           } else if (epi == EPI_SWIGLU) {
@@ -699,12 +753,16 @@ __global__ void __launch_bounds__(224, CTAS)
   }
 
   if (SWAP && args.csk) {
+    if (threadIdx.x == 64) PL_TL(tl_tag, 4);  // tile parked
     cluster_sync();  // every split's partial tile is parked in its CTA's shared memory
+    if (threadIdx.x == 64) PL_TL(tl_tag, 5);
     if (warp >= 2 && warp <= 5) csk_reduce(args, smem, threadIdx.x - 64, BN);
+    if (threadIdx.x == 64) PL_TL(tl_tag, 6);  // this thread's share reduced
     cluster_sync();  // the peers are done reading this CTA's shared memory
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) PL_TL(tl_tag, 1);
   if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
@@ -954,6 +1012,7 @@ __global__ void __launch_bounds__(1024)
                                 __nv_bfloat16* __restrict__ h, int64_t ldh,
                                 const __nv_bfloat16* __restrict__ w, float eps,
                                 __nv_bfloat16* __restrict__ a, int64_t lda) {
+  if (threadIdx.x == 0) PL_TL(2u << 24, 0);
   pdl_trigger();
   const int t = blockIdx.x;
   const int nt = blockDim.x;
@@ -1036,6 +1095,10 @@ __global__ void __launch_bounds__(1024)
         make_uint2(pack_bf16x2(w0.x * rbf(hv[k][0] * inv), w0.y * rbf(hv[k][1] * inv)),
                    pack_bf16x2(w1.x * rbf(hv[k][2] * inv), w1.y * rbf(hv[k][3] * inv)));
   }
+#ifdef PL_TIMELINE
+  __syncthreads();
+  if (threadIdx.x == 0) PL_TL(2u << 24, 1);
+#endif
 }
 
 // Fused decode epilogue 2: QKV split-K reduce (+ Qwen2 bias) + neox RoPE on q and k
@@ -1432,7 +1495,8 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   a.tiles_m = static_cast<int>(swap ? (N + BM - 1) / BM : (T + BM - 1) / BM);
   const int tiles_n = static_cast<int>(swap ? (T + bn - 1) / bn : (N + bn - 1) / bn);
   a.num_items = a.tiles_m * tiles_n * a.splits;
-  constexpr int raster = 32;  // prefill tile band (profiles/r1/prefill_raster_sweep.log)
+  constexpr int raster = 32;  // prefill tile band (profiles/r1/prefill_raster_sweep.log,
+                              // long-K: profiles/r2/prefill_band_longk.log)
   a.raster_m = (!swap && tiles_n > 1 && a.tiles_m > raster) ? raster : 0;
   a.Tp = tiles_n * bn;
   // split-K: the fused epilogues are the partial reduction kernels
@@ -1573,6 +1637,13 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
   return PL_OK;
 }
 
+
+#ifdef PL_TIMELINE
+int tl_set_gemm(void* buf, void* count, unsigned cap) {
+  TimelineSink t{static_cast<unsigned long long*>(buf), static_cast<unsigned*>(count), cap};
+  return cudaMemcpyToSymbol(g_tl, &t, sizeof(t)) == cudaSuccess ? PL_OK : PL_ERR_CUDA;
+}
+#endif
 
 // Weight packing: W [N, K] (row stride ld) -> 16 KB tiles [N/128][K/64], each tile the
 // exact 128-byte-swizzled shared-memory image TMA would produce for a 128 x 64 box, so

@@ -125,6 +125,11 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
 int pack_weight_launch(const __nv_bfloat16* W, int64_t ld, int64_t N, int64_t K, void* out, cudaStream_t st,
                        bool interleave_swiglu = false);
 
+#ifdef PL_TIMELINE
+int tl_set_gemm(void* buf, void* count, unsigned cap);
+int tl_set_attn(void* buf, void* count, unsigned cap);
+#endif
+
 // per-file eager kernel loading (pl_preload_kernels)
 int attention_preload();
 int kernels_preload();
