@@ -15,7 +15,7 @@ for T in 64 32 16 1; do
   timeout 300 python scripts/profile_decode.py --layers 4 --T $T --ctx 640 --iters 20 --last 0 2>&1 | tail -1 >> $O/layers.log
 done
 done
-for T in 64 16 1; do
+for T in 64 32 1; do
   PL_LIB_PATH=$PWD/$P/_lib_tl/libb200link.so timeout 300 python scripts/timeline.py --layers 4 --T $T --ctx 640 > $O/tl_T$T.log 2>&1
 done
 timeout 600 python bench.py --steps 3 --warmup 3 > $O/bench.log 2>&1
