@@ -195,11 +195,56 @@ PL_DEV void store_out(const GemmArgs& a, int epi, int t, int n, float acc) {
   if (a.C2) a.C2[(int64_t)t * a.ldc + n] = v;  // the next stage's receive buffer (peer memory)
 }
 
+// Cluster split-K QKV epilogue (RoPE + K/V append), vectorised: thread q = ep & 15 owns
+// features [4q, 4q + 4) of both rotary halves of the head, column group g = ep >> 4
+// (0..7) owns token columns c_begin + g + 8u; the splits' DSMEM partials come as 16-byte
+// loads.  The position / RoPE-table / KV-slot metadata of a thread's first CSK_COLS
+// columns is loaded by the epilogue warps while the main loop streams (they are idle
+// then; the predecessor completed at their griddepcontrol.wait) and kept as packed bf16.
+// Against one feature per thread with the metadata loaded after the main loop: -3.8 us
+// per layer at T = 64, -2.5 at T = 32 (profiles/r2/decode/csk_v4_preload_ab.log).
+constexpr int CSK_COLS = 2;
+struct CskMeta {
+  uint2 cs[CSK_COLS], sn[CSK_COLS];  // bf16 x4: cos / sin of features [4q, 4q + 4)
+  int sl[CSK_COLS];
+};
+
+PL_DEV void csk_rope_meta(const GemmArgs& args, int c_end, int f1, bool roped, int cb, uint2* cs, uint2* sn,
+                          int* sl) {
+  constexpr int HDIM = 128, HALF = 64;
+  int pp[CSK_COLS];
+#pragma unroll
+  for (int u = 0; u < CSK_COLS; ++u) {
+    const int c = max(0, min(cb + 8 * u, c_end - 1));  // clamped: duplicates are never stored
+    pp[u] = roped ? args.pos[c] : 0;
+    sl[u] = args.slot ? args.slot[c] : -1;
+  }
+#pragma unroll
+  for (int u = 0; u < CSK_COLS; ++u) {
+    const int p = pp[u] < 0 ? 0 : (pp[u] >= args.max_pos ? args.max_pos - 1 : pp[u]);
+    cs[u] = sn[u] = make_uint2(0, 0);
+    if (roped) {
+      cs[u] = *reinterpret_cast<const uint2*>(args.cos_sin + static_cast<int64_t>(p) * HDIM + f1);
+      sn[u] = *reinterpret_cast<const uint2*>(args.cos_sin + static_cast<int64_t>(p) * HDIM + HALF + f1);
+    }
+  }
+}
+
+PL_DEV void csk_preload(const GemmArgs& args, int ep, int BN, CskMeta& m) {
+  const int s = args.splits;
+  const int rank = static_cast<int>(cluster_ctarank());
+  const int ncols = min(args.T, BN);
+  const int per = (ncols + s - 1) / s;
+  const int c_begin = rank * per, c_end = min(ncols, c_begin + per);
+  const bool roped = static_cast<int>(blockIdx.x) / s < args.Hq + args.Hkv;
+  csk_rope_meta(args, c_end, 4 * (ep & 15), roped, c_begin + (ep >> 4), m.cs, m.sn, m.sl);
+}
+
 // Cluster split-K reduction (SWAP, one weight tile per cluster, cluster rank = split):
 // CTA r finalises token columns [r * per, +per) of the tile, summing the splits' parked
 // partials over DSMEM in split order (the order of gemm_splitk_reduce_kernel /
 // reduce_qkv_rope_kernel, so results are bit-identical to the two-kernel path).
-PL_DEV void csk_reduce(const GemmArgs& args, const uint8_t* smem, int ep, int BN) {
+PL_DEV void csk_reduce(const GemmArgs& args, const uint8_t* smem, int ep, int BN, const CskMeta& pre) {
   const int s = args.splits;
   const int rank = static_cast<int>(cluster_ctarank());
   const int m_tile = static_cast<int>(blockIdx.x) / s;
@@ -228,76 +273,92 @@ PL_DEV void csk_reduce(const GemmArgs& args, const uint8_t* smem, int ep, int BN
   }
   constexpr int HDIM = 128, HALF = 64;
   const int hh = m_tile;  // a 128-feature tile is one q / k / v head
-  const int i = ep & (HALF - 1);
-  const int n1 = hh * HDIM + i, n2 = n1 + HALF;
-  const float b1 = args.bias ? bf2f(args.bias[n1]) : 0.f;
-  const float b2 = args.bias ? bf2f(args.bias[n2]) : 0.f;
-  const bool roped = hh < args.Hq + args.Hkv;
-  // Columns (tokens) in batches of CB: every global (pos, slot, RoPE table) and DSMEM
-  // load of a batch is issued before the first use, so a batch costs one L2 round trip
-  // instead of two dependent ones per token (at T = 64 the per-token loop kept the qkv
-  // epilogue at ~8 us).
-  constexpr int CB = 4;
-  for (int cb = c_begin + (ep >> 6); cb < c_end; cb += 2 * CB) {
-    int pp[CB], sl[CB];
-#pragma unroll
-    for (int u = 0; u < CB; ++u) {
-      const int c = min(cb + 2 * u, c_end - 1);  // clamped: duplicates are never stored
-#ifdef PL_XP_NOMETA  // timing experiment only (wrong results)
-      pp[u] = c;
-      sl[u] = -1;
-#else
-      pp[u] = roped ? args.pos[c] : 0;
-      sl[u] = args.slot ? args.slot[c] : -1;
-#endif
+  {
+    const int q = ep & 15, g = ep >> 4;
+    const int f1 = 4 * q, f2 = HALF + 4 * q;
+    const int n1 = hh * HDIM + f1, n2 = hh * HDIM + f2;
+    float b1[4] = {0.f, 0.f, 0.f, 0.f}, b2[4] = {0.f, 0.f, 0.f, 0.f};
+    if (args.bias) {
+      const uint2 u1 = *reinterpret_cast<const uint2*>(args.bias + n1);
+      const uint2 u2 = *reinterpret_cast<const uint2*>(args.bias + n2);
+      const float2 a0 = unpack_bf16x2(u1.x), a1 = unpack_bf16x2(u1.y);
+      const float2 c0 = unpack_bf16x2(u2.x), c1 = unpack_bf16x2(u2.y);
+      b1[0] = a0.x, b1[1] = a0.y, b1[2] = a1.x, b1[3] = a1.y;
+      b2[0] = c0.x, b2[1] = c0.y, b2[2] = c1.x, b2[3] = c1.y;
     }
-    float cs[CB], sn[CB];
+    const bool roped = hh < args.Hq + args.Hkv;
+    for (int cb = c_begin + g, k = 0; cb < c_end; cb += 8 * CSK_COLS, ++k) {
+      uint2 cs[CSK_COLS], sn[CSK_COLS];
+      int sl[CSK_COLS];
+      if (k == 0) {
 #pragma unroll
-    for (int u = 0; u < CB; ++u) {
-      const int p = pp[u] < 0 ? 0 : (pp[u] >= args.max_pos ? args.max_pos - 1 : pp[u]);
-#ifdef PL_XP_NOMETA
-      cs[u] = 1.f + p;
-      sn[u] = 0.f;
-#else
-      cs[u] = roped ? bf2f(args.cos_sin[static_cast<int64_t>(p) * HDIM + i]) : 0.f;
-      sn[u] = roped ? bf2f(args.cos_sin[static_cast<int64_t>(p) * HDIM + HALF + i]) : 0.f;
-#endif
-    }
-    float x1[CB], x2[CB];
-#pragma unroll
-    for (int u = 0; u < CB; ++u) {
-      const int c = min(cb + 2 * u, c_end - 1);
-#ifdef PL_XP_NODSMEM  // timing experiment only (wrong results)
-      x1[u] = reinterpret_cast<const float*>(smem)[c * BM + i];
-      x2[u] = reinterpret_cast<const float*>(smem)[c * BM + i + HALF];
-#else
-      x1[u] = sum_at(c, i);
-      x2[u] = sum_at(c, i + HALF);
-#endif
-    }
-#pragma unroll
-    for (int u = 0; u < CB; ++u) {
-      const int t = cb + 2 * u;
-      if (t >= c_end) break;
-      const float v1 = rbf(x1[u] + b1), v2 = rbf(x2[u] + b2);
-      float o1 = v1, o2 = v2;
-      if (roped) {
-        o1 = rbf(rbf(v1 * cs[u]) + rbf(-v2 * sn[u]));
-        o2 = rbf(rbf(v2 * cs[u]) + rbf(v1 * sn[u]));
+        for (int u = 0; u < CSK_COLS; ++u) cs[u] = pre.cs[u], sn[u] = pre.sn[u], sl[u] = pre.sl[u];
+      } else {  // T > 16 * splits: later columns load theirs here
+        csk_rope_meta(args, c_end, f1, roped, cb, cs, sn, sl);
       }
-      __nv_bfloat16* row = args.C + static_cast<int64_t>(t) * args.ldc;
-      row[n1] = f2bf(o1);
-      row[n2] = f2bf(o2);
-      if (hh >= args.Hq && sl[u] >= 0) {
-        const bool is_k = roped;
-        const int kh = is_k ? hh - args.Hq : hh - args.Hq - args.Hkv;
-        __nv_bfloat16* cache = is_k ? args.k_cache : args.v_cache;
-        __nv_bfloat16* dst = cache + ((static_cast<int64_t>(sl[u] / args.block_size) * args.Hkv + kh) *
-                                          args.block_size + sl[u] % args.block_size) * HDIM;
-        dst[i] = f2bf(o1);
-        dst[i + HALF] = f2bf(o2);
+      // split-ordered sums (0 + x0 + x1 + ..., the order of reduce_qkv_rope_kernel, so the
+      // result is bit-identical to the two-kernel path), 4 splits' loads per round in flight
+      float4 a1[CSK_COLS], a2[CSK_COLS];
+#pragma unroll
+      for (int u = 0; u < CSK_COLS; ++u) a1[u] = a2[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j0 = 0; j0 < s; j0 += 4) {
+        float4 x1[4][CSK_COLS], x2[4][CSK_COLS];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int u = 0; u < CSK_COLS; ++u) {
+            const int j = min(j0 + jj, s - 1);
+            const int c = min(cb + 8 * u, c_end - 1);
+            const uint32_t addr = mapa_shared(smem, j) + static_cast<uint32_t>((c * BM + f1) * 4);
+            x1[jj][u] = ld_dsmem_f32x4(addr);
+            x2[jj][u] = ld_dsmem_f32x4(addr + HALF * 4);
+          }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+          if (j0 + jj < s)
+#pragma unroll
+            for (int u = 0; u < CSK_COLS; ++u) {
+              a1[u].x += x1[jj][u].x, a1[u].y += x1[jj][u].y, a1[u].z += x1[jj][u].z, a1[u].w += x1[jj][u].w;
+              a2[u].x += x2[jj][u].x, a2[u].y += x2[jj][u].y, a2[u].z += x2[jj][u].z, a2[u].w += x2[jj][u].w;
+            }
+      }
+#pragma unroll
+      for (int u = 0; u < CSK_COLS; ++u) {
+        const int t = cb + 8 * u;
+        if (t >= c_end) break;
+        const float s1[4] = {a1[u].x, a1[u].y, a1[u].z, a1[u].w};
+        const float s2[4] = {a2[u].x, a2[u].y, a2[u].z, a2[u].w};
+        const float2 c01 = unpack_bf16x2(cs[u].x), c23 = unpack_bf16x2(cs[u].y);
+        const float2 n01 = unpack_bf16x2(sn[u].x), n23 = unpack_bf16x2(sn[u].y);
+        const float cv[4] = {c01.x, c01.y, c23.x, c23.y}, sv[4] = {n01.x, n01.y, n23.x, n23.y};
+        float o1[4], o2[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float v1 = rbf(s1[e] + b1[e]), v2 = rbf(s2[e] + b2[e]);
+          o1[e] = v1, o2[e] = v2;
+          if (roped) {
+            const float c_ = cv[e], s_ = sv[e];
+            o1[e] = rbf(rbf(v1 * c_) + rbf(-v2 * s_));
+            o2[e] = rbf(rbf(v2 * c_) + rbf(v1 * s_));
+          }
+        }
+        const uint2 w1 = make_uint2(pack_bf16x2(o1[0], o1[1]), pack_bf16x2(o1[2], o1[3]));
+        const uint2 w2 = make_uint2(pack_bf16x2(o2[0], o2[1]), pack_bf16x2(o2[2], o2[3]));
+        __nv_bfloat16* row = args.C + static_cast<int64_t>(t) * args.ldc;
+        *reinterpret_cast<uint2*>(row + n1) = w1;
+        *reinterpret_cast<uint2*>(row + n2) = w2;
+        if (hh >= args.Hq && sl[u] >= 0) {
+          const bool is_k = roped;
+          const int kh = is_k ? hh - args.Hq : hh - args.Hq - args.Hkv;
+          __nv_bfloat16* cache = is_k ? args.k_cache : args.v_cache;
+          __nv_bfloat16* dst = cache + ((static_cast<int64_t>(sl[u] / args.block_size) * args.Hkv + kh) *
+                                            args.block_size + sl[u] % args.block_size) * HDIM;
+          *reinterpret_cast<uint2*>(dst + f1) = w1;
+          *reinterpret_cast<uint2*>(dst + f2) = w2;
+        }
       }
     }
+    return;
   }
 }
 
@@ -403,6 +464,7 @@ __global__ void __launch_bounds__(224, CTAS)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  CskMeta csk_meta;  // cluster split-K RoPE metadata (epilogue warps)
   const uint32_t tl_tag = (1u << 24) | ((static_cast<uint32_t>(args.N) / 128u) << 12) | static_cast<uint32_t>(args.num_kb);
   if (threadIdx.x == 0) PL_TL(tl_tag, 0);
 
@@ -581,6 +643,7 @@ __global__ void __launch_bounds__(224, CTAS)
     const int epi = args.epi;
     int acc = 0;
     uint32_t aphase = 0;
+    if (SWAP && args.csk && args.rope) csk_preload(args, ep, BN, csk_meta);  // overlaps the main loop
     PieceWalk walk;
     walk.init(args);
     Piece pc;
@@ -756,7 +819,7 @@ __global__ void __launch_bounds__(224, CTAS)
     if (threadIdx.x == 64) PL_TL(tl_tag, 4);  // tile parked
     cluster_sync();  // every split's partial tile is parked in its CTA's shared memory
     if (threadIdx.x == 64) PL_TL(tl_tag, 5);
-    if (warp >= 2 && warp <= 5) csk_reduce(args, smem, threadIdx.x - 64, BN);
+    if (warp >= 2 && warp <= 5) csk_reduce(args, smem, threadIdx.x - 64, BN, csk_meta);
     if (threadIdx.x == 64) PL_TL(tl_tag, 6);  // this thread's share reduced
     cluster_sync();  // the peers are done reading this CTA's shared memory
   }
