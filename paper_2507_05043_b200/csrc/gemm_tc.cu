@@ -251,24 +251,65 @@ PL_DEV void csk_reduce(const GemmArgs& args, const uint8_t* smem, int ep, int BN
   const int ncols = min(args.T, BN);
   const int per = (ncols + s - 1) / s;
   const int c_begin = rank * per, c_end = min(ncols, c_begin + per);
-  uint32_t base[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) base[j] = j < s ? mapa_shared(smem, j) : 0u;
-  auto sum_at = [&](int c, int r) {  // split-ordered sum of element (feature row r, token c)
-    const uint32_t off = static_cast<uint32_t>((c * BM + r) * 4);
-    float x[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = j < s ? ld_dsmem_f32(base[j] + off) : 0.f;
-    float v = 0.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < s) v += x[j];
-    return v;
-  };
   if (!args.rope) {
-    const int n = m_tile * BM + ep;
-    if (n >= args.N) return;
-    for (int c = c_begin; c < c_end; ++c) store_out(args, args.epi, c, n, sum_at(c, ep));
+    // vectorised like the RoPE path: thread q = ep & 31 owns features [4q, 4q + 4) of the
+    // tile, column group g = ep >> 5 owns columns c_begin + g + 4u; residual / bias /
+    // output move as bf16 x4
+    const int q = ep & 31, g = ep >> 5;
+    const int n0 = m_tile * BM + 4 * q;
+    if (n0 >= args.N) return;  // N % 4 == 0 on this path (csk needs tiles_n == 1 and N % 128 == 0)
+    const int epi = args.epi;
+    float bb[4] = {0.f, 0.f, 0.f, 0.f};
+    if (epi == EPI_BIAS) {
+      const uint2 u = *reinterpret_cast<const uint2*>(args.bias + n0);
+      const float2 a0 = unpack_bf16x2(u.x), a1 = unpack_bf16x2(u.y);
+      bb[0] = a0.x, bb[1] = a0.y, bb[2] = a1.x, bb[3] = a1.y;
+    }
+    constexpr int CC = 4;  // columns per batch
+    for (int cb = c_begin + g; cb < c_end; cb += 4 * CC) {
+      uint2 res[CC];
+#pragma unroll
+      for (int u = 0; u < CC; ++u) {
+        const int c = min(cb + 4 * u, c_end - 1);  // clamped: duplicates are never stored
+        res[u] = epi == EPI_RESIDUAL ? *reinterpret_cast<const uint2*>(args.residual + (int64_t)c * args.ldr + n0)
+                                     : make_uint2(0, 0);
+      }
+      float4 acc[CC];
+#pragma unroll
+      for (int u = 0; u < CC; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j0 = 0; j0 < s; j0 += 4) {  // split order, 4 splits' loads per round in flight
+        float4 x[4][CC];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int u = 0; u < CC; ++u) {
+            const int c = min(cb + 4 * u, c_end - 1);
+            x[jj][u] = ld_dsmem_f32x4(mapa_shared(smem, min(j0 + jj, s - 1)) +
+                                      static_cast<uint32_t>((c * BM + 4 * q) * 4));
+          }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+          if (j0 + jj < s)
+#pragma unroll
+            for (int u = 0; u < CC; ++u)
+              acc[u].x += x[jj][u].x, acc[u].y += x[jj][u].y, acc[u].z += x[jj][u].z, acc[u].w += x[jj][u].w;
+      }
+#pragma unroll
+      for (int u = 0; u < CC; ++u) {
+        const int t = cb + 4 * u;
+        if (t >= c_end) break;
+        const float av[4] = {acc[u].x, acc[u].y, acc[u].z, acc[u].w};
+        const float2 r01 = unpack_bf16x2(res[u].x), r23 = unpack_bf16x2(res[u].y);
+        const float rv[4] = {r01.x, r01.y, r23.x, r23.y};
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)  // store_out's rounding points
+          o[e] = epi == EPI_RESIDUAL ? rbf(av[e]) + rv[e] : epi == EPI_BIAS ? av[e] + bb[e] : av[e];
+        const uint2 w = make_uint2(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]));
+        *reinterpret_cast<uint2*>(args.C + (int64_t)t * args.ldc + n0) = w;
+        if (args.C2) *reinterpret_cast<uint2*>(args.C2 + (int64_t)t * args.ldc + n0) = w;
+      }
+    }
     return;
   }
   constexpr int HDIM = 128, HALF = 64;
@@ -1595,7 +1636,12 @@ int gemm_launch(const __nv_bfloat16* X, int64_t ldx, const __nv_bfloat16* W, int
     const bool csk_on = (csk_mask & csk_kind) != 0 && (T > 16 || getenv("PL_CSK"));
     const bool rope_ok = fkind != FUSE_QKV_ROPE ||
                          (N == static_cast<int64_t>(fuse->Hq + 2 * fuse->Hkv) * 128 && fuse->block_size > 0);
-    if (csk_on && swap && a.splits > 1 && a.splits <= 8 && tiles_n == 1 && a.num_items == grid &&
+    // (the cluster epilogues move bf16 x4: 8-byte aligned rows)
+    const bool vec_ok = ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 7) == 0 &&
+                        (epi != EPI_RESIDUAL || (ldr % 4 == 0 && (reinterpret_cast<uintptr_t>(residual) & 7) == 0)) &&
+                        (!a.C2 || (reinterpret_cast<uintptr_t>(a.C2) & 7) == 0) &&
+                        (!bias || (reinterpret_cast<uintptr_t>(bias) & 7) == 0);
+    if (csk_on && vec_ok && swap && a.splits > 1 && a.splits <= 8 && tiles_n == 1 && a.num_items == grid &&
         (epi == EPI_STORE || epi == EPI_BIAS || epi == EPI_RESIDUAL) && rope_ok) {
       a.csk = 1;
       cluster = a.splits;
