@@ -134,6 +134,12 @@ def main():
            "schedule_equal_pipelink": ka == kb, "virtual_span_s": round(span, 4),
            "device_stage_bubbles": bubbles,
            "decisions_n": sorted({d.n_microbatches for _, d in res.decisions}),
+           "decision_counts": {str(n): sum(1 for _, d in res.decisions if d.n_microbatches == n)
+                               for n in sorted({d.n_microbatches for _, d in res.decisions})},
+           # the measured decode tables the controller decided on (ms at T tokens)
+           "stage_decode_profiles_ms": [{str(t): round(v * 1e3, 4) for (ph, t), v in sorted(p.entries.items(),
+                                                                                          key=lambda kv: kv[0][1])
+                                         if ph is PL.Phase.DECODE} for p in eng.stage_profiles],
            "realized_links": link_report or None, "clocks": clk.summary, "wall_s": round(wall, 2),
            "setup_s": round(setup, 1)}
     print(json.dumps(out), flush=True)
