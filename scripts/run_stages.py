@@ -140,6 +140,10 @@ def main():
            "stage_decode_profiles_ms": [{str(t): round(v * 1e3, 4) for (ph, t), v in sorted(p.entries.items(),
                                                                                           key=lambda kv: kv[0][1])
                                          if ph is PL.Phase.DECODE} for p in eng.stage_profiles],
+           # full tables at full precision (scripts/controller_bimodal.py replays them on the CPU)
+           "stage_profiles": [{"layers": p.layers, "entries": [[ph.name, t, v] for (ph, t), v in p.entries.items()]}
+                              for p in eng.stage_profiles],
+           "link_profiles": [[lp.src, lp.dst, lp.latency_s, lp.bandwidth_bps] for lp in eng.link_profiles],
            "realized_links": link_report or None, "clocks": clk.summary, "wall_s": round(wall, 2),
            "setup_s": round(setup, 1)}
     print(json.dumps(out), flush=True)
