@@ -717,17 +717,27 @@ __global__ void __launch_bounds__(224, CTAS)
             // lane per pair doing all 64 tokens took ~9 us)
             const int j = m_tile * 64 + (row >> 1);
             const bool odd = row & 1;
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-              float v[16], other[16];
-              fetch(c0, v);
+            for (int g0 = 0; g0 < BN; g0 += 64) {
+              constexpr int NCH = BN < 64 ? BN / 16 : 4;
+              uint32_t rr[NCH][16];
 #pragma unroll
-              for (int c = 0; c < 16; ++c) other[c] = __shfl_xor_sync(0xffffffffu, v[c], 1);
+              for (int h = 0; h < NCH; ++h) tmem_ld16(tcol + g0 + 16 * h, rr[h]);
+              tmem_ld_wait();  // one wait for up to 64 columns (profiles/r2/decode/epilogue_x4_ab.log)
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const float g = odd ? other[k + 8] : v[k];
-                const float u = odd ? v[k + 8] : other[k];
-                const int t = t_base + c0 + k + (odd ? 8 : 0);
-                if (t < args.T) args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(rbf(g))) * rbf(u));
+              for (int h = 0; h < NCH; ++h) {
+                const int c0 = g0 + 16 * h;
+                float v[16], other[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(rr[h][c]);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) other[c] = __shfl_xor_sync(0xffffffffu, v[c], 1);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  const float g = odd ? other[k + 8] : v[k];
+                  const float u = odd ? v[k + 8] : other[k];
+                  const int t = t_base + c0 + k + (odd ? 8 : 0);
+                  if (t < args.T) args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(rbf(g))) * rbf(u));
+                }
               }
             }
           } else if (epi == EPI_SWIGLU) {
@@ -821,15 +831,20 @@ __global__ void __launch_bounds__(224, CTAS)
           }
         } else if (args.splits > 1 && args.pmode == 1) {
           // feature-contiguous partials [split][T][N] (per-token fused reductions)
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            float v[16];
-            fetch_tmem(c0, v);
+          for (int g0 = 0; g0 < BN; g0 += 64) {
+            constexpr int NCH = BN < 64 ? BN / 16 : 4;
+            uint32_t rr[NCH][16];
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) tmem_ld16(tcol + g0 + 16 * h, rr[h]);
+            tmem_ld_wait();  // one wait for up to 64 columns
             if (n < args.N) {
 #pragma unroll
-              for (int c = 0; c < 16; ++c) {
-                const int t = t_base + c0 + c;
-                if (t < args.T) args.partial[((int64_t)split * args.T + t) * args.N + n] = v[c];
-              }
+              for (int h = 0; h < NCH; ++h)
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                  const int t = t_base + g0 + 16 * h + c;
+                  if (t < args.T) args.partial[((int64_t)split * args.T + t) * args.N + n] = __uint_as_float(rr[h][c]);
+                }
             }
           }
         } else if (args.splits > 1) {
@@ -847,6 +862,7 @@ __global__ void __launch_bounds__(224, CTAS)
         } else {
           final_epi(fetch_tmem);
         }
+        if (!args.csk && warp == 2 && lane == 0) PL_TL(tl_tag, 4);  // this warp's epilogue done
       } else {
         // lane <-> token t, column <-> feature n   (splits == 1 on this path)
         token_rows_epilogue<BN>(args, tcol, m_tile * BM + row, n_tile);
@@ -864,6 +880,7 @@ __global__ void __launch_bounds__(224, CTAS)
     if (threadIdx.x == 64) PL_TL(tl_tag, 6);  // this thread's share reduced
     cluster_sync();  // the peers are done reading this CTA's shared memory
   }
+  if (!args.csk && threadIdx.x == 0) PL_TL(tl_tag, 5);  // weight producer done
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) PL_TL(tl_tag, 1);

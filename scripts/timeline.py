@@ -104,7 +104,7 @@ def main():
           "attention: predecessor complete; p3 = GEMM: accumulator complete / attention: last page in")
     print(f"{'kernel':<12} {'ctas':>5} {'start0':>8} {'startN':>8} {'end0':>8} {'endN':>8} {'span':>7} "
           f"{'vs prev':>8} {'GB/s busy':>9} {'p2 min':>7} {'p2 max':>7} {'p3 min':>7} {'p3 max':>7}  "
-          "(p4-p6: cluster split-K park / sync / reduced)")
+          "(p4-p6: cluster split-K park / sync / reduced; other GEMMs p4 = warp 2 epilogue done, p5 = thread 0 at the final barrier)")
     prev_end = None
     tot = {}
     for r in runs:
