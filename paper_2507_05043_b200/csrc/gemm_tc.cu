@@ -50,8 +50,14 @@
 namespace pl {
 
 constexpr int BK = 64;          // bf16 elements per 128-byte swizzle row
-constexpr int GEMM_THREADS = 224;  // warp 0 weight producer, 1 MMA, 2-5 epilogue, 6 activation producer
+constexpr int GEMM_THREADS = 224;  // pair kernel: warp 0 weight producer, 1 MMA, 2-5 epilogue, 6 activation producer
 constexpr int GEMM_ACT_WARP = 6;
+// gemm_tc_kernel adds warp 7: with warps 0, 1 and 6 (done with their roles by then) it
+// takes the second half of the accumulator columns of a single-item CTA's decode
+// epilogue, two warps per TMEM lane quarter (warp w reads lanes [32 (w % 4), +32))
+// (profiles/r2/decode/epilogue_helpers_ab.log: epilogue phases -1 to -1.5 us per GEMM,
+// -3.5 us per layer at T = 32)
+constexpr int TC_THREADS = 256;
 constexpr int BM = 128;         // MMA M (A-operand rows per CTA)
 constexpr int A_TILE_BYTES = BM * BK * 2;
 
@@ -403,6 +409,67 @@ PL_DEV void csk_reduce(const GemmArgs& args, const uint8_t* smem, int ep, int BN
   }
 }
 
+// Decode (SWAP) epilogues over accumulator columns [c_lo, c_hi) (multiples of 16), two
+// TMEM loads (32 columns) per tcgen05.wait::ld (batched waits:
+// profiles/r2/decode/epilogue_x4_ab.log; 32 keeps the 256-thread kernel within 128 registers).
+// SwiGLU on interleaved rows: lane pairs (gate_j, up_j) meet by one shuffle; the pair
+// splits each 16-token chunk (even lane tokens 0-7, odd lane 8-15) so both lanes evaluate
+// SiLU (instruction-bound: one lane per pair doing all 64 tokens took ~9 us).
+PL_DEV void epi_swiglu_cols(const GemmArgs& args, uint32_t tcol, int row, int m_tile, int t_base, int c_lo,
+                            int c_hi) {
+  const int j = m_tile * 64 + (row >> 1);
+  const bool odd = row & 1;
+  for (int g0 = c_lo; g0 < c_hi; g0 += 32) {
+    const int nch = min(2, (c_hi - g0) / 16);
+    uint32_t rr[2][16];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (h < nch) tmem_ld16(tcol + g0 + 16 * h, rr[h]);
+    tmem_ld_wait();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h >= nch) break;
+      const int c0 = g0 + 16 * h;
+      float v[16], other[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(rr[h][c]);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) other[c] = __shfl_xor_sync(0xffffffffu, v[c], 1);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float g = odd ? other[k + 8] : v[k];
+        const float u = odd ? v[k + 8] : other[k];
+        const int t = t_base + c0 + k + (odd ? 8 : 0);
+        if (t < args.T) args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(rbf(g))) * rbf(u));
+      }
+    }
+  }
+}
+
+// feature-contiguous split-K partials [split][T][N] (per-token fused reductions)
+PL_DEV void epi_partial_cols(const GemmArgs& args, uint32_t tcol, int n, int split, int t_base, int c_lo,
+                             int c_hi) {
+  for (int g0 = c_lo; g0 < c_hi; g0 += 32) {
+    const int nch = min(2, (c_hi - g0) / 16);
+    uint32_t rr[2][16];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (h < nch) tmem_ld16(tcol + g0 + 16 * h, rr[h]);
+    tmem_ld_wait();
+    if (n < args.N) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h >= nch) break;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int t = t_base + g0 + 16 * h + c;
+          if (t < args.T) args.partial[((int64_t)split * args.T + t) * args.N + n] = __uint_as_float(rr[h][c]);
+        }
+      }
+    }
+  }
+}
+
 // !SWAP (prefill) epilogue: TMEM lane <-> token t, accumulator column c <-> feature
 // n_tile * BN + c (split-K is never used on this path).
 template <int BN>
@@ -485,7 +552,7 @@ PL_DEV void token_rows_epilogue(const GemmArgs& args, uint32_t tcol, int t, int 
 }
 
 template <int BN, bool SWAP, int CTAS>
-__global__ void __launch_bounds__(224, CTAS)
+__global__ void __launch_bounds__(TC_THREADS, CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs args) {
   using L = GemmSmem<BN, SWAP, CTAS>;
@@ -506,6 +573,11 @@ __global__ void __launch_bounds__(224, CTAS)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   CskMeta csk_meta;  // cluster split-K RoPE metadata (epilogue warps)
+  // second-half epilogue helpers (warps 0, 1, 6, 7) for single-item CTAs of the two hot
+  // decode epilogues (SwiGLU on interleaved rows, feature-contiguous split-K partials)
+  const bool split_epi = SWAP && BN >= 32 && static_cast<int>(gridDim.x) >= args.num_items && !args.csk &&
+                         ((args.splits > 1 && args.pmode == 1) ||
+                          (args.splits == 1 && args.epi == EPI_SWIGLU && args.swiglu_il));
   const uint32_t tl_tag = (1u << 24) | ((static_cast<uint32_t>(args.N) / 128u) << 12) | static_cast<uint32_t>(args.num_kb);
   if (threadIdx.x == 0) PL_TL(tl_tag, 0);
 
@@ -711,35 +783,7 @@ __global__ void __launch_bounds__(224, CTAS)
         // the tile's final epilogue, accumulator values from `fetch(c0, v[16])`
         auto final_epi = [&](auto fetch) {
           if (epi == EPI_SWIGLU && args.swiglu_il) {
-            // interleaved rows: lane pairs (gate_j, up_j) meet by one shuffle, no smem;
-            // the pair splits each 16-token chunk (even lane tokens 0-7, odd lane 8-15)
-            // so both lanes evaluate SiLU (the epilogue is instruction-bound: at T = 64 one
-            // lane per pair doing all 64 tokens took ~9 us)
-            const int j = m_tile * 64 + (row >> 1);
-            const bool odd = row & 1;
-            for (int g0 = 0; g0 < BN; g0 += 64) {
-              constexpr int NCH = BN < 64 ? BN / 16 : 4;
-              uint32_t rr[NCH][16];
-#pragma unroll
-              for (int h = 0; h < NCH; ++h) tmem_ld16(tcol + g0 + 16 * h, rr[h]);
-              tmem_ld_wait();  // one wait for up to 64 columns (profiles/r2/decode/epilogue_x4_ab.log)
-#pragma unroll
-              for (int h = 0; h < NCH; ++h) {
-                const int c0 = g0 + 16 * h;
-                float v[16], other[16];
-#pragma unroll
-                for (int c = 0; c < 16; ++c) v[c] = __uint_as_float(rr[h][c]);
-#pragma unroll
-                for (int c = 0; c < 16; ++c) other[c] = __shfl_xor_sync(0xffffffffu, v[c], 1);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                  const float g = odd ? other[k + 8] : v[k];
-                  const float u = odd ? v[k + 8] : other[k];
-                  const int t = t_base + c0 + k + (odd ? 8 : 0);
-                  if (t < args.T) args.C[(int64_t)t * args.ldc + j] = f2bf(rbf(silu_f(rbf(g))) * rbf(u));
-                }
-              }
-            }
+            epi_swiglu_cols(args, tcol, row, m_tile, t_base, 0, split_epi ? BN / 2 : BN);
           } else if (epi == EPI_SWIGLU) {
             // rows [0,64) gate, [64,128) up of the same 64 output features
             const int j = m_tile * 64 + (row & 63);
@@ -830,23 +874,7 @@ __global__ void __launch_bounds__(224, CTAS)
             for (int c = 0; c < 16; ++c) red[(c0 + c) * BM + row] = v[c];
           }
         } else if (args.splits > 1 && args.pmode == 1) {
-          // feature-contiguous partials [split][T][N] (per-token fused reductions)
-          for (int g0 = 0; g0 < BN; g0 += 64) {
-            constexpr int NCH = BN < 64 ? BN / 16 : 4;
-            uint32_t rr[NCH][16];
-#pragma unroll
-            for (int h = 0; h < NCH; ++h) tmem_ld16(tcol + g0 + 16 * h, rr[h]);
-            tmem_ld_wait();  // one wait for up to 64 columns
-            if (n < args.N) {
-#pragma unroll
-              for (int h = 0; h < NCH; ++h)
-#pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                  const int t = t_base + g0 + 16 * h + c;
-                  if (t < args.T) args.partial[((int64_t)split * args.T + t) * args.N + n] = __uint_as_float(rr[h][c]);
-                }
-            }
-          }
+          epi_partial_cols(args, tcol, n, split, t_base, 0, split_epi ? BN / 2 : BN);
         } else if (args.splits > 1) {
           // partials are token-contiguous per feature row: [split][N][Tp]
           float* prow = args.partial + ((int64_t)split * args.N + n) * args.Tp + t_base;
@@ -870,6 +898,21 @@ __global__ void __launch_bounds__(224, CTAS)
       release_tmem();
 
     }
+  }
+
+  if (split_epi && (warp <= 1 || warp >= GEMM_ACT_WARP) && static_cast<int>(blockIdx.x) < args.num_items) {
+    const int quarter = warp & 3;  // warps 0, 1, 6, 7 -> TMEM lane quarters 0, 1, 2, 3
+    const int row = quarter * 32 + lane;
+    const int split = static_cast<int>(blockIdx.x) % args.splits;
+    const int m_tile = (static_cast<int>(blockIdx.x) / args.splits) % args.tiles_m;
+    mbar_wait(&tfull[0], 0);  // the single item's accumulator (buffer 0, first phase)
+    tc_fence_after();
+    const uint32_t tcol = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    if (args.pmode == 1 && args.splits > 1)
+      epi_partial_cols(args, tcol, m_tile * BM + row, split, 0, BN / 2, BN);
+    else
+      epi_swiglu_cols(args, tcol, row, m_tile, 0, BN / 2, BN);
+    tc_fence_before();
   }
 
   if (SWAP && args.csk) {
@@ -1492,7 +1535,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, i
   const int rc = ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel<BN, SWAP, CTAS>), smem,
                                   "gemm smem attribute");
   if (rc) return rc;
-  return launch_kc("gemm_tc_kernel", gemm_tc_kernel<BN, SWAP, CTAS>, dim3(grid), dim3(GEMM_THREADS), smem, st, cluster,
+  return launch_kc("gemm_tc_kernel", gemm_tc_kernel<BN, SWAP, CTAS>, dim3(grid), dim3(TC_THREADS), smem, st, cluster,
                    ma, mb, a);
 }
 
