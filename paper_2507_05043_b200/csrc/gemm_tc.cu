@@ -17,10 +17,11 @@
 //   !SWAP (prefill): tokens are the A operand (M = 128 rows), features are N = 256;
 //          at T >= 512 gemm_pair_kernel (CTA pairs, cta_group::2, 256 x 256 tiles).
 //
-// Persistent and warp-specialized (224 threads): warp 0 lane 0 = weight TMA
+// Persistent and warp-specialized (256 threads): warp 0 lane 0 = weight TMA
 // producer, warp 6 lane 0 = activation TMA producer (each runs its smem ring
 // continuously across work items), warp 1 = TMEM allocator + MMA issuer (lane 0),
-// warps 2-5 = epilogue, warp w owning TMEM lanes [32(w%4), +32).  The accumulator
+// warps 2-5 = epilogue, warp w owning TMEM lanes [32(w%4), +32); in a single-item
+// CTA's decode epilogue warps 0, 1, 6 and 7 take the second half of the columns.  The accumulator
 // is double-buffered in TMEM so the epilogue of item i overlaps the main loop of
 // item i+1.  Decode split-K: partials + a reduce kernel, or (cluster split-K) a
 // DSMEM reduction inside the launch.
